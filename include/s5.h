@@ -1,0 +1,130 @@
+/*
+ * s5.h -- C-ABI of libs5.so, the B200 (sm_100a) super scalar string sample
+ * sort (S^5, arXiv 1305.1157).
+ *
+ * The reference package `strsort` is pure Python + numba and has no FFI; its
+ * drop-in boundary is the Python entry-point layer.  Each entry point below
+ * replaces one reference routine (cited file:line, paths relative to
+ * /root/reference/pkg/src/strsort/) and is bound from Python with ctypes by
+ * paper_1305_1157_b200/_lib.py; INTEGRATION.md shows the binding a
+ * maintainer would add to the reference package itself.
+ *
+ * Conventions
+ *  - All pointers named d_* are device pointers (caller-owned, e.g. torch
+ *    tensors' data_ptr()); h_* are host pointers.
+ *  - The arena is the reference's byte arena (strings.py:108-144): strings of
+ *    bytes 1..255 closed by a 0; its last byte must be 0.  The device copy
+ *    must be 8-byte aligned and followed by at least S5_ARENA_PAD readable
+ *    zero bytes (arena_len excludes the padding).
+ *  - Handles are int64 offsets of string starts (strings.py:3-7).
+ *  - Calls are stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream) and return 0 or a negative S5_E* code; s5_last_error()
+ *    returns a thread-local message for the last failure.
+ *  - Arithmetic is integer only (bytes, u32 offsets, u64 keys, i64 outputs).
+ */
+#ifndef S5_H_
+#define S5_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define S5_ARENA_PAD 64
+
+enum {
+    S5_OK = 0,
+    S5_E_INVALID = -1,   /* bad argument: unterminated arena, bad v, ... (ValueError) */
+    S5_E_CUDA = -2,      /* CUDA runtime error (RuntimeError)                          */
+    S5_E_WORKSPACE = -3, /* workspace too small                                        */
+    S5_E_RANGE = -4,     /* handle outside the arena / arena >= 4 GiB / n >= 2^31      */
+    S5_E_INTERNAL = -5,  /* internal capacity exceeded (bug)                           */
+    S5_E_NCCL = -6       /* NCCL error (multi-GPU entry points)                        */
+};
+
+/* SampleSortConfig (samplesort.py:37-45) plus the GPU tiering knobs.
+ * Zero fields take defaults. */
+typedef struct {
+    uint32_t v;           /* max splitters per step, 2^d-1 (default 8191)       */
+    uint32_t alpha;       /* oversampling factor (default 2)                    */
+    uint32_t classifier;  /* 0 = "unroll", 1 = "equal" (samplesort.py:43)      */
+    uint32_t small_max;   /* segments <= small_max: warp base case (<= 32)      */
+    uint32_t narrow_max;  /* segments <= narrow_max: one-CTA S^5 step (<=16384) */
+    uint32_t flags;       /* bit0: skip LCP fix-up (debug)                      */
+    uint64_t seed;        /* sample seed (samplesort.py:45)                     */
+} s5_config;
+
+/* Per-call statistics (Counters, counters.py:8-37; SURVEY 8(d) n_p log). */
+#define S5_MAX_LEVELS 128
+typedef struct {
+    uint32_t levels;                     /* level-synchronous passes run          */
+    uint32_t pad_;
+    uint64_t n_per_pass[S5_MAX_LEVELS];  /* strings moved in pass p (n_p)         */
+    uint64_t wide_elems[S5_MAX_LEVELS];  /* of which in multi-CTA S^5 steps       */
+    uint64_t narrow_elems[S5_MAX_LEVELS];/* of which in one-CTA S^5 steps         */
+    uint64_t small_elems[S5_MAX_LEVELS]; /* of which in warp base-case sorts      */
+    uint64_t wide_steps;                 /* S^5 steps over >narrow_max segments   */
+    uint64_t narrow_steps;               /* one-CTA S^5 steps                     */
+    uint64_t small_segments;             /* base-case segments                    */
+    uint64_t key_fetches;                /* arena key gathers (fetches counter)   */
+    uint64_t boundary_lcps;              /* LCPs finished by the boundary kernel  */
+    float ms_total;                      /* device time of the call (CUDA events) */
+    float pad2_;
+} s5_stats;
+
+/* Bytes of device workspace s5_sort needs for n strings. */
+uint64_t s5_workspace_bytes(uint64_t n, uint64_t arena_len, const s5_config *cfg);
+
+/* parallel_sample_sort (samplesort.py:437-444) / sample_sort (:241-267):
+ * permutes d_handles[0..n) in place into sorted order and, if d_lcp is not
+ * NULL, writes the LCP array d_lcp[0..n-1) exactly as _adjacent_lcps
+ * (strings.py:99-102) defines it.  `depth` is the common prefix every
+ * string is known to share (sample_sort's depth argument). */
+int s5_sort(const uint8_t *d_arena, uint64_t arena_len, int64_t *d_handles, uint64_t n,
+            uint64_t depth, int64_t *d_lcp, const s5_config *cfg, void *d_workspace,
+            uint64_t workspace_bytes, void *stream, s5_stats *stats);
+
+/* Same with host buffers: uploads handles, sorts, downloads handles + LCP.
+ * The arena must already be on the device (d_arena). Allocates its own
+ * device buffers (cached between calls). */
+int s5_sort_host(const uint8_t *d_arena, uint64_t arena_len, int64_t *h_handles, uint64_t n,
+                 int64_t *h_lcp, const s5_config *cfg, void *stream, s5_stats *stats);
+
+/* pack_keys (strings.py:176-182) / _pack_keys (:50-53). */
+int s5_pack_keys(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_handles,
+                 uint64_t n, uint64_t depth, uint64_t *d_keys, void *stream);
+
+/* _adjacent_lcps (strings.py:99-102): d_lcp[i] = lcp(s[i], s[i+1]). */
+int s5_adjacent_lcp(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_sorted,
+                    uint64_t n, int64_t *d_lcp, void *stream);
+
+/* _first_unsorted (strings.py:77-82) on the device: writes the first i with
+ * s[i] > s[i+1] (or -1) to *d_result. */
+int s5_first_unsorted(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_handles,
+                      uint64_t n, int64_t *d_result, void *stream);
+
+/* classify_tree_unrolled / classify_tree_equal (classifier.py:259-278):
+ * buckets of n keys against v = 2^d-1 sorted splitters (in-order). */
+int s5_classify(const uint64_t *d_keys, uint64_t n, const uint64_t *d_in_order, uint32_t v,
+                uint32_t classifier, uint16_t *d_buckets, void *stream);
+
+/* select_splitters + build_tree (classifier.py:85-176) on the device, the
+ * path the sort uses: from a sorted sample of m keys, v splitters in level
+ * order (d_level_order[v+1], slot 0 unused) and in order (d_in_order[v]). */
+int s5_build_tree(const uint64_t *d_sorted_sample, uint32_t m, uint32_t v,
+                  uint64_t *d_level_order, uint64_t *d_in_order, void *stream);
+
+/* Host helper for the config-5 generator: order-2 Markov text over sigma
+ * symbols from cumulative rows cdf[sigma][sigma][sigma] and uniforms u[n]
+ * (SURVEY 8(d) recipe 5). */
+int s5_host_markov_text(const double *cdf, const double *u, uint64_t n, uint32_t sigma,
+                        uint8_t *out);
+
+const char *s5_last_error(void);
+int s5_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* S5_H_ */

@@ -1,0 +1,121 @@
+"""ctypes binding of libs5.so (C-ABI declared in include/s5.h).
+
+There is no fallback: if the shared library is missing or fails to load, every
+entry point raises.  ``build()`` compiles it in-tree with nvcc for sm_100a.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libs5.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+S5_ARENA_PAD = 64
+S5_MAX_LEVELS = 128
+
+ERRORS = {
+    -1: ValueError,       # S5_E_INVALID
+    -2: RuntimeError,     # S5_E_CUDA
+    -3: RuntimeError,     # S5_E_WORKSPACE
+    -4: ValueError,       # S5_E_RANGE
+    -5: RuntimeError,     # S5_E_INTERNAL
+    -6: RuntimeError,     # S5_E_NCCL
+}
+
+
+class S5Config(C.Structure):
+    _fields_ = [("v", C.c_uint32), ("alpha", C.c_uint32), ("classifier", C.c_uint32),
+                ("small_max", C.c_uint32), ("narrow_max", C.c_uint32), ("flags", C.c_uint32),
+                ("seed", C.c_uint64)]
+
+
+class S5Stats(C.Structure):
+    _fields_ = [("levels", C.c_uint32), ("pad_", C.c_uint32),
+                ("n_per_pass", C.c_uint64 * S5_MAX_LEVELS),
+                ("wide_elems", C.c_uint64 * S5_MAX_LEVELS),
+                ("narrow_elems", C.c_uint64 * S5_MAX_LEVELS),
+                ("small_elems", C.c_uint64 * S5_MAX_LEVELS),
+                ("wide_steps", C.c_uint64), ("narrow_steps", C.c_uint64),
+                ("small_segments", C.c_uint64), ("key_fetches", C.c_uint64),
+                ("boundary_lcps", C.c_uint64), ("ms_total", C.c_float), ("pad2_", C.c_float)]
+
+    def as_dict(self) -> dict:
+        L = min(self.levels, S5_MAX_LEVELS)
+        return {
+            "levels": int(self.levels),
+            "n_per_pass": [int(x) for x in self.n_per_pass[:L]],
+            "wide_elems": [int(x) for x in self.wide_elems[:L]],
+            "narrow_elems": [int(x) for x in self.narrow_elems[:L]],
+            "small_elems": [int(x) for x in self.small_elems[:L]],
+            "wide_steps": int(self.wide_steps), "narrow_steps": int(self.narrow_steps),
+            "small_segments": int(self.small_segments), "key_fetches": int(self.key_fetches),
+            "boundary_lcps": int(self.boundary_lcps), "ms_total": float(self.ms_total),
+        }
+
+
+_vp = C.c_void_p
+_u64 = C.c_uint64
+_u32 = C.c_uint32
+
+SIGNATURES = {
+    "s5_workspace_bytes": (_u64, [_u64, _u64, C.POINTER(S5Config)]),
+    "s5_sort": (C.c_int, [_vp, _u64, _vp, _u64, _u64, _vp, C.POINTER(S5Config), _vp, _u64, _vp,
+                          C.POINTER(S5Stats)]),
+    "s5_sort_host": (C.c_int, [_vp, _u64, _vp, _u64, _vp, C.POINTER(S5Config), _vp,
+                               C.POINTER(S5Stats)]),
+    "s5_pack_keys": (C.c_int, [_vp, _u64, _vp, _u64, _u64, _vp, _vp]),
+    "s5_adjacent_lcp": (C.c_int, [_vp, _u64, _vp, _u64, _vp, _vp]),
+    "s5_first_unsorted": (C.c_int, [_vp, _u64, _vp, _u64, _vp, _vp]),
+    "s5_classify": (C.c_int, [_vp, _u64, _vp, _u32, _u32, _vp, _vp]),
+    "s5_build_tree": (C.c_int, [_vp, _u32, _u32, _vp, _vp, _vp]),
+    "s5_host_markov_text": (C.c_int, [_vp, _vp, _u64, _u32, _vp]),
+    "s5_last_error": (C.c_char_p, []),
+    "s5_version": (C.c_int, []),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile libs5.so in-tree (nvcc -gencode arch=compute_100a,code=sm_100a)."""
+    cmd = ["make", "-s", "-C", CSRC]
+    if force:
+        cmd.insert(1, "-B")
+    subprocess.run(cmd, check=True)
+    return SO_PATH
+
+
+def lib():
+    """The loaded library; raises if it is absent (no CPU fallback exists)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(SO_PATH):
+                    raise ImportError(
+                        f"{SO_PATH} is missing: build it with paper_1305_1157_b200._lib.build() "
+                        "(nvcc, sm_100a); there is no CPU fallback")
+                L = C.CDLL(SO_PATH)
+                for name, (res, args) in SIGNATURES.items():
+                    fn = getattr(L, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = L
+    return _lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().s5_last_error().decode(errors="replace")
+        raise ERRORS.get(rc, RuntimeError)(f"{what}: {msg} (code {rc})")
+
+
+def current_stream_ptr():
+    import torch
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)

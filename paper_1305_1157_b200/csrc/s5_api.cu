@@ -1,0 +1,441 @@
+// s5_api.cu -- host driver and C-ABI of libs5.so (see include/s5.h).
+//
+// The driver replaces the reference's recursion over SortJobs
+// (samplesort.py:273-434, scheduler.py) with level-synchronous device
+// segment lists: every level launches the wide pipeline, the fused narrow
+// kernel and the warp base case over all live segments at once, and reads
+// back only the next level's list counters (one 64-byte D2H per level).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstddef>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/s5.h"
+#include "s5_kernels.cuh"
+
+using namespace s5;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define S5_CUDA(call)                                                                  \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            return fail(S5_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));    \
+    } while (0)
+
+struct Cfg {
+    uint32_t v, alpha, classifier, small_max, narrow_max, flags, dmax;
+    uint64_t seed;
+};
+
+int resolve(const s5_config* c, Cfg* o) {
+    o->v = c && c->v ? c->v : 8191;
+    o->alpha = c && c->alpha ? c->alpha : 2;
+    o->classifier = c ? c->classifier : 0;
+    o->small_max = c && c->small_max ? c->small_max : 32;
+    o->narrow_max = c && c->narrow_max ? c->narrow_max : kNarrowMaxSize;
+    o->flags = c ? c->flags : 0;
+    o->seed = c ? c->seed : 1;
+    uint32_t d = 0;
+    while (d < 31 && ((1u << d) - 1) < o->v) ++d;
+    if (o->v < 1 || ((1u << d) - 1) != o->v)
+        return fail(S5_E_INVALID, "need 2**d - 1 splitters, got v=%u", o->v);
+    o->dmax = d;
+    if (o->classifier > 1) return fail(S5_E_INVALID, "classifier must be 0 (unroll) or 1 (equal)");
+    if (o->small_max < 1 || o->small_max > 32)
+        return fail(S5_E_INVALID, "small_max must be in [1, 32]");
+    if (o->narrow_max < o->small_max || o->narrow_max > kNarrowMaxSize)
+        return fail(S5_E_INVALID, "narrow_max must be in [small_max, %u]", kNarrowMaxSize);
+    if (o->alpha > 64) return fail(S5_E_INVALID, "alpha must be <= 64");
+    return 0;
+}
+
+uint64_t align_up(uint64_t x, uint64_t a = 256) { return (x + a - 1) / a * a; }
+
+struct Layout {
+    uint64_t off[2], key[2], lists[2][3], cta_start, tree_off, hist_off, tree_pool, hist_pool,
+        ctl, total;
+    uint32_t cap[3];
+    uint64_t tree_cap, hist_cap;
+};
+
+Layout make_layout(uint64_t n, const Cfg& c) {
+    Layout L{};
+    uint64_t at = 0;
+    auto take = [&](uint64_t bytes) {
+        uint64_t p = at;
+        at = align_up(at + bytes);
+        return p;
+    };
+    L.cap[SMALL] = static_cast<uint32_t>(n / 2 + 1);
+    L.cap[NARROW] = static_cast<uint32_t>(n / (c.small_max + 1) + 1);
+    L.cap[WIDE] = static_cast<uint32_t>(n / (c.narrow_max + 1) + 1);
+    for (int s = 0; s < 2; ++s) L.off[s] = take(n * 4);
+    for (int s = 0; s < 2; ++s) L.key[s] = take(n * 8);
+    for (int b = 0; b < 2; ++b)
+        for (int q = 0; q < 3; ++q) L.lists[b][q] = take(uint64_t(L.cap[q]) * sizeof(Seg));
+    L.cta_start = take((uint64_t(L.cap[WIDE]) + 1) * 4);
+    L.tree_off = take(uint64_t(L.cap[WIDE]) * 8);
+    L.hist_off = take(uint64_t(L.cap[WIDE]) * 8);
+    // wide segments have > narrow_max strings; v+1 <= size/8, and at most
+    // ceil(size/64K) <= 296 rows of k <= size/4 counters (see choose_d)
+    L.tree_cap = n / 8 + uint64_t(L.cap[WIDE]) * 2 + 16;
+    L.hist_cap = n + n / 2 + 3 * uint64_t(L.cap[WIDE]) + 65536;
+    L.tree_pool = take(L.tree_cap * 8);
+    L.hist_pool = take(L.hist_cap * 4);
+    L.ctl = take(sizeof(Ctl));
+    L.total = at;
+    return L;
+}
+
+template <typename K>
+int set_smem(K kernel, int bytes) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess)
+        return fail(S5_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
+    return 0;
+}
+
+constexpr int kWideTreeSmem = kWideSampleCap * 8 + (1 << kWideDMax) * 12;
+constexpr int kWideSmem = (1 << kWideDMax) * 8 + ((2 << kWideDMax) + 2) * 4;
+
+int init_attributes() {
+    static std::once_flag once;
+    static int rc = 0;
+    std::call_once(once, [] {
+        rc = set_smem(k_narrow<false>, NarrowSmem::total);
+        if (!rc) rc = set_smem(k_narrow<true>, NarrowSmem::total);
+        if (!rc) rc = set_smem(k_wide_tree, kWideTreeSmem);
+        if (!rc) rc = set_smem(k_wide_count<false>, kWideSmem);
+        if (!rc) rc = set_smem(k_wide_count<true>, kWideSmem);
+        if (!rc) rc = set_smem(k_wide_scatter<false>, kWideSmem);
+        if (!rc) rc = set_smem(k_wide_scatter<true>, kWideSmem);
+        if (!rc) rc = set_smem(k_build_tree, 227 * 1024);
+    });
+    return rc;
+}
+
+struct Pinned {
+    Ctl* ctl = nullptr;
+    long long* ll = nullptr;
+};
+
+Pinned& pinned() {
+    thread_local Pinned p;
+    if (!p.ctl) {
+        cudaHostAlloc(&p.ctl, sizeof(Ctl), cudaHostAllocDefault);
+        cudaHostAlloc(&p.ll, 64, cudaHostAllocDefault);
+    }
+    return p;
+}
+
+int grid_for(uint64_t n, int threads, int max_blocks = 148 * 16) {
+    uint64_t b = (n + threads - 1) / threads;
+    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(b, max_blocks)));
+}
+
+}  // namespace
+
+extern "C" {
+
+int s5_version(void) { return 1; }
+
+const char* s5_last_error(void) { return g_err.c_str(); }
+
+uint64_t s5_workspace_bytes(uint64_t n, uint64_t arena_len, const s5_config* cfg) {
+    (void)arena_len;
+    Cfg c;
+    if (resolve(cfg, &c)) return 0;
+    return make_layout(n, c).total;
+}
+
+int s5_sort(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles, uint64_t n,
+            uint64_t depth, int64_t* d_lcp, const s5_config* cfg, void* d_ws, uint64_t ws_bytes,
+            void* stream_, s5_stats* stats) {
+    Cfg c;
+    if (int rc = resolve(cfg, &c)) return rc;
+    if (stats) memset(stats, 0, sizeof(*stats));
+    if (n <= 1) return 0;
+    if (!d_arena || !d_handles) return fail(S5_E_INVALID, "null arena or handles");
+    if (reinterpret_cast<uintptr_t>(d_arena) % 8)
+        return fail(S5_E_INVALID, "device arena must be 8-byte aligned");
+    if (arena_len == 0) return fail(S5_E_INVALID, "empty arena with n > 1 handles");
+    if (arena_len >= (1ull << 32))
+        return fail(S5_E_RANGE, "arena of %llu bytes: offsets are 32-bit (< 4 GiB)",
+                    (unsigned long long)arena_len);
+    if (n >= (1ull << 31)) return fail(S5_E_RANGE, "n must be < 2^31");
+    if (depth >= arena_len) return fail(S5_E_RANGE, "depth beyond arena");
+    Layout L = make_layout(n, c);
+    if (!d_ws || ws_bytes < L.total)
+        return fail(S5_E_WORKSPACE, "workspace of %llu bytes, need %llu",
+                    (unsigned long long)ws_bytes, (unsigned long long)L.total);
+    if (int rc = init_attributes()) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream_);
+    char* ws = static_cast<char*>(d_ws);
+    Pinned& hp = pinned();
+    if (!hp.ctl) return fail(S5_E_CUDA, "pinned host allocation failed");
+
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (stats) {
+        S5_CUDA(cudaEventCreate(&ev0));
+        S5_CUDA(cudaEventCreate(&ev1));
+        S5_CUDA(cudaEventRecord(ev0, st));
+    }
+
+    SortArgs A{};
+    A.arena = d_arena;
+    for (int s = 0; s < 2; ++s) {
+        A.off[s] = reinterpret_cast<uint32_t*>(ws + L.off[s]);
+        A.key[s] = reinterpret_cast<uint64_t*>(ws + L.key[s]);
+    }
+    A.out = d_handles;
+    A.lcp = d_lcp;
+    for (int q = 0; q < 3; ++q) A.cap[q] = L.cap[q];
+    A.ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
+    A.small_max = c.small_max;
+    A.narrow_max = c.narrow_max;
+    A.dmax = c.dmax;
+    A.alpha = c.alpha;
+    A.seed = c.seed;
+
+    WidePlan P{};
+    P.cta_start = reinterpret_cast<uint32_t*>(ws + L.cta_start);
+    P.tree_off = reinterpret_cast<uint64_t*>(ws + L.tree_off);
+    P.hist_off = reinterpret_cast<uint64_t*>(ws + L.hist_off);
+    P.tree_pool = reinterpret_cast<uint64_t*>(ws + L.tree_pool);
+    P.hist_pool = reinterpret_cast<uint32_t*>(ws + L.hist_pool);
+    P.tree_cap = L.tree_cap;
+    P.hist_cap = L.hist_cap;
+
+    // level 0: cached keys at the common depth, root segment
+    int cur = 0;
+    for (int q = 0; q < 3; ++q) A.next[q] = reinterpret_cast<Seg*>(ws + L.lists[cur][q]);
+    S5_CUDA(cudaMemsetAsync(A.ctl, 0, sizeof(Ctl), st));
+    k_gather<<<grid_for(n, 256), 256, 0, st>>>(d_handles, static_cast<uint32_t>(n), depth,
+                                                arena_len, A);
+    k_init_root<<<1, 32, 0, st>>>(A, static_cast<uint32_t>(n), static_cast<uint32_t>(depth));
+    S5_CUDA(cudaGetLastError());
+
+    unsigned long long fetches_total = 0, hints_total = 0;
+    uint32_t level = 0;
+    for (;; ++level) {
+        S5_CUDA(cudaMemcpyAsync(hp.ctl, A.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        S5_CUDA(cudaStreamSynchronize(st));
+        Ctl h = *hp.ctl;
+        if (h.err & ERR_RANGE) return fail(S5_E_RANGE, "handle outside the arena");
+        if (h.err & ERR_LIST) return fail(S5_E_INTERNAL, "segment list overflow");
+        if (h.err & ERR_POOL) return fail(S5_E_INTERNAL, "wide pool overflow");
+        fetches_total = h.fetches;
+        hints_total = h.hints;
+        uint32_t m[3] = {h.n_list[0], h.n_list[1], h.n_list[2]};
+        if (!m[0] && !m[1] && !m[2]) break;
+        if (level >= 100000) return fail(S5_E_INTERNAL, "no progress");
+        if (stats && level < S5_MAX_LEVELS) {
+            stats->wide_elems[level] = h.elems[WIDE];
+            stats->narrow_elems[level] = h.elems[NARROW];
+            stats->small_elems[level] = h.elems[SMALL];
+            stats->n_per_pass[level] = h.elems[0] + h.elems[1] + h.elems[2];
+            stats->wide_steps += m[WIDE];
+            stats->narrow_steps += m[NARROW];
+            stats->small_segments += m[SMALL];
+        }
+        // swap lists: this level reads `cur`, emits into the other
+        const Seg* segs[3];
+        for (int q = 0; q < 3; ++q) segs[q] = reinterpret_cast<const Seg*>(ws + L.lists[cur][q]);
+        cur ^= 1;
+        for (int q = 0; q < 3; ++q) A.next[q] = reinterpret_cast<Seg*>(ws + L.lists[cur][q]);
+        S5_CUDA(cudaMemsetAsync(A.ctl, 0, offsetof(Ctl, fetches), st));
+
+        if (m[WIDE]) {
+            P.segs = segs[WIDE];
+            P.nsegs = m[WIDE];
+            k_wide_plan<<<1, 1024, 0, st>>>(A, P);
+            k_wide_tree<<<m[WIDE], kWideThreads, kWideTreeSmem, st>>>(A, P);
+            // upper bound on CTAs; surplus CTAs exit on ctl->wide_ctas
+            uint32_t ub = static_cast<uint32_t>(std::min<uint64_t>(
+                uint64_t(m[WIDE]) * kWideCtasMax, n / kWideChunkMin + m[WIDE]));
+            if (c.classifier)
+                k_wide_count<true><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
+            else
+                k_wide_count<false><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
+            dim3 cg(m[WIDE], ((2u << std::min(c.dmax, kWideDMax)) + 1023) / 1024);
+            k_wide_colscan<<<cg, 1024, 0, st>>>(A, P);
+            k_wide_bscan<<<m[WIDE], 1024, 0, st>>>(A, P);
+            if (c.classifier)
+                k_wide_scatter<true><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
+            else
+                k_wide_scatter<false><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
+        }
+        if (m[NARROW]) {
+            if (c.classifier)
+                k_narrow<true><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
+            else
+                k_narrow<false><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
+        }
+        if (m[SMALL]) {
+            uint32_t blocks = (m[SMALL] + 7) / 8;
+            k_small<<<blocks, 256, 0, st>>>(A, segs[SMALL], m[SMALL]);
+        }
+        S5_CUDA(cudaGetLastError());
+    }
+    if (d_lcp && !(c.flags & 1)) {
+        k_lcp_fix<<<grid_for(n - 1, 256), 256, 0, st>>>(d_arena, d_handles, d_lcp, n - 1);
+        S5_CUDA(cudaGetLastError());
+    }
+    if (stats) {
+        S5_CUDA(cudaEventRecord(ev1, st));
+        S5_CUDA(cudaEventSynchronize(ev1));
+        S5_CUDA(cudaEventElapsedTime(&stats->ms_total, ev0, ev1));
+        cudaEventDestroy(ev0);
+        cudaEventDestroy(ev1);
+        stats->levels = level;
+        stats->key_fetches = fetches_total;
+        stats->boundary_lcps = hints_total;
+    }
+    return 0;
+}
+
+int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles, uint64_t n,
+                 int64_t* h_lcp, const s5_config* cfg, void* stream_, s5_stats* stats) {
+    static std::mutex mu;
+    static void* buf = nullptr;
+    static uint64_t buf_bytes = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    if (n <= 1) {
+        if (stats) memset(stats, 0, sizeof(*stats));
+        return 0;
+    }
+    Cfg c;
+    if (int rc = resolve(cfg, &c)) return rc;
+    uint64_t ws = make_layout(n, c).total;
+    uint64_t need = align_up(n * 8) + align_up(n * 8) + ws;
+    if (need > buf_bytes) {
+        if (buf) cudaFree(buf);
+        buf = nullptr;
+        buf_bytes = 0;
+        S5_CUDA(cudaMalloc(&buf, need));
+        buf_bytes = need;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream_);
+    int64_t* dh = static_cast<int64_t*>(buf);
+    int64_t* dl = reinterpret_cast<int64_t*>(static_cast<char*>(buf) + align_up(n * 8));
+    void* dws = static_cast<char*>(buf) + 2 * align_up(n * 8);
+    S5_CUDA(cudaMemcpyAsync(dh, h_handles, n * 8, cudaMemcpyHostToDevice, st));
+    int rc = s5_sort(d_arena, arena_len, dh, n, 0, h_lcp ? dl : nullptr, cfg, dws, ws, stream_,
+                     stats);
+    if (rc) return rc;
+    S5_CUDA(cudaMemcpyAsync(h_handles, dh, n * 8, cudaMemcpyDeviceToHost, st));
+    if (h_lcp) S5_CUDA(cudaMemcpyAsync(h_lcp, dl, (n - 1) * 8, cudaMemcpyDeviceToHost, st));
+    S5_CUDA(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int s5_pack_keys(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_handles,
+                 uint64_t n, uint64_t depth, uint64_t* d_keys, void* stream) {
+    (void)arena_len;
+    if (!n) return 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_pack_keys<<<grid_for(n, 256), 256, 0, st>>>(d_arena, d_handles, n, depth, d_keys);
+    S5_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int s5_adjacent_lcp(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_sorted,
+                    uint64_t n, int64_t* d_lcp, void* stream) {
+    (void)arena_len;
+    if (n <= 1) return 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_adjacent_lcp<<<grid_for(n - 1, 256), 256, 0, st>>>(d_arena, d_sorted, n - 1, d_lcp);
+    S5_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int s5_first_unsorted(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_handles,
+                      uint64_t n, int64_t* d_result, void* stream) {
+    (void)arena_len;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    S5_CUDA(cudaMemsetAsync(d_result, 0xFF, 8, st));  // -1 == ULLONG_MAX
+    if (n <= 1) return 0;
+    k_first_unsorted<<<grid_for(n - 1, 256), 256, 0, st>>>(
+        d_arena, d_handles, n - 1, reinterpret_cast<unsigned long long*>(d_result));
+    S5_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int s5_classify(const uint64_t* d_keys, uint64_t n, const uint64_t* d_in_order, uint32_t v,
+                uint32_t classifier, uint16_t* d_buckets, void* stream) {
+    uint32_t d = 0;
+    while (d < 31 && ((1u << d) - 1) < v) ++d;
+    if (v < 1 || ((1u << d) - 1) != v || d > kWideDMax)
+        return fail(S5_E_INVALID, "need 2**d - 1 splitters (d <= %u), got %u", kWideDMax, v);
+    if (!n) return 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int smem = (1 << d) * 8;
+    if (smem > 48 * 1024) {
+        if (int rc = set_smem(k_classify<false>, smem)) return rc;
+        if (int rc = set_smem(k_classify<true>, smem)) return rc;
+    }
+    if (classifier)
+        k_classify<true><<<grid_for(n, 256, 296), 256, smem, st>>>(d_keys, n, d_in_order, d, d_buckets);
+    else
+        k_classify<false><<<grid_for(n, 256, 296), 256, smem, st>>>(d_keys, n, d_in_order, d, d_buckets);
+    S5_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int s5_build_tree(const uint64_t* d_sorted_sample, uint32_t m, uint32_t v,
+                  uint64_t* d_level_order, uint64_t* d_in_order, void* stream) {
+    uint32_t d = 0;
+    while (d < 31 && ((1u << d) - 1) < v) ++d;
+    if (v < 1 || ((1u << d) - 1) != v || d > kWideDMax)
+        return fail(S5_E_INVALID, "need 2**d - 1 splitters (d <= %u), got %u", kWideDMax, v);
+    if (m < 1) return fail(S5_E_INVALID, "empty sample");
+    uint64_t smem = uint64_t(m) * 8 + (uint64_t(1) << d) * 12;
+    if (smem > 227 * 1024) return fail(S5_E_INVALID, "sample too large for one CTA");
+    if (int rc = init_attributes()) return rc;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    k_build_tree<<<1, 1024, smem, st>>>(d_sorted_sample, m, d, d_level_order, d_in_order);
+    S5_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int s5_host_markov_text(const double* cdf, const double* u, uint64_t n, uint32_t sigma,
+                        uint8_t* out) {
+    if (sigma < 1 || sigma > 255) return fail(S5_E_INVALID, "sigma must be in [1, 255]");
+    uint32_t a = 0, b = sigma > 1 ? 1 : 0;  // virtual sym[-2] = 0, sym[-1] = 1
+    const uint64_t row = sigma;
+    for (uint64_t i = 0; i < n; ++i) {
+        const double* c = cdf + (uint64_t(a) * sigma + b) * row;
+        double x = u[i];
+        uint32_t lo = 0, hi = sigma;  // smallest s with c[s] >= x
+        while (lo < hi) {
+            uint32_t mid = (lo + hi) >> 1;
+            if (c[mid] >= x) hi = mid; else lo = mid + 1;
+        }
+        uint32_t s = lo < sigma ? lo : sigma - 1;
+        out[i] = static_cast<uint8_t>(0x40 + s);
+        a = b;
+        b = s;
+    }
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+// s5_device.cuh -- device helpers shared by the S^5 kernels (sm_100a).
+//
+// Keys follow the reference's packing (strings.py:36-47, D1/D2 of SPEC.md):
+// 8 bytes MSB-first, every byte after the first terminator forced to 0, so
+// unsigned integer order equals lexicographic order of the 8-byte windows.
+#pragma once
+
+#include <cstdint>
+
+namespace s5 {
+
+constexpr uint64_t kOnes = 0x0101010101010101ull;
+constexpr uint64_t kHighs = 0x8080808080808080ull;
+
+__device__ __forceinline__ uint64_t bswap64(uint64_t w) {
+    uint32_t lo = static_cast<uint32_t>(w), hi = static_cast<uint32_t>(w >> 32);
+    return (static_cast<uint64_t>(__byte_perm(lo, 0, 0x0123)) << 32) |
+           __byte_perm(hi, 0, 0x0123);
+}
+
+// Key of the string window starting at arena[pos]: two aligned 8-byte loads
+// and a funnel shift give the bytes in string order (first byte in the least
+// significant position); the exact first zero byte is the lowest flagged
+// byte of the SWAR zero test (borrows only propagate upward), bytes from it
+// on are cleared, and a byte swap yields the MSB-first key.
+// Needs arena 8-byte aligned with >= 16 readable bytes past pos.
+__device__ __forceinline__ uint64_t load_key(const uint8_t* __restrict__ arena, uint64_t pos) {
+    const uint64_t* p = reinterpret_cast<const uint64_t*>(arena + (pos & ~7ull));
+    uint64_t lo = __ldg(p);
+    uint64_t hi = __ldg(p + 1);
+    uint32_t sh = static_cast<uint32_t>(pos & 7) * 8;
+    uint64_t w = sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+    uint64_t t = (w - kOnes) & ~w & kHighs;
+    if (t) {
+        uint32_t j = (__ffsll(static_cast<long long>(t)) - 1) >> 3;  // first zero byte
+        w &= (1ull << (8 * j)) - 1;                                    // j == 0 -> 0
+    }
+    return bswap64(w);
+}
+
+// Index (0..8) of the first zero byte of an MSB-first key; 8 if none.
+__device__ __forceinline__ uint32_t zero_index(uint64_t key) {
+    uint64_t w = bswap64(key);
+    uint64_t t = (w - kOnes) & ~w & kHighs;
+    return t ? static_cast<uint32_t>((__ffsll(static_cast<long long>(t)) - 1) >> 3) : 8u;
+}
+
+// classifier.py:145-150 (_has_zero_byte)
+__device__ __forceinline__ bool has_zero_byte(uint64_t key) { return zero_index(key) < 8; }
+
+// Leading equal bytes of two keys that differ (strings.py:56-61 semantics:
+// a shared terminator cannot precede the first difference).
+__device__ __forceinline__ uint32_t diff_bytes(uint64_t a, uint64_t b) {
+    return static_cast<uint32_t>(__clzll(static_cast<long long>(a ^ b))) >> 3;
+}
+
+// Level-order node holding in-order rank c of a perfect tree of depth d
+// (inverse of inorder_rank, classifier.py:179-181).
+__device__ __forceinline__ uint32_t node_of_rank(uint32_t c, uint32_t d) {
+    uint32_t r = c + 1;
+    uint32_t tz = __ffs(r) - 1;
+    uint32_t l = d - 1 - tz;
+    return (1u << l) + (r >> (tz + 1));
+}
+
+// In-order rank of level-order node i at level l (classifier.py:179-181).
+__device__ __forceinline__ uint32_t inorder_rank(uint32_t i, uint32_t l, uint32_t d) {
+    return (2u * (i - (1u << l)) + 1u) * (1u << (d - 1 - l)) - 1u;
+}
+
+// Bucket of key k in the tree t[1..v] (level order, v = 2^d - 1):
+//   c = #splitters < k; bucket = 2c+1 if splitter c == k else 2c
+// (classify_oracle, classifier.py:187-200).
+// UNROLL: full branch-free descent + one leaf equality test
+//   (_classify_strings_unrolled, samplesort.py:51-83).
+// EQUAL: equality test per node with early exit and the duplicate-splitter
+//   walk to the first equal slot (_classify_strings_equal, samplesort.py:86-105).
+template <bool EQUAL>
+__device__ __forceinline__ uint32_t classify(uint64_t k, const uint64_t* t, uint32_t d) {
+    if (!EQUAL) {
+        uint32_t i = 1;
+        for (uint32_t l = 0; l < d; ++l) i = 2 * i + (k > t[i] ? 1u : 0u);
+        uint32_t c = i - (1u << d);
+        uint32_t b = 2 * c;
+        if (c < (1u << d) - 1 && t[node_of_rank(c, d)] == k) b += 1;
+        return b;
+    } else {
+        uint32_t i = 1;
+        for (uint32_t l = 0; l < d; ++l) {
+            uint64_t node = t[i];
+            if (k == node) {
+                uint32_t j = inorder_rank(i, l, d);
+                while (j > 0 && t[node_of_rank(j - 1, d)] == k) --j;
+                return 2 * j + 1;
+            }
+            i = 2 * i + (k > node ? 1u : 0u);
+        }
+        return 2 * (i - (1u << d));
+    }
+}
+
+// Stateless sample RNG: splitmix64 finaliser over (seed, segment, index).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t segment_seed(uint64_t seed, uint64_t begin,
+                                                          uint64_t size, uint64_t depth) {
+    return seed * 0x9E3779B97F4A7C15ull ^ begin * 0xD1B54A32D192ED03ull ^
+           size * 0x8CB92BA72F3D8DD7ull ^ depth * 0xABC98388FB8FAC03ull;
+}
+
+__device__ __forceinline__ uint32_t sample_index(uint64_t sseed, uint32_t t, uint32_t size) {
+    uint64_t r = mix64(sseed + (static_cast<uint64_t>(t) + 1) * 0x9E3779B97F4A7C15ull);
+    return static_cast<uint32_t>(__umul64hi(r, size));
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+}  // namespace s5

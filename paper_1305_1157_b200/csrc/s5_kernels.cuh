@@ -1,0 +1,813 @@
+// s5_kernels.cuh -- sm_100a kernels of the level-synchronous S^5 string sort.
+//
+// Data in HBM (one sort call, n strings):
+//   arena   u8[N + pad]                     read-only, 8-byte aligned
+//   off[2]  u32[n]  key[2] u64[n]           ping-pong (offset, cached 8-byte key)
+//   out     i64[n]  (the caller's handles)  final order, written once per string
+//   lcp     i64[n-1]                        exact values or -(depth+1) hints
+// A segment {begin, size, depth, side} is a range of off/key[side] whose
+// strings share `depth` leading bytes and whose keys hold bytes
+// [depth, depth+8).  Each level processes every live segment once:
+//   wide   (size > narrow_max): multi-CTA S^5 step -- plan, tree, count,
+//          column scan, bucket scan + emit, scatter (samplesort.py:369-434)
+//   narrow (size <= narrow_max): one fused CTA S^5 step (samplesort.py:213-238)
+//   small  (size <= small_max <= 32): warp sort on cached keys with refills
+//          and LCP emission (replaces basesort.py's mkqs/insertion tiers)
+#pragma once
+
+#include <cstdint>
+
+#include "s5_device.cuh"
+
+namespace s5 {
+
+struct Seg {
+    uint32_t begin, size, depth, side;
+};
+
+// Device control block: next-level list counters, error bits, statistics.
+struct Ctl {
+    uint32_t n_list[3];  // next-level wide, narrow, small segment counts
+    uint32_t err;        // bit0 handle range, bit1 list overflow, bit2 pool overflow
+    unsigned long long elems[3];  // strings in next-level wide/narrow/small lists
+    unsigned long long fetches;   // arena key gathers
+    unsigned long long hints;     // boundary LCP hints written
+    uint32_t wide_ctas;           // plan: CTAs of the current wide launch
+    uint32_t pad;
+    unsigned long long tree_words, hist_words;  // plan: pool use of the current level
+};
+
+enum : uint32_t { ERR_RANGE = 1, ERR_LIST = 2, ERR_POOL = 4 };
+enum : int { WIDE = 0, NARROW = 1, SMALL = 2 };
+
+struct SortArgs {
+    const uint8_t* arena;
+    uint32_t* off[2];
+    uint64_t* key[2];
+    int64_t* out;
+    int64_t* lcp;
+    Seg* next[3];
+    uint32_t cap[3];
+    Ctl* ctl;
+    uint32_t small_max, narrow_max;
+    uint32_t dmax;  // log2(cfg.v + 1)
+    uint32_t alpha;
+    uint64_t seed;
+};
+
+constexpr uint32_t kNarrowThreads = 512;
+constexpr uint32_t kNarrowDMax = 10;          // v <= 1023, k <= 2047
+constexpr uint32_t kNarrowMaxSize = 16384;    // tags fit 14-bit ranks
+constexpr uint32_t kNarrowSampleCap = 8192;
+constexpr uint32_t kWideThreads = 1024;
+constexpr uint32_t kWideDMax = 13;            // v <= 8191, k <= 16383
+constexpr uint32_t kWideSampleCap = 16384;
+constexpr uint32_t kWideChunkMin = 65536;     // strings per CTA at least
+constexpr uint32_t kWideCtasMax = 296;        // 2 waves of 148 SMs
+
+__host__ __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) {
+    uint32_t d = 0;
+    while ((1u << d) < x) ++d;
+    return d;
+}
+
+// Splitter tree depth for a segment: about 16 strings per inner bucket.
+__host__ __device__ __forceinline__ uint32_t choose_d(uint32_t size, uint32_t dmax) {
+    uint32_t d = ceil_log2((size + 15) / 16);
+    if (d < 1) d = 1;
+    return d < dmax ? d : dmax;
+}
+
+__host__ __device__ __forceinline__ uint32_t wide_ctas(uint32_t size) {
+    uint32_t c = (size + kWideChunkMin - 1) / kWideChunkMin;
+    return c < 1 ? 1 : (c > kWideCtasMax ? kWideCtasMax : c);
+}
+
+__device__ __forceinline__ void emit_child(const SortArgs& A, uint32_t begin, uint32_t size,
+                                           uint32_t depth, uint32_t side) {
+    int cls = size <= A.small_max ? SMALL : (size <= A.narrow_max ? NARROW : WIDE);
+    uint32_t idx = atomicAdd(&A.ctl->n_list[cls], 1u);
+    if (idx < A.cap[cls]) {
+        A.next[cls][idx] = Seg{begin, size, depth, side};
+        atomicAdd(&A.ctl->elems[cls], static_cast<unsigned long long>(size));
+    } else {
+        atomicOr(&A.ctl->err, ERR_LIST);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// block-level building blocks
+
+// In-place ascending bitonic sort of s[0..M), M a power of two.
+template <uint32_t THREADS>
+__device__ void bitonic_sort_smem(uint64_t* s, uint32_t M) {
+    for (uint32_t k = 2; k <= M; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < M; i += THREADS) {
+                uint32_t ixj = i ^ j;
+                if (ixj > i) {
+                    uint64_t a = s[i], b = s[ixj];
+                    bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        s[i] = b;
+                        s[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// select_splitters + _fill_level_order (classifier.py:85-126), level by level:
+// node i covers sample range [na[i], nb[i]] with fallback sample[nf[i]];
+// its splitter is the range middle, equal samples are skipped with binary
+// searches (the sample is sorted), an empty range yields the fallback for the
+// whole subtree (D5).  Produces exactly the reference's splitters.
+template <uint32_t THREADS>
+__device__ void build_tree_levels(const uint64_t* sample, uint32_t m, uint32_t d,
+                                  uint64_t* tree, int32_t* na, int32_t* nb, uint32_t* nf) {
+    if (threadIdx.x == 0) {
+        na[1] = 0;
+        nb[1] = static_cast<int32_t>(m) - 1;
+        nf[1] = 0;
+        tree[0] = 0;
+    }
+    __syncthreads();
+    for (uint32_t l = 0; l < d; ++l) {
+        uint32_t first = 1u << l;
+        for (uint32_t i = first + threadIdx.x; i < 2 * first; i += THREADS) {
+            int32_t a = na[i], b = nb[i];
+            uint32_t f = nf[i];
+            uint64_t x;
+            int32_t la = 1, lb = 0, ra = 1, rb = 0;
+            uint32_t cf = f;
+            if (a > b) {
+                x = sample[f];
+            } else {
+                int32_t mm = (a + b) >> 1;
+                x = sample[mm];
+                int32_t lo = a, hi = mm;  // first index in [a, mm] with sample >= x
+                while (lo < hi) {
+                    int32_t mid = (lo + hi) >> 1;
+                    if (sample[mid] < x) lo = mid + 1; else hi = mid;
+                }
+                int32_t b2 = lo - 1;
+                lo = mm + 1;
+                hi = b + 1;  // first index in (mm, b] with sample > x
+                while (lo < hi) {
+                    int32_t mid = (lo + hi) >> 1;
+                    if (sample[mid] <= x) lo = mid + 1; else hi = mid;
+                }
+                la = a; lb = b2; ra = lo; rb = b;
+                cf = static_cast<uint32_t>(mm);
+            }
+            tree[i] = x;
+            if (l + 1 < d) {
+                na[2 * i] = la; nb[2 * i] = lb; nf[2 * i] = cf;
+                na[2 * i + 1] = ra; nb[2 * i + 1] = rb; nf[2 * i + 1] = cf;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Exclusive scan of h[0..k) in place, h[k] = total.  All threads call.
+template <uint32_t THREADS>
+__device__ void block_exclusive_scan(uint32_t* h, uint32_t k, uint32_t* warp_sums) {
+    const uint32_t per = (k + THREADS) / THREADS;  // covers k+1 slots
+    uint32_t lo = threadIdx.x * per;
+    uint32_t sum = 0;
+    for (uint32_t j = 0; j < per; ++j) {
+        uint32_t idx = lo + j;
+        if (idx < k) sum += h[idx];
+    }
+    uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = sum;
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sums[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        constexpr uint32_t NW = THREADS / 32;
+        uint32_t x = lane < NW ? warp_sums[lane] : 0;
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane < NW) warp_sums[lane] = x;  // inclusive
+    }
+    __syncthreads();
+    uint32_t run = incl - sum + (w ? warp_sums[w - 1] : 0);
+    for (uint32_t j = 0; j < per; ++j) {
+        uint32_t idx = lo + j;
+        if (idx < k) {
+            uint32_t c = h[idx];
+            h[idx] = run;
+            run += c;
+        } else if (idx == k) {
+            h[idx] = run;
+        }
+    }
+    __syncthreads();
+}
+
+// Per-bucket epilogue shared by narrow and wide steps: LCP hint at the
+// bucket's left boundary (bucket_layout boundaries, classifier.py:284-304),
+// and a child segment for every unfinished bucket of >= 2 strings with the
+// reference's depth rule for equality buckets (+8) and finished rule (D8:
+// equality bucket of a terminated splitter = identical strings).
+__device__ __forceinline__ void bucket_epilogue(const SortArgs& A, const Seg& s, uint32_t b,
+                                                uint32_t start, uint32_t cnt, uint64_t splitter) {
+    uint32_t pos0 = s.begin + start;
+    if (start > 0 && A.lcp) {
+        A.lcp[pos0 - 1] = -static_cast<int64_t>(s.depth) - 1;
+        atomicAdd(&A.ctl->hints, 1ull);
+    }
+    bool odd = b & 1;
+    bool fin = cnt == 1 || (odd && has_zero_byte(splitter));
+    if (!fin) emit_child(A, pos0, cnt, s.depth + (odd ? 8u : 0u), s.side ^ 1u);
+}
+
+// Element epilogue: final slot for finished buckets (handle + identical-string
+// LCP), refetched key at depth+8 for equality buckets, plain move otherwise.
+__device__ __forceinline__ void place(const SortArgs& A, const Seg& s, uint32_t b, bool fin,
+                                      uint32_t p, uint32_t bucket_end, uint32_t o, uint64_t k,
+                                      unsigned long long& fetches) {
+    uint32_t dst = s.begin + p;
+    uint32_t ns = s.side ^ 1u;
+    if (fin) {
+        A.out[dst] = o;
+        if ((b & 1) && A.lcp && p + 1 < bucket_end) A.lcp[dst] = s.depth + zero_index(k);
+    } else if (b & 1) {
+        A.off[ns][dst] = o;
+        A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + s.depth + 8);
+        ++fetches;
+    } else {
+        A.off[ns][dst] = o;
+        A.key[ns][dst] = k;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// level 0: gather keys at the common depth (pack_keys, strings.py:176-182)
+
+__global__ void k_gather(const int64_t* __restrict__ handles, uint32_t n, uint64_t depth,
+                         uint64_t arena_len, SortArgs A) {
+    uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        int64_t h = handles[i];
+        if (h < 0 || static_cast<uint64_t>(h) + depth >= arena_len) {
+            atomicOr(&A.ctl->err, ERR_RANGE);
+            h = 0;
+        }
+        A.off[0][i] = static_cast<uint32_t>(h);
+        A.key[0][i] = load_key(A.arena, static_cast<uint64_t>(h) + depth);
+    }
+}
+
+__global__ void k_init_root(SortArgs A, uint32_t n, uint32_t depth) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        emit_child(A, 0, n, depth, 0);
+        A.ctl->fetches += n;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// narrow tier: one fused CTA per segment (sample, tree, classify+count with
+// warp-aggregated shared-memory histogram, scan, emit, scatter)
+
+struct NarrowSmem {
+    static constexpr uint32_t tree_bytes = (1u << kNarrowDMax) * 8;                  // 8 KB
+    static constexpr uint32_t big_bytes =                                              // 64 KB
+        (kNarrowSampleCap * 8 > kNarrowMaxSize * 4) ? kNarrowSampleCap * 8 : kNarrowMaxSize * 4;
+    static constexpr uint32_t node_bytes = (1u << kNarrowDMax) * 12;                  // 12 KB
+    static constexpr uint32_t hist_bytes = ((2u << kNarrowDMax) + 2) * 4;             // 8 KB
+    static constexpr uint32_t aux_bytes = node_bytes > hist_bytes ? node_bytes : hist_bytes;
+    static constexpr uint32_t total = tree_bytes + big_bytes + aux_bytes + 64 * 4;
+};
+
+template <bool EQUAL>
+__global__ void __launch_bounds__(kNarrowThreads, 2)
+k_narrow(SortArgs A, const Seg* __restrict__ segs) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint64_t* tree = reinterpret_cast<uint64_t*>(sm);
+    uint8_t* big = sm + NarrowSmem::tree_bytes;
+    uint64_t* sample = reinterpret_cast<uint64_t*>(big);
+    uint32_t* tags = reinterpret_cast<uint32_t*>(big);
+    uint8_t* aux = big + NarrowSmem::big_bytes;
+    int32_t* na = reinterpret_cast<int32_t*>(aux);
+    int32_t* nb = na + (1u << kNarrowDMax);
+    uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << kNarrowDMax));
+    uint32_t* hist = reinterpret_cast<uint32_t*>(aux);
+    uint32_t* warp_sums = reinterpret_cast<uint32_t*>(aux + NarrowSmem::aux_bytes);
+
+    const Seg s = segs[blockIdx.x];
+    const uint32_t d = choose_d(s.size, A.dmax < kNarrowDMax ? A.dmax : kNarrowDMax);
+    const uint32_t v = (1u << d) - 1, k = 2 * v + 1;
+    uint32_t m = A.alpha * v;
+    if (m > kNarrowSampleCap) m = kNarrowSampleCap;
+    uint32_t M = 1;
+    while (M < m) M <<= 1;
+    const uint32_t* __restrict__ off = A.off[s.side] + s.begin;
+    const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
+
+    // stage 1: sample (classifier.py:76-82) and splitter tree
+    const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
+    for (uint32_t t = threadIdx.x; t < M; t += kNarrowThreads)
+        sample[t] = t < m ? key[sample_index(sseed, t, s.size)] : ~0ull;
+    __syncthreads();
+    bitonic_sort_smem<kNarrowThreads>(sample, M);
+    build_tree_levels<kNarrowThreads>(sample, m, d, tree, na, nb, nf);
+    for (uint32_t b = threadIdx.x; b <= k; b += kNarrowThreads) hist[b] = 0;
+    __syncthreads();
+
+    // stage 2: classify + count; tag = bucket | rank-in-bucket << 11
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t base = 0; base < s.size; base += kNarrowThreads) {
+        uint32_t i = base + threadIdx.x;
+        bool act = i < s.size;
+        uint32_t b = act ? classify<EQUAL>(key[i], tree, d) : 0xFFFFFFFFu;
+        uint32_t peers = __match_any_sync(0xffffffffu, b);
+        uint32_t leader = __ffs(peers) - 1;
+        uint32_t r = 0;
+        if (act && lane == leader) r = atomicAdd(&hist[b], __popc(peers));
+        r = __shfl_sync(0xffffffffu, r, leader) + __popc(peers & lanemask_lt());
+        if (act) tags[i] = b | (r << 11);
+    }
+    __syncthreads();
+
+    // stage 3: bucket boundaries (bucket_layout) and children
+    block_exclusive_scan<kNarrowThreads>(hist, k, warp_sums);
+    for (uint32_t b = threadIdx.x; b < k; b += kNarrowThreads) {
+        uint32_t cnt = hist[b + 1] - hist[b];
+        if (cnt) {
+            uint64_t spl = (b & 1) ? tree[node_of_rank(b >> 1, d)] : 0;
+            bucket_epilogue(A, s, b, hist[b], cnt, spl);
+        }
+    }
+
+    // stage 4: out-of-place distribution (samplesort.py:146-152)
+    unsigned long long fetches = 0;
+    for (uint32_t i = threadIdx.x; i < s.size; i += kNarrowThreads) {
+        uint32_t tg = tags[i];
+        uint32_t b = tg & 2047u, r = tg >> 11;
+        uint32_t start = hist[b], end = hist[b + 1];
+        uint64_t kk = key[i];
+        bool fin = (end - start == 1) || ((b & 1) && has_zero_byte(kk));
+        place(A, s, b, fin, start + r, end, off[i], kk, fetches);
+    }
+    if (fetches) atomicAdd(&A.ctl->fetches, fetches);
+}
+
+// ---------------------------------------------------------------------------
+// small tier: one warp per segment of <= 32 strings.  Bitonic sort of
+// (run, key); pairs of equal unterminated keys stay in a run whose keys are
+// refilled at depth+8 (the mkqs equal-partition refill, basesort.py:146-150);
+// each adjacent pair's LCP is emitted the moment it is resolved:
+//   keys differ            -> depth + equal leading bytes
+//   keys equal, terminated -> depth + bytes before the terminator (|s|)
+
+__device__ __forceinline__ bool comp_less(uint32_t ra, uint64_t ka, uint32_t rb, uint64_t kb) {
+    return ra < rb || (ra == rb && ka < kb);
+}
+
+__device__ __forceinline__ void warp_bitonic(uint32_t& run, uint64_t& key, uint32_t& off,
+                                             uint32_t lane) {
+#pragma unroll
+    for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            uint32_t orun = __shfl_xor_sync(0xffffffffu, run, j);
+            uint64_t okey = __shfl_xor_sync(0xffffffffu, key, j);
+            uint32_t ooff = __shfl_xor_sync(0xffffffffu, off, j);
+            bool up = (lane & k) == 0;
+            bool lower = (lane & j) == 0;
+            bool take = (lower == up) ? comp_less(orun, okey, run, key)
+                                      : comp_less(run, key, orun, okey);
+            if (take) {
+                run = orun;
+                key = okey;
+                off = ooff;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_small(SortArgs A, const Seg* __restrict__ segs,
+                                               uint32_t nsegs) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (warp >= nsegs) return;
+    const Seg s = segs[warp];
+    const bool valid = lane < s.size;
+    const bool pair_valid = lane + 1 < s.size;
+    uint32_t o = valid ? A.off[s.side][s.begin + lane] : 0u;
+    uint64_t k = valid ? A.key[s.side][s.begin + lane] : ~0ull;
+    uint32_t run = valid ? 0u : 0xFFFFFFFFu;
+    uint64_t depth = s.depth;
+    bool resolved = false;
+    uint64_t my_lcp = 0;
+    unsigned long long fetches = 0;
+    for (;;) {
+        warp_bitonic(run, k, o, lane);
+        uint64_t nk = __shfl_down_sync(0xffffffffu, k, 1);
+        uint32_t nrun = __shfl_down_sync(0xffffffffu, run, 1);
+        if (pair_valid && !resolved && nrun == run) {
+            if (k != nk) {
+                my_lcp = depth + diff_bytes(k, nk);
+                resolved = true;
+            } else if (has_zero_byte(k)) {
+                my_lcp = depth + zero_index(k);
+                resolved = true;
+            }
+        }
+        uint32_t unres = __ballot_sync(0xffffffffu, pair_valid && !resolved);
+        if (!unres) break;
+        bool prev_unres = lane > 0 && ((unres >> (lane - 1)) & 1u);
+        uint32_t starts = __ballot_sync(0xffffffffu, !prev_unres);
+        uint32_t le = starts & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
+        uint32_t run_start = 31u - __clz(le);
+        bool active = ((unres >> lane) & 1u) || prev_unres;
+        depth += 8;
+        if (active) {
+            k = load_key(A.arena, static_cast<uint64_t>(o) + depth);
+            ++fetches;
+        }
+        run = valid ? run_start : 0xFFFFFFFFu;
+    }
+    if (valid) A.out[s.begin + lane] = o;
+    if (pair_valid && A.lcp) A.lcp[s.begin + lane] = static_cast<int64_t>(my_lcp);
+    for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
+    if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
+}
+
+// ---------------------------------------------------------------------------
+// wide tier (segments > narrow_max): the fully parallel step of
+// samplesort.py:369-434 with CTAs as workers.
+
+struct WidePlan {
+    const Seg* segs;
+    uint32_t nsegs;
+    uint32_t* cta_start;   // [nsegs + 1]
+    uint64_t* tree_off;    // [nsegs]  u64 words into tree_pool
+    uint64_t* hist_off;    // [nsegs]  u32 words into hist_pool: C rows of k, then k+1 starts
+    uint64_t* tree_pool;
+    uint32_t* hist_pool;
+    uint64_t tree_cap, hist_cap;
+};
+
+struct WideGeom {
+    uint32_t d, v, k, C;
+};
+
+__device__ __forceinline__ WideGeom wide_geom(const Seg& s, uint32_t dmax) {
+    WideGeom g;
+    g.d = choose_d(s.size, dmax < kWideDMax ? dmax : kWideDMax);
+    g.v = (1u << g.d) - 1;
+    g.k = 2 * g.v + 1;
+    g.C = wide_ctas(s.size);
+    return g;
+}
+
+// Exclusive scans of CTA counts and pool sizes over the wide segments.
+__global__ void __launch_bounds__(1024) k_wide_plan(SortArgs A, WidePlan P) {
+    __shared__ unsigned long long s_carry[3];
+    __shared__ unsigned long long s_w[3][32];
+    if (threadIdx.x == 0) s_carry[0] = s_carry[1] = s_carry[2] = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint32_t base = 0; base < P.nsegs; base += 1024) {
+        uint32_t i = base + threadIdx.x;
+        unsigned long long x[3] = {0, 0, 0};
+        if (i < P.nsegs) {
+            WideGeom g = wide_geom(P.segs[i], A.dmax);
+            x[0] = g.C;
+            x[1] = g.v + 1;
+            x[2] = static_cast<unsigned long long>(g.C) * g.k + g.k + 1;
+        }
+        unsigned long long incl[3];
+        for (int q = 0; q < 3; ++q) {
+            unsigned long long y = x[q];
+            for (uint32_t o = 1; o < 32; o <<= 1) {
+                unsigned long long z = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y += z;
+            }
+            incl[q] = y;
+            if (lane == 31) s_w[q][w] = y;
+        }
+        __syncthreads();
+        if (w == 0) {
+            for (int q = 0; q < 3; ++q) {
+                unsigned long long y = s_w[q][lane];
+                for (uint32_t o = 1; o < 32; o <<= 1) {
+                    unsigned long long z = __shfl_up_sync(0xffffffffu, y, o);
+                    if (lane >= o) y += z;
+                }
+                s_w[q][lane] = y;
+            }
+        }
+        __syncthreads();
+        if (i < P.nsegs) {
+            unsigned long long e[3];
+            for (int q = 0; q < 3; ++q)
+                e[q] = s_carry[q] + incl[q] - x[q] + (w ? s_w[q][w - 1] : 0ull);
+            P.cta_start[i] = static_cast<uint32_t>(e[0]);
+            P.tree_off[i] = e[1];
+            P.hist_off[i] = e[2];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int q = 0; q < 3; ++q) s_carry[q] += s_w[q][31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        P.cta_start[P.nsegs] = static_cast<uint32_t>(s_carry[0]);
+        A.ctl->wide_ctas = static_cast<uint32_t>(s_carry[0]);
+        A.ctl->tree_words = s_carry[1];
+        A.ctl->hist_words = s_carry[2];
+        if (s_carry[1] > P.tree_cap || s_carry[2] > P.hist_cap) {
+            atomicOr(&A.ctl->err, ERR_POOL);
+            A.ctl->wide_ctas = 0;  // skip the level's wide kernels; host reports the error
+        }
+    }
+}
+
+// Sample + splitter tree per wide segment (one CTA each).
+__global__ void __launch_bounds__(kWideThreads, 1) k_wide_tree(SortArgs A, WidePlan P) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    if (A.ctl->wide_ctas == 0) return;
+    uint64_t* sample = reinterpret_cast<uint64_t*>(sm);
+    int32_t* na = reinterpret_cast<int32_t*>(sm + kWideSampleCap * 8);
+    int32_t* nb = na + (1u << kWideDMax);
+    uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << kWideDMax));
+    const Seg s = P.segs[blockIdx.x];
+    const WideGeom g = wide_geom(s, A.dmax);
+    uint32_t m = A.alpha * g.v;
+    if (m > kWideSampleCap) m = kWideSampleCap;
+    uint32_t M = 1;
+    while (M < m) M <<= 1;
+    const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
+    const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
+    for (uint32_t t = threadIdx.x; t < M; t += kWideThreads)
+        sample[t] = t < m ? key[sample_index(sseed, t, s.size)] : ~0ull;
+    __syncthreads();
+    bitonic_sort_smem<kWideThreads>(sample, M);
+    build_tree_levels<kWideThreads>(sample, m, g.d, P.tree_pool + P.tree_off[blockIdx.x], na, nb, nf);
+}
+
+__device__ __forceinline__ uint32_t find_seg(const uint32_t* cta_start, uint32_t nsegs,
+                                             uint32_t g) {
+    uint32_t lo = 0, hi = nsegs;  // last s with cta_start[s] <= g
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (cta_start[mid] <= g) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// Per-CTA histogram of a contiguous chunk (stage 2, samplesort.py:383-400).
+template <bool EQUAL>
+__global__ void __launch_bounds__(kWideThreads, 1) k_wide_count(SortArgs A, WidePlan P) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const uint32_t G = blockIdx.x;
+    if (G >= A.ctl->wide_ctas) return;
+    uint64_t* tree = reinterpret_cast<uint64_t*>(sm);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sm + (1u << kWideDMax) * 8);
+    const uint32_t si = find_seg(P.cta_start, P.nsegs, G);
+    const Seg s = P.segs[si];
+    const WideGeom g = wide_geom(s, A.dmax);
+    const uint32_t c = G - P.cta_start[si];
+    const uint32_t chunk = (s.size + g.C - 1) / g.C;
+    const uint32_t lo = c * chunk;
+    const uint32_t hi = min(s.size, lo + chunk);
+    const uint64_t* tsrc = P.tree_pool + P.tree_off[si];
+    for (uint32_t i = threadIdx.x; i <= g.v; i += kWideThreads) tree[i] = tsrc[i];
+    for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) hist[b] = 0;
+    __syncthreads();
+    const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t base = lo; base < hi; base += kWideThreads) {
+        uint32_t i = base + threadIdx.x;
+        bool act = i < hi;
+        uint32_t b = act ? classify<EQUAL>(key[i], tree, g.d) : 0xFFFFFFFFu;
+        uint32_t peers = __match_any_sync(0xffffffffu, b);
+        if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[b], __popc(peers));
+    }
+    __syncthreads();
+    uint32_t* row = P.hist_pool + P.hist_off[si] + static_cast<uint64_t>(c) * g.k;
+    for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) row[b] = hist[b];
+}
+
+// Column prefix over the C rows of every bucket (the worker-major cursor scan
+// of samplesort.py:402-410); totals land in the bucket-start area.
+__global__ void __launch_bounds__(1024) k_wide_colscan(SortArgs A, WidePlan P) {
+    if (A.ctl->wide_ctas == 0) return;
+    const uint32_t si = blockIdx.x;
+    const Seg s = P.segs[si];
+    const WideGeom g = wide_geom(s, A.dmax);
+    const uint32_t b = blockIdx.y * blockDim.x + threadIdx.x;
+    if (b >= g.k) return;
+    uint32_t* rows = P.hist_pool + P.hist_off[si];
+    uint32_t run = 0;
+    uint32_t c = 0;
+    for (; c + 8 <= g.C; c += 8) {
+        uint32_t x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = rows[static_cast<uint64_t>(c + q) * g.k + b];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            rows[static_cast<uint64_t>(c + q) * g.k + b] = run;
+            run += x[q];
+        }
+    }
+    for (; c < g.C; ++c) {
+        uint32_t x = rows[static_cast<uint64_t>(c) * g.k + b];
+        rows[static_cast<uint64_t>(c) * g.k + b] = run;
+        run += x;
+    }
+    rows[static_cast<uint64_t>(g.C) * g.k + b] = run;
+}
+
+// Bucket starts (stage 3) and the per-bucket epilogue (children, LCP hints).
+__global__ void __launch_bounds__(1024) k_wide_bscan(SortArgs A, WidePlan P) {
+    __shared__ uint32_t warp_sums[32];
+    if (A.ctl->wide_ctas == 0) return;
+    const uint32_t si = blockIdx.x;
+    const Seg s = P.segs[si];
+    const WideGeom g = wide_geom(s, A.dmax);
+    uint32_t* starts = P.hist_pool + P.hist_off[si] + static_cast<uint64_t>(g.C) * g.k;
+    block_exclusive_scan<1024>(starts, g.k, warp_sums);
+    const uint64_t* tree = P.tree_pool + P.tree_off[si];
+    for (uint32_t b = threadIdx.x; b < g.k; b += 1024) {
+        uint32_t cnt = starts[b + 1] - starts[b];
+        if (cnt) {
+            uint64_t spl = (b & 1) ? tree[node_of_rank(b >> 1, g.d)] : 0;
+            bucket_epilogue(A, s, b, starts[b], cnt, spl);
+        }
+    }
+}
+
+// Out-of-place distribution with per-CTA cursors (stage 4, samplesort.py:412-417).
+template <bool EQUAL>
+__global__ void __launch_bounds__(kWideThreads, 1) k_wide_scatter(SortArgs A, WidePlan P) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const uint32_t G = blockIdx.x;
+    if (G >= A.ctl->wide_ctas) return;
+    uint64_t* tree = reinterpret_cast<uint64_t*>(sm);
+    uint32_t* cur = reinterpret_cast<uint32_t*>(sm + (1u << kWideDMax) * 8);
+    const uint32_t si = find_seg(P.cta_start, P.nsegs, G);
+    const Seg s = P.segs[si];
+    const WideGeom g = wide_geom(s, A.dmax);
+    const uint32_t c = G - P.cta_start[si];
+    const uint32_t chunk = (s.size + g.C - 1) / g.C;
+    const uint32_t lo = c * chunk;
+    const uint32_t hi = min(s.size, lo + chunk);
+    const uint64_t* tsrc = P.tree_pool + P.tree_off[si];
+    const uint32_t* rows = P.hist_pool + P.hist_off[si];
+    const uint32_t* starts = rows + static_cast<uint64_t>(g.C) * g.k;
+    for (uint32_t i = threadIdx.x; i <= g.v; i += kWideThreads) tree[i] = tsrc[i];
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) {
+        uint32_t st = starts[b], cnt = starts[b + 1] - st;
+        bool fin = cnt == 1 || ((b & 1) && has_zero_byte(tree[node_of_rank(b >> 1, g.d)]));
+        cur[b] = (st + rows[static_cast<uint64_t>(c) * g.k + b]) | (fin ? 0x80000000u : 0u);
+    }
+    __syncthreads();
+    const uint32_t* __restrict__ off = A.off[s.side] + s.begin;
+    const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
+    const uint32_t lane = threadIdx.x & 31;
+    unsigned long long fetches = 0;
+    for (uint32_t base = lo; base < hi; base += kWideThreads) {
+        uint32_t i = base + threadIdx.x;
+        bool act = i < hi;
+        uint64_t kk = act ? key[i] : 0;
+        uint32_t o = act ? off[i] : 0;
+        uint32_t b = act ? classify<EQUAL>(kk, tree, g.d) : 0xFFFFFFFFu;
+        uint32_t peers = __match_any_sync(0xffffffffu, b);
+        uint32_t leader = __ffs(peers) - 1;
+        uint32_t r = 0;
+        if (act && lane == leader) r = atomicAdd(&cur[b], __popc(peers));
+        r = __shfl_sync(0xffffffffu, r, leader);
+        if (act) {
+            bool fin = r >> 31;
+            uint32_t p = (r & 0x7FFFFFFFu) + __popc(peers & lanemask_lt());
+            uint32_t end = fin && (b & 1) ? starts[b + 1] : 0;
+            place(A, s, b, fin, p, end, o, kk, fetches);
+        }
+    }
+    for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
+    if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
+}
+
+// ---------------------------------------------------------------------------
+// LCP at bucket boundaries: the two strings differ within the 8-byte window
+// at the recorded depth (they were classified into different buckets).
+
+__global__ void k_lcp_fix(const uint8_t* __restrict__ arena, const int64_t* __restrict__ out,
+                          int64_t* __restrict__ lcp, uint64_t m) {
+    uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+         i += stride) {
+        int64_t v = lcp[i];
+        if (v >= 0) continue;
+        uint64_t d = static_cast<uint64_t>(-v - 1);
+        uint64_t a = static_cast<uint64_t>(out[i]), b = static_cast<uint64_t>(out[i + 1]);
+        for (;;) {
+            uint64_t ka = load_key(arena, a + d), kb = load_key(arena, b + d);
+            if (ka != kb) { lcp[i] = static_cast<int64_t>(d + diff_bytes(ka, kb)); break; }
+            if (has_zero_byte(ka)) { lcp[i] = static_cast<int64_t>(d + zero_index(ka)); break; }
+            d += 8;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// standalone operation surfaces (parity tests of the pieces)
+
+__global__ void k_pack_keys(const uint8_t* __restrict__ arena, const int64_t* __restrict__ h,
+                            uint64_t n, uint64_t depth, uint64_t* __restrict__ out) {
+    uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += stride)
+        out[i] = load_key(arena, static_cast<uint64_t>(h[i]) + depth);
+}
+
+// lcp of adjacent sorted strings, 8 bytes per step (strings.py:56-61, :99-102)
+__global__ void k_adjacent_lcp(const uint8_t* __restrict__ arena, const int64_t* __restrict__ h,
+                               uint64_t m, int64_t* __restrict__ out) {
+    uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+         i += stride) {
+        uint64_t a = static_cast<uint64_t>(h[i]), b = static_cast<uint64_t>(h[i + 1]);
+        uint64_t d = 0;
+        for (;;) {
+            uint64_t ka = load_key(arena, a + d), kb = load_key(arena, b + d);
+            if (ka != kb) { out[i] = static_cast<int64_t>(d + diff_bytes(ka, kb)); break; }
+            if (has_zero_byte(ka)) { out[i] = static_cast<int64_t>(d + zero_index(ka)); break; }
+            d += 8;
+        }
+    }
+}
+
+// _first_unsorted (strings.py:77-82): min i with s[i] > s[i+1]
+__global__ void k_first_unsorted(const uint8_t* __restrict__ arena,
+                                 const int64_t* __restrict__ h, uint64_t m,
+                                 unsigned long long* __restrict__ result) {
+    uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
+         i += stride) {
+        uint64_t a = static_cast<uint64_t>(h[i]), b = static_cast<uint64_t>(h[i + 1]);
+        uint64_t d = 0;
+        for (;;) {
+            uint64_t ka = load_key(arena, a + d), kb = load_key(arena, b + d);
+            if (ka != kb) {
+                if (ka > kb) atomicMin(result, static_cast<unsigned long long>(i));
+                break;
+            }
+            if (has_zero_byte(ka)) break;
+            d += 8;
+        }
+    }
+}
+
+// classify_tree_unrolled / _equal over a key batch: level order built in
+// shared memory from the in-order splitters (_fill_level_order).
+template <bool EQUAL>
+__global__ void k_classify(const uint64_t* __restrict__ keys, uint64_t n,
+                           const uint64_t* __restrict__ in_order, uint32_t d,
+                           uint16_t* __restrict__ out) {
+    extern __shared__ __align__(16) uint64_t tree[];
+    const uint32_t v = (1u << d) - 1;
+    for (uint32_t i = threadIdx.x + 1; i <= v; i += blockDim.x) {
+        uint32_t l = 31 - __clz(i);
+        tree[i] = in_order[inorder_rank(i, l, d)];
+    }
+    if (threadIdx.x == 0) tree[0] = 0;
+    __syncthreads();
+    uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += stride)
+        out[i] = static_cast<uint16_t>(classify<EQUAL>(keys[i], tree, d));
+}
+
+// select_splitters + build_tree from a sorted sample (single CTA).
+__global__ void __launch_bounds__(1024) k_build_tree(const uint64_t* __restrict__ sample,
+                                                     uint32_t m, uint32_t d,
+                                                     uint64_t* __restrict__ level_order,
+                                                     uint64_t* __restrict__ in_order) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint64_t* s = reinterpret_cast<uint64_t*>(sm);
+    int32_t* na = reinterpret_cast<int32_t*>(sm + static_cast<uint64_t>(m) * 8);
+    int32_t* nb = na + (1u << d);
+    uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << d));
+    for (uint32_t i = threadIdx.x; i < m; i += 1024) s[i] = sample[i];
+    __syncthreads();
+    build_tree_levels<1024>(s, m, d, level_order, na, nb, nf);
+    const uint32_t v = (1u << d) - 1;
+    for (uint32_t c = threadIdx.x; c < v; c += 1024) in_order[c] = level_order[node_of_rank(c, d)];
+}
+
+}  // namespace s5

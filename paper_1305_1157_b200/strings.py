@@ -127,3 +127,147 @@ class DatasetStats:
     D: int
     sigma: int
     avg_len: float
+
+
+# ---------------------------------------------------------------------------
+# device operations (libs5.so); handles may be numpy or CUDA int64 tensors
+
+def _to_dev_handles(handles, dev):
+    import torch
+    if isinstance(handles, torch.Tensor):
+        return handles.to(dev, torch.int64).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(handles, np.int64)).to(dev)
+
+
+def _dev():
+    import torch
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def pack_keys(arena: StringArena, handles, depth: int = 0, out=None):
+    """Packed word key of every handle at ``depth`` (strings.py:176-182)."""
+    import torch
+    from . import _lib
+    dev = handles.device if isinstance(handles, torch.Tensor) and handles.is_cuda else _dev()
+    h = _to_dev_handles(handles, dev)
+    keys = torch.empty(h.numel(), dtype=torch.int64, device=dev)
+    if h.numel():
+        rc = _lib.lib().s5_pack_keys(arena.device(dev).data_ptr(), arena.data.size, h.data_ptr(),
+                                     h.numel(), int(depth), keys.data_ptr(),
+                                     _lib.current_stream_ptr())
+        _lib.check(rc, "s5_pack_keys")
+    if isinstance(handles, torch.Tensor) and handles.is_cuda:
+        return keys.view(torch.uint64) if hasattr(torch, "uint64") else keys
+    res = keys.cpu().numpy().view(np.uint64)
+    if out is not None:
+        out[:] = res
+        return out
+    return res
+
+
+def extract_key(arena: StringArena, handle: int, depth: int = 0) -> int:
+    """Packed key of one string at ``depth`` (strings.py:185-191)."""
+    return int(pack_keys(arena, np.asarray([handle], np.int64), depth)[0])
+
+
+def adjacent_lcps(arena: StringArena, sorted_handles):
+    """LCP array of a sorted handle array (_adjacent_lcps, strings.py:99-102)."""
+    import torch
+    from . import _lib
+    dev = (sorted_handles.device if isinstance(sorted_handles, torch.Tensor)
+           and sorted_handles.is_cuda else _dev())
+    h = _to_dev_handles(sorted_handles, dev)
+    n = h.numel()
+    out = torch.empty(max(n - 1, 0), dtype=torch.int64, device=dev)
+    if n > 1:
+        rc = _lib.lib().s5_adjacent_lcp(arena.device(dev).data_ptr(), arena.data.size,
+                                        h.data_ptr(), n, out.data_ptr(), _lib.current_stream_ptr())
+        _lib.check(rc, "s5_adjacent_lcp")
+    if isinstance(sorted_handles, torch.Tensor) and sorted_handles.is_cuda:
+        return out
+    return out.cpu().numpy()
+
+
+def lcp(arena: StringArena, a: int, b: int) -> int:
+    """Longest common prefix of two strings, terminators excluded (strings.py:194-196)."""
+    return int(adjacent_lcps(arena, np.asarray([a, b], np.int64))[0])
+
+
+def first_unsorted(arena: StringArena, handles) -> int:
+    """First i with s[i] > s[i+1], or -1 (strings.py:77-82), on the device."""
+    import torch
+    from . import _lib
+    dev = handles.device if isinstance(handles, torch.Tensor) and handles.is_cuda else _dev()
+    h = _to_dev_handles(handles, dev)
+    res = torch.empty(1, dtype=torch.int64, device=dev)
+    rc = _lib.lib().s5_first_unsorted(arena.device(dev).data_ptr(), arena.data.size, h.data_ptr(),
+                                      h.numel(), res.data_ptr(), _lib.current_stream_ptr())
+    _lib.check(rc, "s5_first_unsorted")
+    return int(res.item())
+
+
+def verify_sorted_permutation(arena: StringArena, original, result) -> VerifyResult:
+    """Permutation + sortedness check (strings.py:221-234), on the device."""
+    import torch
+    dev = _dev()
+    if len(original) != len(result):
+        return VerifyResult(False, "not_permutation", int(result[0]) if len(result) else -1)
+    a = torch.sort(_to_dev_handles(original, dev)).values
+    b = torch.sort(_to_dev_handles(result, dev)).values
+    diff = torch.nonzero(a != b)
+    if diff.numel():
+        return VerifyResult(False, "not_permutation", int(b[diff[0, 0]].item()))
+    bad = first_unsorted(arena, result)
+    if bad >= 0:
+        return VerifyResult(False, "not_sorted", bad)
+    return VerifyResult(True)
+
+
+def string_lengths(arena: StringArena, handles):
+    """Distance from every handle to its terminator (strings.py:85-96, 249-253)."""
+    import torch
+    dev = handles.device if isinstance(handles, torch.Tensor) and handles.is_cuda else _dev()
+    h = _to_dev_handles(handles, dev)
+    zeros = torch.nonzero(arena.device(dev)[: arena.data.size] == 0).flatten()
+    nxt = zeros[torch.searchsorted(zeros, h)]
+    out = nxt - h
+    if isinstance(handles, torch.Tensor) and handles.is_cuda:
+        return out
+    return out.cpu().numpy()
+
+
+def distinguishing_prefix(arena: StringArena, sorted_handles, lcp_arr=None) -> int:
+    """D = sum min(|s|+1, max(lcp_prev, lcp_next)+1) over a sorted order
+    (compute_stats, strings.py:256-284); uses a given LCP array if supplied."""
+    import torch
+    dev = _dev()
+    h = _to_dev_handles(sorted_handles, dev)
+    n = h.numel()
+    if n == 0:
+        raise EmptyInput("compute_stats needs at least one string")
+    lens = string_lengths(arena, h)
+    if n == 1:
+        return int(min(int(lens[0].item()) + 1, 1))
+    if lcp_arr is None:
+        lcp_arr = adjacent_lcps(arena, h)
+    l = _to_dev_handles(lcp_arr, dev)
+    best = torch.zeros(n, dtype=torch.int64, device=dev)
+    best[:-1] = l
+    best[1:] = torch.maximum(best[1:], l)
+    return int(torch.minimum(lens + 1, best + 1).sum().item())
+
+
+def compute_stats(arena: StringArena, handles, sorted_handles=None) -> DatasetStats:
+    """n, N, D, sigma, mean length (strings.py:256-284); sorts on the GPU if needed."""
+    n = int(len(handles))
+    if n == 0:
+        raise EmptyInput("compute_stats needs at least one string")
+    lens = string_lengths(arena, handles)
+    lens = lens.cpu().numpy() if hasattr(lens, "cpu") else lens
+    total = int(lens.sum()) + n
+    if sorted_handles is None:
+        from .samplesort import parallel_sample_sort
+        sorted_handles = np.array(handles, np.int64, copy=True)
+        parallel_sample_sort(arena, sorted_handles)
+    D = distinguishing_prefix(arena, sorted_handles)
+    return DatasetStats(n, total, D, arena.sigma, float(lens.mean()))

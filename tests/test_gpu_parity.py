@@ -1,0 +1,217 @@
+"""Parity of the B200 library (libs5.so through its C-ABI) with the reference.
+
+Golden fixtures were produced by the reference package itself
+(tests/golden/make_golden.py); larger inputs are checked against the CPU
+oracle (oracle/, pinned to the reference in test_oracle_golden.py); full-size
+configurations against the reference's published digests
+and size-independent properties.  Integer path: every comparison is exact.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1305_1157_b200 import (SampleSortConfig, StringArena, adjacent_lcps, compute_stats,
+                                  datasets, distinguishing_prefix, first_unsorted, pack_keys,
+                                  parallel_sample_sort, sample_sort, sort_with_lcp,
+                                  verify_sorted_permutation)
+from paper_1305_1157_b200 import classifier as CL
+from paper_1305_1157_b200 import Counters
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = {
+    "default": SampleSortConfig(),
+    "equal": SampleSortConfig(classifier="equal"),
+    "tiny_tiers": SampleSortConfig(v=15, small_max=8, narrow_max=64, seed=3),
+    "wide_everywhere": SampleSortConfig(v=255, small_max=32, narrow_max=32, seed=5),
+    "alpha8": SampleSortConfig(v=1023, alpha=8, small_max=16, narrow_max=2048),
+}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    yield
+
+
+def _check_sorted(arena, h0, got, want_sorted=None, got_lcp=None, want_lcp=None, name=""):
+    assert np.array_equal(np.sort(got), np.sort(h0)), f"{name}: not a permutation"
+    if want_sorted is not None:
+        assert O.contents_equal(arena, got, want_sorted), f"{name}: string sequence differs"
+    else:
+        assert O.first_unsorted(arena, got) == -1, f"{name}: not sorted"
+    if want_lcp is not None:
+        assert np.array_equal(got_lcp, want_lcp), f"{name}: LCP differs"
+
+
+@pytest.mark.parametrize("cfg_name", list(CONFIGS))
+def test_sort_matches_reference_golden(sort_cases, cfg_name):
+    cfg = CONFIGS[cfg_name]
+    for name, c in sort_cases.items():
+        arena = StringArena(c["arena"])
+        h = c["handles"].copy()
+        h2, lcp = sort_with_lcp(arena, h, cfg=cfg)
+        assert h2 is h
+        _check_sorted(arena, c["handles"], h, c["sorted"], lcp, c["lcp"], f"{cfg_name}/{name}")
+        if h.size:
+            assert distinguishing_prefix(arena, h, lcp) == int(c["D"]), name
+
+
+def test_sample_sort_entry_and_counters(sort_cases):
+    c = sort_cases["random_20000"]
+    arena = StringArena(c["arena"])
+    h = c["handles"].copy()
+    ctr = Counters()
+    sample_sort(arena, h, cfg=SampleSortConfig(v=63), counters=ctr)
+    assert O.contents_equal(arena, h, c["sorted"])
+    assert ctr.get("parallel_steps") >= 1 and ctr.get("fetches") >= h.size
+    h = c["handles"].copy()
+    parallel_sample_sort(arena, h, 8)
+    assert O.contents_equal(arena, h, c["sorted"])
+
+
+def test_device_resident_handles(sort_cases):
+    import torch
+    c = sort_cases["harness_random_50000"]
+    arena = StringArena(c["arena"])
+    d = torch.from_numpy(c["handles"].copy()).cuda()
+    lcp = torch.empty(d.numel() - 1, dtype=torch.int64, device="cuda")
+    parallel_sample_sort(arena, d, lcp_out=lcp)
+    got = d.cpu().numpy()
+    _check_sorted(arena, c["handles"], got, c["sorted"], lcp.cpu().numpy(), c["lcp"])
+
+
+def test_sort_from_depth():
+    # sample_sort's depth argument: all strings share the first `depth` bytes
+    rng = np.random.default_rng(3)
+    strs = [b"prefix" + bytes(rng.integers(97, 100, rng.integers(0, 9)).tolist()) for _ in range(5000)]
+    from paper_1305_1157_b200 import arena_from_strings
+    arena, h = arena_from_strings(strs)
+    want = np.asarray(h)[np.argsort(np.array(strs, dtype=object), kind="stable")]
+    lcp = np.empty(h.size - 1, np.int64)
+    sample_sort(arena, h, depth=6, lcp_out=lcp)
+    assert O.contents_equal(arena, h, want)
+    assert np.array_equal(lcp, O.adjacent_lcps(arena, h))
+
+
+def test_tiny_inputs():
+    from paper_1305_1157_b200 import arena_from_strings
+    for n in (0, 1, 2, 3, 10, 31, 32, 33, 64, 65):
+        strs = [bytes([97 + (i * 7) % 5]) * ((i * 3) % 4) for i in range(n)]
+        arena, h = arena_from_strings(strs)
+        parallel_sample_sort(arena, h)
+        raw = arena.data.tobytes()
+        got = [raw[x:raw.index(0, x)] for x in h]
+        assert got == sorted(strs), n
+
+
+def test_pack_keys_matches_reference():
+    from conftest import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "pack_keys.npz"))
+    arena = StringArena(z["arena"])
+    for depth in range(17):
+        got = pack_keys(arena, z[f"d{depth}__handles"], depth)
+        assert np.array_equal(got, z[f"d{depth}__keys"]), depth
+
+
+def test_adjacent_lcp_and_verify_match_reference(sort_cases):
+    for name, c in sort_cases.items():
+        arena = StringArena(c["arena"])
+        assert np.array_equal(adjacent_lcps(arena, c["sorted"]), c["lcp"]), name
+        assert first_unsorted(arena, c["sorted"]) == -1
+        assert verify_sorted_permutation(arena, c["handles"], c["sorted"]).ok
+    c = sort_cases["random_1000"]
+    arena = StringArena(c["arena"])
+    bad = c["sorted"].copy()
+    bad[[3, 700]] = bad[[700, 3]]
+    r = verify_sorted_permutation(arena, c["handles"], bad)
+    assert not r.ok and r.reason == "not_sorted" and r.index == O.first_unsorted(arena, bad)
+    bad = c["sorted"].copy()
+    bad[0] = bad[1]
+    assert verify_sorted_permutation(arena, c["handles"], bad).reason == "not_permutation"
+
+
+def test_classifier_and_tree_match_reference(classifier_cases):
+    for name, c in classifier_cases.items():
+        spl = c["splitters"]
+        if name != "cterm":
+            lo, io = CL.build_tree_from_sample(c["sample"], spl.size)
+            assert np.array_equal(io, spl), name
+            assert np.array_equal(lo[1:], c["level_order"][1:]), name
+        tree = CL.build_tree(spl)
+        assert np.array_equal(tree.level_order, c["level_order"])
+        assert np.array_equal(tree.splitter_lcp, c["splitter_lcp"])
+        want = c["buckets"]
+        assert np.array_equal(CL.classify_tree_unrolled(c["keys"], tree).astype(np.int64), want), name
+        assert np.array_equal(CL.classify_tree_equal(c["keys"], tree).astype(np.int64), want), name
+
+
+def test_classifier_exhaustive_small_trees():
+    # test_classifier.py:181-196 shape: v in {1,3,7}, adversarial keys, duplicate splitters
+    rng = np.random.default_rng(11)
+    for v in (1, 3, 7, 15):
+        for dup in (False, True):
+            for _ in range(20):
+                pool = rng.integers(1, 40, v).astype(np.uint64)
+                if dup and v > 1:
+                    pool[rng.integers(0, v)] = pool[0]
+                spl = np.sort(pool)
+                keys = set()
+                for x in spl.tolist():
+                    keys.update((x, max(0, x - 1), x + 1))
+                keys.update((0, 2**64 - 1))
+                keys = np.asarray(sorted(keys), np.uint64)
+                want = O.classify_oracle(keys, spl)
+                tree = CL.build_tree(spl)
+                assert np.array_equal(CL.classify_tree_unrolled(keys, tree).astype(np.int64), want)
+                assert np.array_equal(CL.classify_tree_equal(keys, tree).astype(np.int64), want)
+
+
+@pytest.mark.parametrize("config,n", [(1, None), (2, 1 << 20), (3, 1 << 19), (4, 1 << 19),
+                                      (5, 1 << 20)])
+def test_configs_reduced_vs_oracle(config, n):
+    arena, h0 = datasets.generate(config, n)
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, O.max_threads())
+    want_lcp = O.adjacent_lcps(arena, want)
+    for cfg in (SampleSortConfig(), SampleSortConfig(classifier="equal", seed=9)):
+        h = h0.copy()
+        _, lcp = sort_with_lcp(arena, h, cfg=cfg)
+        _check_sorted(arena, h0, h, want, lcp, want_lcp, f"cfg{config}")
+        if config == 5:
+            assert np.array_equal(h, want)  # no duplicates: permutation is unique
+
+
+def test_config1_reference_digests():
+    arena, h = datasets.generate(1)
+    _, lcp = sort_with_lcp(arena, h)
+    ds, dl = datasets.DIGESTS[1]
+    assert O.digest_strings(arena, h)[:16] == ds
+    assert O.digest_lcp(lcp)[:16] == dl
+    assert distinguishing_prefix(arena, h, lcp) == datasets.EXPECTED[1][2]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("config", [2, 3, 4, 5])
+def test_full_config_reference_digests(config):
+    """Full BASELINE sizes: digests of the reference's output + properties."""
+    import torch
+    arena, h0 = datasets.generate(config)
+    n, N, D = datasets.EXPECTED[config]
+    assert h0.size == n and arena.data.size == N
+    d = torch.from_numpy(h0).cuda()
+    lcp = torch.empty(n - 1, dtype=torch.int64, device="cuda")
+    parallel_sample_sort(arena, d, lcp_out=lcp)
+    assert first_unsorted(arena, d) == -1
+    assert torch.equal(torch.sort(d).values, torch.from_numpy(h0).cuda())
+    assert torch.equal(adjacent_lcps(arena, d), lcp)   # independent LCP kernel
+    assert distinguishing_prefix(arena, d, lcp) == D
+    got = d.cpu().numpy()
+    ds, dl = datasets.DIGESTS[config]
+    assert O.digest_lcp(lcp.cpu().numpy())[:16] == dl
+    assert O.digest_strings(arena, got, 63 if config == 5 else -1)[:16] == ds
+    del arena
