@@ -51,7 +51,7 @@ typedef struct {
     uint32_t classifier;  /* 0 = "unroll", 1 = "equal" (samplesort.py:43)      */
     uint32_t small_max;   /* segments <= small_max: warp base case (<= 32)      */
     uint32_t narrow_max;  /* segments <= narrow_max: one-CTA S^5 step (<=16384) */
-    uint32_t flags;       /* bit0: skip LCP fix-up (debug)                      */
+    uint32_t flags;       /* bit0: skip LCP fix-up (debug); bit1: per-kernel timing */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
 } s5_config;
 
@@ -69,9 +69,20 @@ typedef struct {
     uint64_t small_segments;             /* base-case segments                    */
     uint64_t key_fetches;                /* arena key gathers (fetches counter)   */
     uint64_t boundary_lcps;              /* LCPs finished by the boundary kernel  */
+    uint64_t launches;                   /* kernels launched by the call          */
     float ms_total;                      /* device time of the call (CUDA events) */
     float pad2_;
+    /* cfg->flags bit1: per-kernel device time (CUDA events around every
+     * launch, same stream), indexed by S5_K_* */
+    float kern_ms[16];
+    uint32_t kern_launches[16];
 } s5_stats;
+
+enum {
+    S5_K_GATHER = 0, S5_K_WIDE_PLAN, S5_K_WIDE_TREE, S5_K_WIDE_COUNT, S5_K_WIDE_COLSCAN,
+    S5_K_WIDE_BSCAN, S5_K_WIDE_SCATTER, S5_K_NARROW, S5_K_SMALL, S5_K_LCP_FIX, S5_K_INIT,
+    S5_K_COUNT
+};
 
 /* Bytes of device workspace s5_sort needs for n strings. */
 uint64_t s5_workspace_bytes(uint64_t n, uint64_t arena_len, const s5_config *cfg);
@@ -84,6 +95,20 @@ uint64_t s5_workspace_bytes(uint64_t n, uint64_t arena_len, const s5_config *cfg
 int s5_sort(const uint8_t *d_arena, uint64_t arena_len, int64_t *d_handles, uint64_t n,
             uint64_t depth, int64_t *d_lcp, const s5_config *cfg, void *d_workspace,
             uint64_t workspace_bytes, void *stream, s5_stats *stats);
+
+/* Debug variant honouring the reference's audit hook (samplesort.py:235-236,
+ * :431-432): after every level, fn receives the child segments the level
+ * emitted ({begin, size, depth, side}) and host copies of both ping-pong
+ * offset arrays; segment i's strings are side_k[begin .. begin+size) with
+ * k = side, all sharing `depth` leading bytes (Eq. (1)). Slow: copies 8n bytes
+ * per level. */
+typedef struct { uint32_t begin, size, depth, side; } s5_segment;
+typedef void (*s5_audit_fn)(void *user, uint32_t level, const s5_segment *segs, uint64_t nsegs,
+                            const uint32_t *side0, const uint32_t *side1, uint64_t n);
+int s5_sort_audit(const uint8_t *d_arena, uint64_t arena_len, int64_t *d_handles, uint64_t n,
+                  uint64_t depth, int64_t *d_lcp, const s5_config *cfg, void *d_workspace,
+                  uint64_t workspace_bytes, void *stream, s5_stats *stats, s5_audit_fn fn,
+                  void *user);
 
 /* Same with host buffers: uploads handles, sorts, downloads handles + LCP.
  * The arena must already be on the device (d_arena). Allocates its own

@@ -42,7 +42,9 @@ class S5Stats(C.Structure):
                 ("small_elems", C.c_uint64 * S5_MAX_LEVELS),
                 ("wide_steps", C.c_uint64), ("narrow_steps", C.c_uint64),
                 ("small_segments", C.c_uint64), ("key_fetches", C.c_uint64),
-                ("boundary_lcps", C.c_uint64), ("ms_total", C.c_float), ("pad2_", C.c_float)]
+                ("boundary_lcps", C.c_uint64), ("launches", C.c_uint64),
+                ("ms_total", C.c_float), ("pad2_", C.c_float),
+                ("kern_ms", C.c_float * 16), ("kern_launches", C.c_uint32 * 16)]
 
     def as_dict(self) -> dict:
         L = min(self.levels, S5_MAX_LEVELS)
@@ -55,17 +57,35 @@ class S5Stats(C.Structure):
             "wide_steps": int(self.wide_steps), "narrow_steps": int(self.narrow_steps),
             "small_segments": int(self.small_segments), "key_fetches": int(self.key_fetches),
             "boundary_lcps": int(self.boundary_lcps), "ms_total": float(self.ms_total),
+            "launches": int(self.launches),
+            "kernels": {KERNELS[i]: {"ms": float(self.kern_ms[i]),
+                                     "launches": int(self.kern_launches[i])}
+                        for i in range(len(KERNELS)) if self.kern_launches[i]},
         }
 
+
+KERNELS = ["k_gather", "k_wide_plan", "k_wide_tree", "k_wide_count", "k_wide_colscan",
+           "k_wide_bscan", "k_wide_scatter", "k_narrow", "k_small", "k_lcp_fix", "k_init_root"]
 
 _vp = C.c_void_p
 _u64 = C.c_uint64
 _u32 = C.c_uint32
 
+
+class S5Segment(C.Structure):
+    _fields_ = [("begin", C.c_uint32), ("size", C.c_uint32), ("depth", C.c_uint32),
+                ("side", C.c_uint32)]
+
+
+AUDIT_FN = C.CFUNCTYPE(None, _vp, _u32, C.POINTER(S5Segment), _u64, C.POINTER(_u32),
+                       C.POINTER(_u32), _u64)
+
 SIGNATURES = {
     "s5_workspace_bytes": (_u64, [_u64, _u64, C.POINTER(S5Config)]),
     "s5_sort": (C.c_int, [_vp, _u64, _vp, _u64, _u64, _vp, C.POINTER(S5Config), _vp, _u64, _vp,
                           C.POINTER(S5Stats)]),
+    "s5_sort_audit": (C.c_int, [_vp, _u64, _vp, _u64, _u64, _vp, C.POINTER(S5Config), _vp, _u64,
+                                _vp, C.POINTER(S5Stats), AUDIT_FN, _vp]),
     "s5_sort_host": (C.c_int, [_vp, _u64, _vp, _u64, _vp, C.POINTER(S5Config), _vp,
                                C.POINTER(S5Stats)]),
     "s5_pack_keys": (C.c_int, [_vp, _u64, _vp, _u64, _u64, _vp, _vp]),

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/s5.h"
 #include "s5_kernels.cuh"
@@ -152,6 +153,45 @@ int grid_for(uint64_t n, int threads, int max_blocks = 148 * 16) {
     return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(b, max_blocks)));
 }
 
+// Launch bookkeeping; with cfg flags bit1, CUDA events around every launch
+// give per-kernel device time on the launching stream.
+struct Prof {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    uint64_t launches = 0;
+    uint32_t count[16] = {};
+    struct Rec { int k; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+    void begin(int k) {
+        ++launches;
+        ++count[k];
+        if (!on) return;
+        Rec r{k, nullptr, nullptr};
+        cudaEventCreate(&r.a);
+        cudaEventCreate(&r.b);
+        cudaEventRecord(r.a, st);
+        recs.push_back(r);
+    }
+    void end() {
+        if (on && !recs.empty()) cudaEventRecord(recs.back().b, st);
+    }
+    void finish(s5_stats* stats) {
+        if (stats) {
+            stats->launches = launches;
+            for (int k = 0; k < 16; ++k) stats->kern_launches[k] = count[k];
+        }
+        for (auto& r : recs) {
+            float ms = 0;
+            if (stats && cudaEventSynchronize(r.b) == cudaSuccess &&
+                cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess)
+                stats->kern_ms[r.k] += ms;
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        recs.clear();
+    }
+};
+
 }  // namespace
 
 extern "C" {
@@ -167,9 +207,10 @@ uint64_t s5_workspace_bytes(uint64_t n, uint64_t arena_len, const s5_config* cfg
     return make_layout(n, c).total;
 }
 
-int s5_sort(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles, uint64_t n,
-            uint64_t depth, int64_t* d_lcp, const s5_config* cfg, void* d_ws, uint64_t ws_bytes,
-            void* stream_, s5_stats* stats) {
+static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles, uint64_t n,
+                     uint64_t depth, int64_t* d_lcp, const s5_config* cfg, void* d_ws,
+                     uint64_t ws_bytes, void* stream_, s5_stats* stats, s5_audit_fn audit,
+                     void* audit_user) {
     Cfg c;
     if (int rc = resolve(cfg, &c)) return rc;
     if (stats) memset(stats, 0, sizeof(*stats));
@@ -229,9 +270,16 @@ int s5_sort(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles, uint
     int cur = 0;
     for (int q = 0; q < 3; ++q) A.next[q] = reinterpret_cast<Seg*>(ws + L.lists[cur][q]);
     S5_CUDA(cudaMemsetAsync(A.ctl, 0, sizeof(Ctl), st));
+    Prof prof;
+    prof.on = stats && (c.flags & 2);
+    prof.st = st;
+    prof.begin(S5_K_GATHER);
     k_gather<<<grid_for(n, 256), 256, 0, st>>>(d_handles, static_cast<uint32_t>(n), depth,
                                                 arena_len, A);
+    prof.end();
+    prof.begin(S5_K_INIT);
     k_init_root<<<1, 32, 0, st>>>(A, static_cast<uint32_t>(n), static_cast<uint32_t>(depth));
+    prof.end();
     S5_CUDA(cudaGetLastError());
 
     unsigned long long fetches_total = 0, hints_total = 0;
@@ -248,6 +296,24 @@ int s5_sort(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles, uint
         uint32_t m[3] = {h.n_list[0], h.n_list[1], h.n_list[2]};
         if (!m[0] && !m[1] && !m[2]) break;
         if (level >= 100000) return fail(S5_E_INTERNAL, "no progress");
+        if (audit && level > 0) {
+            // debug replay of the reference's audit hook (samplesort.py:235-236, :431-432):
+            // the children emitted by the previous level, with both sides' offsets
+            std::vector<Seg> hs(uint64_t(m[0]) + m[1] + m[2]);
+            std::vector<uint32_t> side0(n), side1(n);
+            uint64_t at = 0;
+            for (int q = 0; q < 3; ++q) {
+                if (m[q])
+                    S5_CUDA(cudaMemcpyAsync(hs.data() + at, ws + L.lists[cur][q],
+                                            uint64_t(m[q]) * sizeof(Seg), cudaMemcpyDeviceToHost, st));
+                at += m[q];
+            }
+            S5_CUDA(cudaMemcpyAsync(side0.data(), A.off[0], n * 4, cudaMemcpyDeviceToHost, st));
+            S5_CUDA(cudaMemcpyAsync(side1.data(), A.off[1], n * 4, cudaMemcpyDeviceToHost, st));
+            S5_CUDA(cudaStreamSynchronize(st));
+            audit(audit_user, level, reinterpret_cast<const s5_segment*>(hs.data()), hs.size(),
+                  side0.data(), side1.data(), n);
+        }
         if (stats && level < S5_MAX_LEVELS) {
             stats->wide_elems[level] = h.elems[WIDE];
             stats->narrow_elems[level] = h.elems[NARROW];
@@ -267,37 +333,55 @@ int s5_sort(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles, uint
         if (m[WIDE]) {
             P.segs = segs[WIDE];
             P.nsegs = m[WIDE];
+            prof.begin(S5_K_WIDE_PLAN);
             k_wide_plan<<<1, 1024, 0, st>>>(A, P);
+            prof.end();
+            prof.begin(S5_K_WIDE_TREE);
             k_wide_tree<<<m[WIDE], kWideThreads, kWideTreeSmem, st>>>(A, P);
+            prof.end();
             // upper bound on CTAs; surplus CTAs exit on ctl->wide_ctas
             uint32_t ub = static_cast<uint32_t>(std::min<uint64_t>(
                 uint64_t(m[WIDE]) * kWideCtasMax, n / kWideChunkMin + m[WIDE]));
+            prof.begin(S5_K_WIDE_COUNT);
             if (c.classifier)
                 k_wide_count<true><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
             else
                 k_wide_count<false><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
+            prof.end();
             dim3 cg(m[WIDE], ((2u << std::min(c.dmax, kWideDMax)) + 1023) / 1024);
+            prof.begin(S5_K_WIDE_COLSCAN);
             k_wide_colscan<<<cg, 1024, 0, st>>>(A, P);
+            prof.end();
+            prof.begin(S5_K_WIDE_BSCAN);
             k_wide_bscan<<<m[WIDE], 1024, 0, st>>>(A, P);
+            prof.end();
+            prof.begin(S5_K_WIDE_SCATTER);
             if (c.classifier)
                 k_wide_scatter<true><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
             else
                 k_wide_scatter<false><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
+            prof.end();
         }
         if (m[NARROW]) {
+            prof.begin(S5_K_NARROW);
             if (c.classifier)
                 k_narrow<true><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
             else
                 k_narrow<false><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
+            prof.end();
         }
         if (m[SMALL]) {
             uint32_t blocks = (m[SMALL] + 7) / 8;
+            prof.begin(S5_K_SMALL);
             k_small<<<blocks, 256, 0, st>>>(A, segs[SMALL], m[SMALL]);
+            prof.end();
         }
         S5_CUDA(cudaGetLastError());
     }
     if (d_lcp && !(c.flags & 1)) {
+        prof.begin(S5_K_LCP_FIX);
         k_lcp_fix<<<grid_for(n - 1, 256), 256, 0, st>>>(d_arena, d_handles, d_lcp, n - 1);
+        prof.end();
         S5_CUDA(cudaGetLastError());
     }
     if (stats) {
@@ -310,7 +394,22 @@ int s5_sort(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles, uint
         stats->key_fetches = fetches_total;
         stats->boundary_lcps = hints_total;
     }
+    prof.finish(stats);
     return 0;
+}
+
+int s5_sort(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles, uint64_t n,
+            uint64_t depth, int64_t* d_lcp, const s5_config* cfg, void* d_ws, uint64_t ws_bytes,
+            void* stream, s5_stats* stats) {
+    return sort_impl(d_arena, arena_len, d_handles, n, depth, d_lcp, cfg, d_ws, ws_bytes, stream,
+                     stats, nullptr, nullptr);
+}
+
+int s5_sort_audit(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles, uint64_t n,
+                  uint64_t depth, int64_t* d_lcp, const s5_config* cfg, void* d_ws,
+                  uint64_t ws_bytes, void* stream, s5_stats* stats, s5_audit_fn fn, void* user) {
+    return sort_impl(d_arena, arena_len, d_handles, n, depth, d_lcp, cfg, d_ws, ws_bytes, stream,
+                     stats, fn, user);
 }
 
 int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles, uint64_t n,

@@ -1,0 +1,234 @@
+"""Multi-GPU S^5: one process per GPU, sample-sort partitioning over NCCL.
+
+SURVEY.md 8(e).  The arena is replicated on every rank; rank g holds a
+contiguous shard of the handles.  One exchange step turns the shards into
+contiguous slices of the global sorted order:
+
+1. every rank draws ``oversample * G`` sample handles from its shard;
+   ``all_gather`` of the sample handles (the arena is replicated, so
+   handles are enough);
+2. every rank sorts all samples by full string content with a
+   (string, handle) tie-break, so identical strings may be split across
+   ranks (their order is free: the reference is not stable), and picks the
+   same G-1 splitters;
+3. every local string is classified to a destination rank by binary search
+   over the splitters with full-string comparison (8-byte keys at
+   increasing depth, only undecided pairs reload);
+4. ``all_to_all_single`` of the per-destination counts, then of the
+   handles (NCCL over NVLink on GPUs; gloo in the CPU tests);
+5. each rank sorts its received strings with the single-GPU sorter and
+   emits their LCP array;
+6. the LCP across each rank boundary is one string comparison (the next
+   rank's first handle is all-gathered).
+
+The string primitives come from a backend: ``GpuBackend`` (libs5.so; the
+product path) or, in the CPU tests only, an oracle-backed stand-in injected
+by the test.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+class GpuBackend:
+    """String primitives on the local GPU (libs5.so)."""
+
+    def __init__(self, arena, cfg=None):
+        import torch
+        self.arena = arena
+        self.cfg = cfg
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        arena.device(self.device)
+
+    def pack_keys(self, handles, depth: int):
+        from .strings import pack_keys
+        k = pack_keys(self.arena, handles, depth)
+        return k.view(handles.dtype) if k.dtype != handles.dtype else k
+
+    def lengths(self, handles):
+        from .strings import string_lengths
+        return string_lengths(self.arena, handles)
+
+    def sort(self, handles):
+        """Sort a device int64 tensor in place; returns (handles, lcp)."""
+        import torch
+        from .samplesort import gpu_sort
+        n = handles.numel()
+        lcp = torch.empty(max(n - 1, 0), dtype=torch.int64, device=handles.device)
+        if n > 1:
+            gpu_sort(self.arena, handles, 0, self.cfg, lcp)
+        return handles, lcp
+
+
+def _u64_less(a, b):
+    """Unsigned a < b for int64 tensors holding uint64 bit patterns."""
+    import torch
+    sign = torch.tensor(-(1 << 63), dtype=torch.int64, device=a.device)
+    return (a ^ sign) < (b ^ sign)
+
+
+def compare_strings(backend, a, b):
+    """Three-way compare of strings a[i] vs b[i] with (string, handle)
+    tie-break: -1, 0, +1 per element (strings.py:64-74 order, extended)."""
+    import torch
+    out = torch.zeros(a.numel(), dtype=torch.int64, device=a.device)
+    live = torch.arange(a.numel(), device=a.device)
+    depth = 0
+    while live.numel():
+        ka = backend.pack_keys(a[live], depth)
+        kb = backend.pack_keys(b[live], depth)
+        lt = _u64_less(ka, kb)
+        gt = _u64_less(kb, ka)
+        out[live[lt]] = -1
+        out[live[gt]] = 1
+        eq = ~(lt | gt)
+        # equal keys containing the terminator: identical strings -> tie-break
+        w = ka[eq]
+        zero = torch.zeros_like(w, dtype=torch.bool)
+        for s in range(8):
+            zero |= ((w >> (56 - 8 * s)) & 0xFF) == 0
+        idx = live[eq]
+        term = idx[zero]
+        out[term] = torch.sign(a[term] - b[term])
+        live = idx[~zero]
+        depth += 8
+    return out
+
+
+@dataclass
+class ShardResult:
+    handles: object       # this rank's slice of the global sorted order
+    lcp: object           # LCPs of the slice plus the one across the next boundary
+    offset: int           # global index of handles[0]
+    counts: list          # slice sizes of all ranks
+
+
+def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 64,
+                            seed: int = 1, backend=None) -> ShardResult:
+    """Globally sort the union of every rank's ``local_handles``.
+
+    Returns this rank's contiguous slice of the global order and its LCP
+    array: ``lcp[i]`` is the LCP of slice[i] and slice[i+1], and the last
+    entry (absent on the last nonempty rank) is the LCP of slice[-1] and
+    the next rank's first string, so concatenating all ranks' ``lcp``
+    gives the global LCP array of length n-1.
+    """
+    import torch
+    import torch.distributed as dist
+
+    G = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    be = backend or GpuBackend(arena)
+    dev = local_handles.device
+    h = local_handles.contiguous()
+    n_local = h.numel()
+
+    # 1. samples (with replacement, seeded per rank) -> all_gather
+    s = oversample * G
+    gen = torch.Generator(device="cpu").manual_seed(seed * 1_000_003 + rank)
+    if n_local:
+        pick = torch.randint(0, n_local, (s,), generator=gen).to(dev)
+        samp = h[pick]
+    else:
+        samp = torch.full((s,), -1, dtype=torch.int64, device=dev)
+    gathered = [torch.empty_like(samp) for _ in range(G)]
+    dist.all_gather(gathered, samp, group=group)
+    allsamp = torch.cat(gathered)
+    allsamp = allsamp[allsamp >= 0]
+
+    # 2. identical splitters on every rank: sort by (string, handle)
+    splitters = _pick_splitters(be, allsamp, G)
+
+    # 3. destination of every local string
+    dest = torch.zeros(n_local, dtype=torch.int64, device=dev)
+    if n_local and splitters.numel():
+        lo = torch.zeros(n_local, dtype=torch.int64, device=dev)
+        hi = torch.full((n_local,), splitters.numel(), dtype=torch.int64, device=dev)
+        while True:
+            active = lo < hi
+            if not bool(active.any()):
+                break
+            idx = torch.nonzero(active).flatten()
+            mid = (lo[idx] + hi[idx]) // 2
+            c = compare_strings(be, splitters[mid], h[idx])   # splitter < string ?
+            right = c < 0
+            lo[idx[right]] = mid[right] + 1
+            hi[idx[~right]] = mid[~right]
+        dest = lo
+    order = torch.argsort(dest, stable=True)
+    send = h[order]
+    send_counts = torch.bincount(dest, minlength=G).to(torch.int64)
+
+    # 4. exchange counts, then handles
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    recv = torch.empty(int(recv_counts.sum().item()), dtype=torch.int64, device=dev)
+    dist.all_to_all_single(recv, send, output_split_sizes=recv_counts.tolist(),
+                           input_split_sizes=send_counts.tolist(), group=group)
+
+    # 5. local sort + LCP
+    recv, lcp = be.sort(recv)
+
+    # 6. boundary LCPs and global offsets
+    sizes = torch.tensor([recv.numel()], dtype=torch.int64, device=dev)
+    all_sizes = [torch.empty_like(sizes) for _ in range(G)]
+    dist.all_gather(all_sizes, sizes, group=group)
+    counts = [int(x.item()) for x in all_sizes]
+    first = recv[:1] if recv.numel() else torch.full((1,), -1, dtype=torch.int64, device=dev)
+    firsts = [torch.empty_like(first) for _ in range(G)]
+    dist.all_gather(firsts, first, group=group)
+    nxt = None
+    for r in range(rank + 1, G):
+        if counts[r]:
+            nxt = firsts[r]
+            break
+    if recv.numel() and nxt is not None:
+        pair = torch.cat([recv[-1:], nxt])
+        bl = _lcp_pair(be, pair)
+        lcp = torch.cat([lcp, bl])
+    offset = sum(counts[:rank])
+    return ShardResult(recv, lcp, offset, counts)
+
+
+def _lcp_pair(be, pair):
+    import torch
+    depth = 0
+    while True:
+        k = be.pack_keys(pair, depth)
+        if int(k[0].item()) != int(k[1].item()):
+            x = (int(k[0].item()) ^ int(k[1].item())) & ((1 << 64) - 1)
+            return torch.tensor([depth + (64 - x.bit_length()) // 8], dtype=torch.int64,
+                                device=pair.device)
+        w = int(k[0].item()) & ((1 << 64) - 1)
+        b = w.to_bytes(8, "big")
+        if 0 in b:
+            return torch.tensor([depth + b.index(0)], dtype=torch.int64, device=pair.device)
+        depth += 8
+
+
+def _pick_splitters(be, samples, G: int):
+    """G-1 evenly spaced samples of the (string, handle)-sorted sample set."""
+    import torch
+    if G <= 1 or samples.numel() == 0:
+        return samples[:0]
+    s = samples.clone()
+    s, lcp = be.sort(s)
+    # identical strings: order by handle so every rank picks the same splitters
+    lens = be.lengths(s)
+    if s.numel() > 1:
+        same = (lcp == lens[:-1]) & (lcp == lens[1:])
+        run = torch.cat([torch.zeros(1, dtype=torch.int64, device=s.device),
+                         torch.cumsum((~same).to(torch.int64), 0)])
+        key = run * 0  # stable two-key sort: by handle, then by run
+        order = torch.argsort(s, stable=True)
+        s, run = s[order], run[order]
+        order = torch.argsort(run, stable=True)
+        s = s[order]
+        del key
+    m = s.numel()
+    idx = torch.tensor([(j + 1) * m // G for j in range(G - 1)], dtype=torch.int64,
+                       device=s.device).clamp(max=m - 1)
+    return s[idx]

@@ -215,3 +215,54 @@ def test_full_config_reference_digests(config):
     assert O.digest_lcp(lcp.cpu().numpy())[:16] == dl
     assert O.digest_strings(arena, got, 63 if config == 5 else -1)[:16] == ds
     del arena
+
+
+def _random_strings(n, seed, max_len=20, lo=33, hi=127):
+    # helpers.random_strings (pkg/tests/helpers.py:134-138) shape, vectorised
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(0, max_len, n)
+    body = rng.integers(lo, hi, int(lens.sum())).astype(np.uint8).tobytes()
+    out, at = [], 0
+    for ln in lens.tolist():
+        out.append(body[at:at + ln])
+        at += ln
+    return out
+
+
+@pytest.mark.parametrize("cfg", [SampleSortConfig(v=255, small_max=16, narrow_max=512),
+                                 SampleSortConfig(v=15, small_max=8, narrow_max=32)])
+def test_eq1_audit(cfg):
+    """test_samplesort.py:144-160, :206-225: every child's claimed depth is a
+    lower bound on the pairwise lcp of its strings."""
+    from paper_1305_1157_b200 import arena_from_strings
+    strs = _random_strings(100_000, seed=14)
+    arena, h = arena_from_strings(strs)
+    rng = np.random.default_rng(1)
+    seen, violations = [], []
+
+    def audit(side, lo, hi, depth):
+        seen.append((lo, hi, depth))
+        idx = rng.integers(lo, hi, (min(100, hi - lo), 2))
+        for i, j in idx:
+            if O.lcp(arena, int(side[i]), int(side[j])) < depth:
+                violations.append((lo, hi, depth))
+                return
+
+    orig = h.copy()
+    parallel_sample_sort(arena, h, 2, cfg=cfg, audit=audit)
+    assert violations == []
+    assert seen and all(0 <= lo < hi <= h.size for lo, hi, _ in seen)
+    assert sum(hi - lo for lo, hi, d in seen if d == 0) <= h.size
+    assert O.first_unsorted(arena, h) == -1
+    assert np.array_equal(np.sort(h), np.sort(orig))
+
+
+def test_identical_strings_equality_chain():
+    """test_samplesort.py:126-132 / :228-232: identical 17-char strings walk the
+    equality buckets 0 -> 8 -> 16 and finish on the terminated splitter."""
+    from paper_1305_1157_b200 import arena_from_strings
+    arena, h = arena_from_strings([b"q" * 17] * 100_000)
+    ctr = Counters()
+    _, lcp = sort_with_lcp(arena, h, cfg=SampleSortConfig(v=31), counters=ctr)
+    assert ctr.get("parallel_steps") == 3
+    assert np.all(lcp == 17)
