@@ -110,11 +110,13 @@ int s5_sort_audit(const uint8_t *d_arena, uint64_t arena_len, int64_t *d_handles
                   uint64_t workspace_bytes, void *stream, s5_stats *stats, s5_audit_fn fn,
                   void *user);
 
-/* Same with host buffers: uploads handles, sorts, downloads handles + LCP.
+/* Same with host buffers: uploads handles, sorts, downloads handles + LCP
+ * through two pinned staging chunks (host memcpy overlapped with the DMA).
  * The arena must already be on the device (d_arena). Allocates its own
- * device buffers (cached between calls). */
+ * device buffers (cached between calls); serialised by an internal lock. */
 int s5_sort_host(const uint8_t *d_arena, uint64_t arena_len, int64_t *h_handles, uint64_t n,
-                 int64_t *h_lcp, const s5_config *cfg, void *stream, s5_stats *stats);
+                 uint64_t depth, int64_t *h_lcp, const s5_config *cfg, void *stream,
+                 s5_stats *stats);
 
 /* pack_keys (strings.py:176-182) / _pack_keys (:50-53). */
 int s5_pack_keys(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_handles,

@@ -86,7 +86,7 @@ SIGNATURES = {
                           C.POINTER(S5Stats)]),
     "s5_sort_audit": (C.c_int, [_vp, _u64, _vp, _u64, _u64, _vp, C.POINTER(S5Config), _vp, _u64,
                                 _vp, C.POINTER(S5Stats), AUDIT_FN, _vp]),
-    "s5_sort_host": (C.c_int, [_vp, _u64, _vp, _u64, _vp, C.POINTER(S5Config), _vp,
+    "s5_sort_host": (C.c_int, [_vp, _u64, _vp, _u64, _u64, _vp, C.POINTER(S5Config), _vp,
                                C.POINTER(S5Stats)]),
     "s5_pack_keys": (C.c_int, [_vp, _u64, _vp, _u64, _u64, _vp, _vp]),
     "s5_adjacent_lcp": (C.c_int, [_vp, _u64, _vp, _u64, _vp, _vp]),

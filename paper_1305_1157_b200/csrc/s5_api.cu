@@ -14,6 +14,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/s5.h"
@@ -412,12 +413,50 @@ int s5_sort_audit(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles
                      stats, fn, user);
 }
 
+// Host-buffer entry: handles and LCP move through two pinned staging chunks
+// so the host memcpy of chunk i overlaps the DMA of chunk i-1 (H2D) and the
+// DMA of chunk i+1 overlaps the copy-out of chunk i (D2H).
+namespace {
+
+void par_memcpy(void* dst, const void* src, uint64_t bytes) {
+    const uint64_t kMin = 8ull << 20;
+    unsigned t = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    uint64_t parts = std::min<uint64_t>(t, (bytes + kMin - 1) / kMin);
+    if (parts <= 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    uint64_t per = (bytes + parts - 1) / parts;
+    for (uint64_t p = 0; p < parts; ++p) {
+        uint64_t a = p * per, b = std::min(bytes, a + per);
+        if (a >= b) break;
+        th.emplace_back([=] { memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
+    }
+    for (auto& x : th) x.join();
+}
+
+struct HostPath {
+    std::mutex mu;
+    void* dbuf = nullptr;
+    uint64_t dbytes = 0;
+    void* stage[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    static constexpr uint64_t kChunk = 64ull << 20;
+};
+
+HostPath& host_path() {
+    static HostPath hp;
+    return hp;
+}
+
+}  // namespace
+
 int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles, uint64_t n,
-                 int64_t* h_lcp, const s5_config* cfg, void* stream_, s5_stats* stats) {
-    static std::mutex mu;
-    static void* buf = nullptr;
-    static uint64_t buf_bytes = 0;
-    std::lock_guard<std::mutex> lock(mu);
+                 uint64_t depth, int64_t* h_lcp, const s5_config* cfg, void* stream_,
+                 s5_stats* stats) {
+    HostPath& H = host_path();
+    std::lock_guard<std::mutex> lock(H.mu);
     if (n <= 1) {
         if (stats) memset(stats, 0, sizeof(*stats));
         return 0;
@@ -426,23 +465,69 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
     if (int rc = resolve(cfg, &c)) return rc;
     uint64_t ws = make_layout(n, c).total;
     uint64_t need = align_up(n * 8) + align_up(n * 8) + ws;
-    if (need > buf_bytes) {
-        if (buf) cudaFree(buf);
-        buf = nullptr;
-        buf_bytes = 0;
-        S5_CUDA(cudaMalloc(&buf, need));
-        buf_bytes = need;
+    if (need > H.dbytes) {
+        if (H.dbuf) cudaFree(H.dbuf);
+        H.dbuf = nullptr;
+        H.dbytes = 0;
+        S5_CUDA(cudaMalloc(&H.dbuf, need));
+        H.dbytes = need;
+    }
+    if (!H.stage[0]) {
+        for (int i = 0; i < 2; ++i) {
+            S5_CUDA(cudaHostAlloc(&H.stage[i], HostPath::kChunk, cudaHostAllocDefault));
+            S5_CUDA(cudaEventCreateWithFlags(&H.ev[i], cudaEventDisableTiming));
+        }
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream_);
-    int64_t* dh = static_cast<int64_t*>(buf);
-    int64_t* dl = reinterpret_cast<int64_t*>(static_cast<char*>(buf) + align_up(n * 8));
-    void* dws = static_cast<char*>(buf) + 2 * align_up(n * 8);
-    S5_CUDA(cudaMemcpyAsync(dh, h_handles, n * 8, cudaMemcpyHostToDevice, st));
-    int rc = s5_sort(d_arena, arena_len, dh, n, 0, h_lcp ? dl : nullptr, cfg, dws, ws, stream_,
-                     stats);
+    int64_t* dh = static_cast<int64_t*>(H.dbuf);
+    int64_t* dl = reinterpret_cast<int64_t*>(static_cast<char*>(H.dbuf) + align_up(n * 8));
+    void* dws = static_cast<char*>(H.dbuf) + 2 * align_up(n * 8);
+
+    // H2D of the handles
+    const uint64_t bytes = n * 8;
+    uint64_t i = 0;
+    for (uint64_t off = 0; off < bytes; off += HostPath::kChunk, ++i) {
+        uint64_t len = std::min(HostPath::kChunk, bytes - off);
+        int b = static_cast<int>(i & 1);
+        if (i >= 2) S5_CUDA(cudaEventSynchronize(H.ev[b]));
+        par_memcpy(H.stage[b], reinterpret_cast<const char*>(h_handles) + off, len);
+        S5_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dh) + off, H.stage[b], len,
+                                cudaMemcpyHostToDevice, st));
+        S5_CUDA(cudaEventRecord(H.ev[b], st));
+    }
+    int rc = s5_sort(d_arena, arena_len, dh, n, depth, h_lcp ? dl : nullptr, cfg, dws, ws,
+                     stream_, stats);
     if (rc) return rc;
-    S5_CUDA(cudaMemcpyAsync(h_handles, dh, n * 8, cudaMemcpyDeviceToHost, st));
-    if (h_lcp) S5_CUDA(cudaMemcpyAsync(h_lcp, dl, (n - 1) * 8, cudaMemcpyDeviceToHost, st));
+
+    // D2H of handles then LCP, one DMA ahead of the copy-out
+    struct Piece { const char* d; char* h; uint64_t len; };
+    std::vector<Piece> pieces;
+    for (uint64_t off = 0; off < bytes; off += HostPath::kChunk)
+        pieces.push_back({reinterpret_cast<const char*>(dh) + off,
+                          reinterpret_cast<char*>(h_handles) + off,
+                          std::min(HostPath::kChunk, bytes - off)});
+    if (h_lcp) {
+        const uint64_t lb = (n - 1) * 8;
+        for (uint64_t off = 0; off < lb; off += HostPath::kChunk)
+            pieces.push_back({reinterpret_cast<const char*>(dl) + off,
+                              reinterpret_cast<char*>(h_lcp) + off,
+                              std::min(HostPath::kChunk, lb - off)});
+    }
+    auto issue = [&](uint64_t k) -> int {
+        int b = static_cast<int>(k & 1);
+        S5_CUDA(cudaMemcpyAsync(H.stage[b], pieces[k].d, pieces[k].len, cudaMemcpyDeviceToHost, st));
+        S5_CUDA(cudaEventRecord(H.ev[b], st));
+        return 0;
+    };
+    if (!pieces.empty())
+        if (int e = issue(0)) return e;
+    for (uint64_t k = 0; k < pieces.size(); ++k) {
+        if (k + 1 < pieces.size())
+            if (int e = issue(k + 1)) return e;
+        int b = static_cast<int>(k & 1);
+        S5_CUDA(cudaEventSynchronize(H.ev[b]));
+        par_memcpy(pieces[k].h, H.stage[b], pieces[k].len);
+    }
     S5_CUDA(cudaStreamSynchronize(st));
     return 0;
 }

@@ -214,21 +214,73 @@ __device__ void block_exclusive_scan(uint32_t* h, uint32_t k, uint32_t* warp_sum
     __syncthreads();
 }
 
-// Per-bucket epilogue shared by narrow and wide steps: LCP hint at the
+__device__ __forceinline__ int size_class(const SortArgs& A, uint32_t size) {
+    return size <= A.small_max ? SMALL : (size <= A.narrow_max ? NARROW : WIDE);
+}
+
+struct EmitScratch {
+    uint32_t cnt[3];
+    uint32_t base[3];
+    unsigned long long elems[3];
+    unsigned long long hints;
+};
+
+// Per-bucket epilogue of one S^5 step, aggregated per CTA: LCP hint at every
 // bucket's left boundary (bucket_layout boundaries, classifier.py:284-304),
 // and a child segment for every unfinished bucket of >= 2 strings with the
 // reference's depth rule for equality buckets (+8) and finished rule (D8:
-// equality bucket of a terminated splitter = identical strings).
-__device__ __forceinline__ void bucket_epilogue(const SortArgs& A, const Seg& s, uint32_t b,
-                                                uint32_t start, uint32_t cnt, uint64_t splitter) {
-    uint32_t pos0 = s.begin + start;
-    if (start > 0 && A.lcp) {
-        A.lcp[pos0 - 1] = -static_cast<int64_t>(s.depth) - 1;
-        atomicAdd(&A.ctl->hints, 1ull);
+// equality bucket of a terminated splitter = identical strings).  Children
+// are counted in shared memory first, so each CTA reserves its list slots
+// with one global atomic per size class.  `tree` may be shared or global.
+template <uint32_t THREADS>
+__device__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* starts, uint32_t k,
+                           const uint64_t* tree, uint32_t d, EmitScratch* es) {
+    if (threadIdx.x < 3) {
+        es->cnt[threadIdx.x] = 0;
+        es->elems[threadIdx.x] = 0;
     }
-    bool odd = b & 1;
-    bool fin = cnt == 1 || (odd && has_zero_byte(splitter));
-    if (!fin) emit_child(A, pos0, cnt, s.depth + (odd ? 8u : 0u), s.side ^ 1u);
+    if (threadIdx.x == 0) es->hints = 0;
+    __syncthreads();
+    uint32_t my_hints = 0;
+    unsigned long long my_elems[3] = {0, 0, 0};
+    for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
+        uint32_t st = starts[b], cnt = starts[b + 1] - st;
+        if (!cnt) continue;
+        if (st > 0 && A.lcp) {
+            A.lcp[s.begin + st - 1] = -static_cast<int64_t>(s.depth) - 1;
+            ++my_hints;
+        }
+        bool odd = b & 1;
+        bool fin = cnt == 1 || (odd && has_zero_byte(tree[node_of_rank(b >> 1, d)]));
+        if (!fin) {
+            int cls = size_class(A, cnt);
+            atomicAdd(&es->cnt[cls], 1u);
+            my_elems[cls] += cnt;
+        }
+    }
+    if (my_hints) atomicAdd(&es->hints, static_cast<unsigned long long>(my_hints));
+    for (int q = 0; q < 3; ++q)
+        if (my_elems[q]) atomicAdd(&es->elems[q], my_elems[q]);
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        uint32_t q = threadIdx.x, c = es->cnt[q];
+        es->base[q] = c ? atomicAdd(&A.ctl->n_list[q], c) : 0;
+        if (c && es->base[q] + c > A.cap[q]) atomicOr(&A.ctl->err, ERR_LIST);
+        if (es->elems[q]) atomicAdd(&A.ctl->elems[q], es->elems[q]);
+        es->cnt[q] = 0;
+    }
+    if (threadIdx.x == 0 && es->hints) atomicAdd(&A.ctl->hints, es->hints);
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
+        uint32_t st = starts[b], cnt = starts[b + 1] - st;
+        if (cnt < 2) continue;
+        bool odd = b & 1;
+        if (odd && has_zero_byte(tree[node_of_rank(b >> 1, d)])) continue;
+        int cls = size_class(A, cnt);
+        uint32_t slot = es->base[cls] + atomicAdd(&es->cnt[cls], 1u);
+        if (slot < A.cap[cls])
+            A.next[cls][slot] = Seg{s.begin + st, cnt, s.depth + (odd ? 8u : 0u), s.side ^ 1u};
+    }
 }
 
 // Element epilogue: final slot for finished buckets (handle + identical-string
@@ -341,13 +393,8 @@ k_narrow(SortArgs A, const Seg* __restrict__ segs) {
 
     // stage 3: bucket boundaries (bucket_layout) and children
     block_exclusive_scan<kNarrowThreads>(hist, k, warp_sums);
-    for (uint32_t b = threadIdx.x; b < k; b += kNarrowThreads) {
-        uint32_t cnt = hist[b + 1] - hist[b];
-        if (cnt) {
-            uint64_t spl = (b & 1) ? tree[node_of_rank(b >> 1, d)] : 0;
-            bucket_epilogue(A, s, b, hist[b], cnt, spl);
-        }
-    }
+    __shared__ EmitScratch es;
+    emit_block<kNarrowThreads>(A, s, hist, k, tree, d, &es);
 
     // stage 4: out-of-place distribution (samplesort.py:146-152)
     unsigned long long fetches = 0;
@@ -641,13 +688,8 @@ __global__ void __launch_bounds__(1024) k_wide_bscan(SortArgs A, WidePlan P) {
     uint32_t* starts = P.hist_pool + P.hist_off[si] + static_cast<uint64_t>(g.C) * g.k;
     block_exclusive_scan<1024>(starts, g.k, warp_sums);
     const uint64_t* tree = P.tree_pool + P.tree_off[si];
-    for (uint32_t b = threadIdx.x; b < g.k; b += 1024) {
-        uint32_t cnt = starts[b + 1] - starts[b];
-        if (cnt) {
-            uint64_t spl = (b & 1) ? tree[node_of_rank(b >> 1, g.d)] : 0;
-            bucket_epilogue(A, s, b, starts[b], cnt, spl);
-        }
-    }
+    __shared__ EmitScratch es;
+    emit_block<1024>(A, s, starts, g.k, tree, g.d, &es);
 }
 
 // Out-of-place distribution with per-CTA cursors (stage 4, samplesort.py:412-417).

@@ -36,6 +36,10 @@ DIGESTS = {
     5: ("ad23b81651a34cef", "6fe7b06e97f0fc71"),
 }
 
+#: config 5 has no duplicates, so the sorted handle array itself is unique:
+#: sha256[:16] of its int64 LE bytes and its first five entries
+HANDLE_DIGESTS = {5: ("0f9c3331ca2ab3a2", [8554485, 128901439, 12150689, 619002, 15495257])}
+
 DESCRIPTION = {
     1: "random a-z, length U[8,20], n=2^17, seed 1",
     2: "random printable ASCII 0x21-0x7E, length U[1,32], n=2^25, seed 2",

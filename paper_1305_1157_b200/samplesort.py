@@ -138,12 +138,11 @@ def _sort(arena, handles, depth, cfg, counters, audit, lcp_out):
         return handles
     on_device = isinstance(handles, torch.Tensor) and handles.is_cuda
     dev = _device_of(handles)
-    if on_device:
-        d_h = handles
-    else:
+    if not on_device:
         if not isinstance(handles, np.ndarray) or handles.dtype != np.int64:
             raise TypeError("handles must be a numpy int64 array or a CUDA int64 tensor")
-        d_h = torch.from_numpy(np.ascontiguousarray(handles)).to(dev, non_blocking=False)
+        return _sort_host(arena, handles, depth, cfg, counters, lcp_out, dev)
+    d_h = handles
     d_lcp = None
     if lcp_out is not None:
         if isinstance(lcp_out, torch.Tensor) and lcp_out.is_cuda:
@@ -153,10 +152,42 @@ def _sort(arena, handles, depth, cfg, counters, audit, lcp_out):
     st = _lib.S5Stats()
     gpu_sort(arena, d_h, depth, cfg, d_lcp, st)
     _record(counters, st)
-    if not on_device:
-        handles[:] = d_h.cpu().numpy()
     if lcp_out is not None and d_lcp is not lcp_out:
         lcp_out[: n - 1] = d_lcp.cpu().numpy()
+    return handles
+
+
+def _sort_host(arena, handles, depth, cfg, counters, lcp_out, dev):
+    """numpy handles: the C-ABI host path (s5_sort_host) -- H2D, sort, D2H."""
+    import torch
+    n = int(handles.size)
+    cfg = cfg or SampleSortConfig()
+    h = handles if handles.flags.c_contiguous and handles.flags.writeable else \
+        np.ascontiguousarray(handles)
+    lcp_buf = None
+    if lcp_out is not None:
+        if isinstance(lcp_out, np.ndarray) and lcp_out.dtype == np.int64 and \
+                lcp_out.flags.c_contiguous and lcp_out.size >= n - 1:
+            lcp_buf = lcp_out
+        else:
+            lcp_buf = np.empty(n - 1, np.int64)
+    c = cfg.to_c()
+    st = _lib.S5Stats()
+    with torch.cuda.device(dev):
+        arena_dev = arena.device(dev)
+        rc = _lib.lib().s5_sort_host(arena_dev.data_ptr(), arena.data.size, h.ctypes.data, n,
+                                     int(depth), lcp_buf.ctypes.data if lcp_buf is not None
+                                     else None, C.byref(c), _lib.current_stream_ptr(),
+                                     C.byref(st))
+    _lib.check(rc, "s5_sort_host")
+    _record(counters, st)
+    if h is not handles:
+        handles[:] = h
+    if lcp_out is not None and lcp_buf is not lcp_out:
+        if isinstance(lcp_out, torch.Tensor):
+            lcp_out.copy_(torch.from_numpy(lcp_buf))
+        else:
+            lcp_out[: n - 1] = lcp_buf
     return handles
 
 

@@ -213,7 +213,13 @@ def test_full_config_reference_digests(config):
     got = d.cpu().numpy()
     ds, dl = datasets.DIGESTS[config]
     assert O.digest_lcp(lcp.cpu().numpy())[:16] == dl
-    assert O.digest_strings(arena, got, 63 if config == 5 else -1)[:16] == ds
+    if config in datasets.HANDLE_DIGESTS:
+        import hashlib
+        hd, first5 = datasets.HANDLE_DIGESTS[config]
+        assert got[:5].tolist() == first5
+        assert hashlib.sha256(got.astype("<i8").tobytes()).hexdigest()[:16] == hd
+    else:
+        assert O.digest_strings(arena, got)[:16] == ds
     del arena
 
 
