@@ -53,6 +53,8 @@ typedef struct {
     uint32_t narrow_max;  /* segments <= narrow_max: one-CTA S^5 step (<=16384) */
     uint32_t flags;       /* bit0: skip LCP fix-up (debug); bit1: per-kernel timing */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
+    uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
+    uint32_t reserved;
 } s5_config;
 
 /* Per-call statistics (Counters, counters.py:8-37; SURVEY 8(d) n_p log). */
@@ -76,12 +78,14 @@ typedef struct {
      * launch, same stream), indexed by S5_K_* */
     float kern_ms[16];
     uint32_t kern_launches[16];
+    uint64_t local_elems[S5_MAX_LEVELS]; /* of which in one-CTA S^5 + base case    */
+    uint64_t local_steps;                /* one-CTA S^5 + base-case segments      */
 } s5_stats;
 
 enum {
     S5_K_GATHER = 0, S5_K_WIDE_PLAN, S5_K_WIDE_TREE, S5_K_WIDE_COUNT, S5_K_WIDE_COLSCAN,
     S5_K_WIDE_BSCAN, S5_K_WIDE_SCATTER, S5_K_NARROW, S5_K_SMALL, S5_K_LCP_FIX, S5_K_INIT,
-    S5_K_COUNT
+    S5_K_LOCAL, S5_K_COUNT
 };
 
 /* Bytes of device workspace s5_sort needs for n strings. */

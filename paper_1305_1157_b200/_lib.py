@@ -31,7 +31,7 @@ ERRORS = {
 class S5Config(C.Structure):
     _fields_ = [("v", C.c_uint32), ("alpha", C.c_uint32), ("classifier", C.c_uint32),
                 ("small_max", C.c_uint32), ("narrow_max", C.c_uint32), ("flags", C.c_uint32),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("local_max", C.c_uint32), ("reserved", C.c_uint32)]
 
 
 class S5Stats(C.Structure):
@@ -44,7 +44,8 @@ class S5Stats(C.Structure):
                 ("small_segments", C.c_uint64), ("key_fetches", C.c_uint64),
                 ("boundary_lcps", C.c_uint64), ("launches", C.c_uint64),
                 ("ms_total", C.c_float), ("pad2_", C.c_float),
-                ("kern_ms", C.c_float * 16), ("kern_launches", C.c_uint32 * 16)]
+                ("kern_ms", C.c_float * 16), ("kern_launches", C.c_uint32 * 16),
+                ("local_elems", C.c_uint64 * S5_MAX_LEVELS), ("local_steps", C.c_uint64)]
 
     def as_dict(self) -> dict:
         L = min(self.levels, S5_MAX_LEVELS)
@@ -54,6 +55,8 @@ class S5Stats(C.Structure):
             "wide_elems": [int(x) for x in self.wide_elems[:L]],
             "narrow_elems": [int(x) for x in self.narrow_elems[:L]],
             "small_elems": [int(x) for x in self.small_elems[:L]],
+            "local_elems": [int(x) for x in self.local_elems[:L]],
+            "local_steps": int(self.local_steps),
             "wide_steps": int(self.wide_steps), "narrow_steps": int(self.narrow_steps),
             "small_segments": int(self.small_segments), "key_fetches": int(self.key_fetches),
             "boundary_lcps": int(self.boundary_lcps), "ms_total": float(self.ms_total),
@@ -65,7 +68,8 @@ class S5Stats(C.Structure):
 
 
 KERNELS = ["k_gather", "k_wide_plan", "k_wide_tree", "k_wide_count", "k_wide_colscan",
-           "k_wide_bscan", "k_wide_scatter", "k_narrow", "k_small", "k_lcp_fix", "k_init_root"]
+           "k_wide_bscan", "k_wide_scatter", "k_narrow", "k_small", "k_lcp_fix", "k_init_root",
+           "k_local"]
 
 _vp = C.c_void_p
 _u64 = C.c_uint64

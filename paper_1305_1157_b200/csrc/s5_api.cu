@@ -44,9 +44,12 @@ int fail(int code, const char* fmt, ...) {
     } while (0)
 
 struct Cfg {
-    uint32_t v, alpha, classifier, small_max, narrow_max, flags, dmax;
+    uint32_t v, alpha, classifier, small_max, local_max, narrow_max, flags, dmax;
     uint64_t seed;
 };
+
+constexpr uint32_t kLocalThreads = 512, kLocalItems = 8;
+using LocalCfg = LocalSmem<kLocalThreads, kLocalItems>;
 
 int resolve(const s5_config* c, Cfg* o) {
     o->v = c && c->v ? c->v : 8191;
@@ -54,6 +57,7 @@ int resolve(const s5_config* c, Cfg* o) {
     o->classifier = c ? c->classifier : 0;
     o->small_max = c && c->small_max ? c->small_max : 32;
     o->narrow_max = c && c->narrow_max ? c->narrow_max : kNarrowMaxSize;
+    o->local_max = c && c->local_max ? c->local_max : LocalCfg::maxn;
     o->flags = c ? c->flags : 0;
     o->seed = c ? c->seed : 1;
     uint32_t d = 0;
@@ -66,6 +70,9 @@ int resolve(const s5_config* c, Cfg* o) {
         return fail(S5_E_INVALID, "small_max must be in [1, 32]");
     if (o->narrow_max < o->small_max || o->narrow_max > kNarrowMaxSize)
         return fail(S5_E_INVALID, "narrow_max must be in [small_max, %u]", kNarrowMaxSize);
+    if (o->local_max > LocalCfg::maxn) o->local_max = LocalCfg::maxn;
+    if (o->local_max < o->small_max) o->local_max = o->small_max;
+    if (o->local_max > o->narrow_max) o->local_max = o->narrow_max;
     if (o->alpha > 64) return fail(S5_E_INVALID, "alpha must be <= 64");
     return 0;
 }
@@ -73,9 +80,9 @@ int resolve(const s5_config* c, Cfg* o) {
 uint64_t align_up(uint64_t x, uint64_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
-    uint64_t off[2], key[2], lists[2][3], cta_start, tree_off, hist_off, tree_pool, hist_pool,
+    uint64_t off[2], key[2], lists[2][NCLS], cta_start, tree_off, hist_off, tree_pool, hist_pool,
         ctl, total;
-    uint32_t cap[3];
+    uint32_t cap[NCLS];
     uint64_t tree_cap, hist_cap;
 };
 
@@ -88,12 +95,13 @@ Layout make_layout(uint64_t n, const Cfg& c) {
         return p;
     };
     L.cap[SMALL] = static_cast<uint32_t>(n / 2 + 1);
-    L.cap[NARROW] = static_cast<uint32_t>(n / (c.small_max + 1) + 1);
+    L.cap[LOCAL] = static_cast<uint32_t>(n / (c.small_max + 1) + 1);
+    L.cap[NARROW] = static_cast<uint32_t>(n / (c.local_max + 1) + 1);
     L.cap[WIDE] = static_cast<uint32_t>(n / (c.narrow_max + 1) + 1);
     for (int s = 0; s < 2; ++s) L.off[s] = take(n * 4);
     for (int s = 0; s < 2; ++s) L.key[s] = take(n * 8);
     for (int b = 0; b < 2; ++b)
-        for (int q = 0; q < 3; ++q) L.lists[b][q] = take(uint64_t(L.cap[q]) * sizeof(Seg));
+        for (int q = 0; q < NCLS; ++q) L.lists[b][q] = take(uint64_t(L.cap[q]) * sizeof(Seg));
     L.cta_start = take((uint64_t(L.cap[WIDE]) + 1) * 4);
     L.tree_off = take(uint64_t(L.cap[WIDE]) * 8);
     L.hist_off = take(uint64_t(L.cap[WIDE]) * 8);
@@ -131,6 +139,8 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_wide_scatter<false>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_scatter<true>, kWideSmem);
         if (!rc) rc = set_smem(k_build_tree, 227 * 1024);
+        if (!rc) rc = set_smem(k_local<kLocalThreads, kLocalItems, false>, LocalCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalThreads, kLocalItems, true>, LocalCfg::total);
     });
     return rc;
 }
@@ -250,9 +260,10 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     }
     A.out = d_handles;
     A.lcp = d_lcp;
-    for (int q = 0; q < 3; ++q) A.cap[q] = L.cap[q];
+    for (int q = 0; q < NCLS; ++q) A.cap[q] = L.cap[q];
     A.ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
     A.small_max = c.small_max;
+    A.local_max = c.local_max;
     A.narrow_max = c.narrow_max;
     A.dmax = c.dmax;
     A.alpha = c.alpha;
@@ -269,7 +280,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
 
     // level 0: cached keys at the common depth, root segment
     int cur = 0;
-    for (int q = 0; q < 3; ++q) A.next[q] = reinterpret_cast<Seg*>(ws + L.lists[cur][q]);
+    for (int q = 0; q < NCLS; ++q) A.next[q] = reinterpret_cast<Seg*>(ws + L.lists[cur][q]);
     S5_CUDA(cudaMemsetAsync(A.ctl, 0, sizeof(Ctl), st));
     Prof prof;
     prof.on = stats && (c.flags & 2);
@@ -294,16 +305,16 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         if (h.err & ERR_POOL) return fail(S5_E_INTERNAL, "wide pool overflow");
         fetches_total = h.fetches;
         hints_total = h.hints;
-        uint32_t m[3] = {h.n_list[0], h.n_list[1], h.n_list[2]};
-        if (!m[0] && !m[1] && !m[2]) break;
+        uint32_t m[NCLS] = {h.n_list[0], h.n_list[1], h.n_list[2], h.n_list[3]};
+        if (!m[0] && !m[1] && !m[2] && !m[3]) break;
         if (level >= 100000) return fail(S5_E_INTERNAL, "no progress");
         if (audit && level > 0) {
             // debug replay of the reference's audit hook (samplesort.py:235-236, :431-432):
             // the children emitted by the previous level, with both sides' offsets
-            std::vector<Seg> hs(uint64_t(m[0]) + m[1] + m[2]);
+            std::vector<Seg> hs(uint64_t(m[0]) + m[1] + m[2] + m[3]);
             std::vector<uint32_t> side0(n), side1(n);
             uint64_t at = 0;
-            for (int q = 0; q < 3; ++q) {
+            for (int q = 0; q < NCLS; ++q) {
                 if (m[q])
                     S5_CUDA(cudaMemcpyAsync(hs.data() + at, ws + L.lists[cur][q],
                                             uint64_t(m[q]) * sizeof(Seg), cudaMemcpyDeviceToHost, st));
@@ -319,16 +330,18 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             stats->wide_elems[level] = h.elems[WIDE];
             stats->narrow_elems[level] = h.elems[NARROW];
             stats->small_elems[level] = h.elems[SMALL];
-            stats->n_per_pass[level] = h.elems[0] + h.elems[1] + h.elems[2];
+            stats->local_elems[level] = h.elems[LOCAL];
+            stats->local_steps += m[LOCAL];
+            stats->n_per_pass[level] = h.elems[0] + h.elems[1] + h.elems[2] + h.elems[3];
             stats->wide_steps += m[WIDE];
             stats->narrow_steps += m[NARROW];
             stats->small_segments += m[SMALL];
         }
         // swap lists: this level reads `cur`, emits into the other
-        const Seg* segs[3];
-        for (int q = 0; q < 3; ++q) segs[q] = reinterpret_cast<const Seg*>(ws + L.lists[cur][q]);
+        const Seg* segs[NCLS];
+        for (int q = 0; q < NCLS; ++q) segs[q] = reinterpret_cast<const Seg*>(ws + L.lists[cur][q]);
         cur ^= 1;
-        for (int q = 0; q < 3; ++q) A.next[q] = reinterpret_cast<Seg*>(ws + L.lists[cur][q]);
+        for (int q = 0; q < NCLS; ++q) A.next[q] = reinterpret_cast<Seg*>(ws + L.lists[cur][q]);
         S5_CUDA(cudaMemsetAsync(A.ctl, 0, offsetof(Ctl, fetches), st));
 
         if (m[WIDE]) {
@@ -369,6 +382,16 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
                 k_narrow<true><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
             else
                 k_narrow<false><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
+            prof.end();
+        }
+        if (m[LOCAL]) {
+            prof.begin(S5_K_LOCAL);
+            if (c.classifier)
+                k_local<kLocalThreads, kLocalItems, true>
+                    <<<m[LOCAL], kLocalThreads, LocalCfg::total, st>>>(A, segs[LOCAL]);
+            else
+                k_local<kLocalThreads, kLocalItems, false>
+                    <<<m[LOCAL], kLocalThreads, LocalCfg::total, st>>>(A, segs[LOCAL]);
             prof.end();
         }
         if (m[SMALL]) {

@@ -27,9 +27,10 @@ struct Seg {
 
 // Device control block: next-level list counters, error bits, statistics.
 struct Ctl {
-    uint32_t n_list[3];  // next-level wide, narrow, small segment counts
+    uint32_t n_list[4];  // next-level wide, narrow, small, local segment counts
     uint32_t err;        // bit0 handle range, bit1 list overflow, bit2 pool overflow
-    unsigned long long elems[3];  // strings in next-level wide/narrow/small lists
+    uint32_t pad0;
+    unsigned long long elems[4];  // strings in next-level wide/narrow/small/local lists
     unsigned long long fetches;   // arena key gathers
     unsigned long long hints;     // boundary LCP hints written
     uint32_t wide_ctas;           // plan: CTAs of the current wide launch
@@ -38,7 +39,7 @@ struct Ctl {
 };
 
 enum : uint32_t { ERR_RANGE = 1, ERR_LIST = 2, ERR_POOL = 4 };
-enum : int { WIDE = 0, NARROW = 1, SMALL = 2 };
+enum : int { WIDE = 0, NARROW = 1, SMALL = 2, LOCAL = 3, NCLS = 4 };
 
 struct SortArgs {
     const uint8_t* arena;
@@ -46,10 +47,10 @@ struct SortArgs {
     uint64_t* key[2];
     int64_t* out;
     int64_t* lcp;
-    Seg* next[3];
-    uint32_t cap[3];
+    Seg* next[NCLS];
+    uint32_t cap[NCLS];
     Ctl* ctl;
-    uint32_t small_max, narrow_max;
+    uint32_t small_max, local_max, narrow_max;
     uint32_t dmax;  // log2(cfg.v + 1)
     uint32_t alpha;
     uint64_t seed;
@@ -85,7 +86,8 @@ __host__ __device__ __forceinline__ uint32_t wide_ctas(uint32_t size) {
 
 __device__ __forceinline__ void emit_child(const SortArgs& A, uint32_t begin, uint32_t size,
                                            uint32_t depth, uint32_t side) {
-    int cls = size <= A.small_max ? SMALL : (size <= A.narrow_max ? NARROW : WIDE);
+    int cls = size <= A.small_max ? SMALL
+            : size <= A.local_max ? LOCAL : (size <= A.narrow_max ? NARROW : WIDE);
     uint32_t idx = atomicAdd(&A.ctl->n_list[cls], 1u);
     if (idx < A.cap[cls]) {
         A.next[cls][idx] = Seg{begin, size, depth, side};
@@ -215,13 +217,14 @@ __device__ void block_exclusive_scan(uint32_t* h, uint32_t k, uint32_t* warp_sum
 }
 
 __device__ __forceinline__ int size_class(const SortArgs& A, uint32_t size) {
-    return size <= A.small_max ? SMALL : (size <= A.narrow_max ? NARROW : WIDE);
+    return size <= A.small_max ? SMALL
+         : size <= A.local_max ? LOCAL : (size <= A.narrow_max ? NARROW : WIDE);
 }
 
 struct EmitScratch {
-    uint32_t cnt[3];
-    uint32_t base[3];
-    unsigned long long elems[3];
+    uint32_t cnt[NCLS];
+    uint32_t base[NCLS];
+    unsigned long long elems[NCLS];
     unsigned long long hints;
 };
 
@@ -232,17 +235,19 @@ struct EmitScratch {
 // equality bucket of a terminated splitter = identical strings).  Children
 // are counted in shared memory first, so each CTA reserves its list slots
 // with one global atomic per size class.  `tree` may be shared or global.
-template <uint32_t THREADS>
+// KEEP_SMALL: buckets of <= small_max strings are finished by the calling CTA
+// itself (k_local) instead of becoming children.
+template <uint32_t THREADS, bool KEEP_SMALL = false>
 __device__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* starts, uint32_t k,
                            const uint64_t* tree, uint32_t d, EmitScratch* es) {
-    if (threadIdx.x < 3) {
+    if (threadIdx.x < NCLS) {
         es->cnt[threadIdx.x] = 0;
         es->elems[threadIdx.x] = 0;
     }
     if (threadIdx.x == 0) es->hints = 0;
     __syncthreads();
     uint32_t my_hints = 0;
-    unsigned long long my_elems[3] = {0, 0, 0};
+    unsigned long long my_elems[NCLS] = {0, 0, 0, 0};
     for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
         uint32_t st = starts[b], cnt = starts[b + 1] - st;
         if (!cnt) continue;
@@ -252,17 +257,17 @@ __device__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* star
         }
         bool odd = b & 1;
         bool fin = cnt == 1 || (odd && has_zero_byte(tree[node_of_rank(b >> 1, d)]));
-        if (!fin) {
+        if (!fin && !(KEEP_SMALL && cnt <= A.small_max)) {
             int cls = size_class(A, cnt);
             atomicAdd(&es->cnt[cls], 1u);
             my_elems[cls] += cnt;
         }
     }
     if (my_hints) atomicAdd(&es->hints, static_cast<unsigned long long>(my_hints));
-    for (int q = 0; q < 3; ++q)
+    for (int q = 0; q < NCLS; ++q)
         if (my_elems[q]) atomicAdd(&es->elems[q], my_elems[q]);
     __syncthreads();
-    if (threadIdx.x < 3) {
+    if (threadIdx.x < NCLS) {
         uint32_t q = threadIdx.x, c = es->cnt[q];
         es->base[q] = c ? atomicAdd(&A.ctl->n_list[q], c) : 0;
         if (c && es->base[q] + c > A.cap[q]) atomicOr(&A.ctl->err, ERR_LIST);
@@ -273,7 +278,7 @@ __device__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* star
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
         uint32_t st = starts[b], cnt = starts[b + 1] - st;
-        if (cnt < 2) continue;
+        if (cnt < 2 || (KEEP_SMALL && cnt <= A.small_max)) continue;
         bool odd = b & 1;
         if (odd && has_zero_byte(tree[node_of_rank(b >> 1, d)])) continue;
         int cls = size_class(A, cnt);
@@ -487,6 +492,267 @@ __global__ void __launch_bounds__(256) k_small(SortArgs A, const Seg* __restrict
     }
     if (valid) A.out[s.begin + lane] = o;
     if (pair_valid && A.lcp) A.lcp[s.begin + lane] = static_cast<int64_t>(my_lcp);
+    for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
+    if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
+}
+
+// ---------------------------------------------------------------------------
+// local tier: one CTA finishes a segment of <= THREADS*ITEMS strings.  The
+// strings stay in registers while the CTA samples, builds its splitter tree
+// and classifies them; the bucketed copy goes to shared memory, and every
+// bucket of <= small_max strings is sorted right there by the warp-window
+// base case (below) and written to its final slot with its LCPs.  Only
+// larger buckets leave as children.  Fuses a sequential S^5 step
+// (samplesort.py:213-238) with the base case that follows it.
+
+// Bitonic network over a 64-entry warp window, two entries per lane
+// (positions lane and lane+32), ascending by (hi, key).
+__device__ __forceinline__ void warp_bitonic64(uint32_t (&h)[2], uint64_t (&k)[2],
+                                               uint32_t (&o)[2], uint32_t lane) {
+#pragma unroll
+    for (uint32_t K = 2; K <= 64; K <<= 1) {
+#pragma unroll
+        for (uint32_t J = K >> 1; J > 0; J >>= 1) {
+            if (J == 32) {  // K == 64: positions lane / lane+32 in this thread
+                if (comp_less(h[1], k[1], h[0], k[0])) {
+                    uint32_t th = h[0]; h[0] = h[1]; h[1] = th;
+                    uint64_t tk = k[0]; k[0] = k[1]; k[1] = tk;
+                    uint32_t to = o[0]; o[0] = o[1]; o[1] = to;
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    uint32_t i = lane + 32u * t;
+                    uint32_t oh = __shfl_xor_sync(0xffffffffu, h[t], J);
+                    uint64_t ok = __shfl_xor_sync(0xffffffffu, k[t], J);
+                    uint32_t oo = __shfl_xor_sync(0xffffffffu, o[t], J);
+                    bool up = (i & K) == 0;
+                    bool lower = (lane & J) == 0;
+                    bool take = (lower == up) ? comp_less(oh, ok, h[t], k[t])
+                                              : comp_less(h[t], k[t], oh, ok);
+                    if (take) { h[t] = oh; k[t] = ok; o[t] = oo; }
+                }
+            }
+        }
+    }
+}
+
+// Warp base case over the window [base, base+64) of a bucketed segment: it
+// owns every small bucket that STARTS in [base, base+32) (such a bucket ends
+// before base+63).  Entries sort by (bucket << 8 | run, key); a run is a group
+// of equal unterminated keys that is refilled at depth+8 and re-sorted
+// (the mkqs equal-partition refill, basesort.py:146-150); each adjacent pair's
+// LCP is emitted when resolved, as in k_small.
+__device__ __forceinline__ void window_base_case(const SortArgs& A, const Seg& s, uint32_t base,
+                                                 const uint64_t* key1, const uint32_t* off1,
+                                                 const uint16_t* bpos, const uint32_t* starts,
+                                                 const uint8_t* own, uint32_t lane,
+                                                 unsigned long long& fetches) {
+    uint32_t h[2], o[2];
+    uint64_t k[2];
+    bool valid[2], pair_ok[2];
+    uint32_t bkt[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        uint32_t p = base + lane + 32u * t;
+        bool in = p < s.size;
+        uint32_t b = in ? bpos[p] : 0xFFFFu;
+        bkt[t] = b;
+        valid[t] = in && own[p] && starts[b] >= base && starts[b] < base + 32;
+        h[t] = in ? (b << 8) : 0xFFFFFFFFu;
+        k[t] = valid[t] ? key1[p] : 0ull;
+        o[t] = valid[t] ? off1[p] : 0u;
+    }
+    if (!__any_sync(0xffffffffu, valid[0] || valid[1])) return;
+    // pair (p, p+1) is internal to an owned bucket
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        uint32_t nb = __shfl_down_sync(0xffffffffu, bkt[t], 1);
+        bool nvalid = __shfl_down_sync(0xffffffffu, valid[t], 1);
+        if (t == 0) {
+            uint32_t nb31 = __shfl_sync(0xffffffffu, bkt[1], 0);
+            bool nv31 = __shfl_sync(0xffffffffu, valid[1], 0);
+            if (lane == 31) { nb = nb31; nvalid = nv31; }
+        } else if (lane == 31) {
+            nvalid = false;
+        }
+        pair_ok[t] = valid[t] && nvalid && nb == bkt[t];
+    }
+    bool resolved[2] = {!pair_ok[0], !pair_ok[1]};
+    uint64_t lcpv[2] = {0, 0};
+    uint64_t depth = s.depth;
+    for (;;) {
+        warp_bitonic64(h, k, o, lane);
+        uint64_t nk[2];
+        uint32_t nh[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            nk[t] = __shfl_down_sync(0xffffffffu, k[t], 1);
+            nh[t] = __shfl_down_sync(0xffffffffu, h[t], 1);
+        }
+        uint64_t k1_0 = __shfl_sync(0xffffffffu, k[1], 0);
+        uint32_t h1_0 = __shfl_sync(0xffffffffu, h[1], 0);
+        if (lane == 31) { nk[0] = k1_0; nh[0] = h1_0; }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            if (!resolved[t] && nh[t] == h[t]) {
+                if (k[t] != nk[t]) {
+                    lcpv[t] = depth + diff_bytes(k[t], nk[t]);
+                    resolved[t] = true;
+                } else if (has_zero_byte(k[t])) {
+                    lcpv[t] = depth + zero_index(k[t]);
+                    resolved[t] = true;
+                }
+            }
+        }
+        uint64_t U = static_cast<uint64_t>(__ballot_sync(0xffffffffu, !resolved[0])) |
+                     (static_cast<uint64_t>(__ballot_sync(0xffffffffu, !resolved[1])) << 32);
+        if (!U) break;
+        uint64_t S = ~(U << 1);  // bit p: position p starts a run
+        depth += 8;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            uint32_t p = lane + 32u * t;
+            uint64_t le = p == 63 ? ~0ull : ((2ull << p) - 1);
+            uint32_t run_start = 63u - static_cast<uint32_t>(__clzll(static_cast<long long>(S & le)));
+            bool active = ((U >> p) & 1) || (p > 0 && ((U >> (p - 1)) & 1));
+            if (active) {
+                k[t] = load_key(A.arena, static_cast<uint64_t>(o[t]) + depth);
+                ++fetches;
+            }
+            if (h[t] != 0xFFFFFFFFu) h[t] = (h[t] & ~0xFFu) | run_start;
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        uint32_t p = base + lane + 32u * t;
+        if (valid[t]) {
+            A.out[s.begin + p] = o[t];
+            if (pair_ok[t] && A.lcp) A.lcp[s.begin + p] = static_cast<int64_t>(lcpv[t]);
+        }
+    }
+}
+
+template <uint32_t THREADS, uint32_t ITEMS>
+struct LocalSmem {
+    static constexpr uint32_t maxn = THREADS * ITEMS;
+    static constexpr uint32_t dl = 31 - __builtin_clz(maxn / 8);  // v+1 <= maxn/8
+    static constexpr uint32_t key_bytes = maxn * 8;                 // key1 | sample
+    static constexpr uint32_t off_bytes = maxn * 4;                 // off1 | tree scratch
+    static constexpr uint32_t bpos_bytes = maxn * 2;
+    static constexpr uint32_t own_bytes = maxn;
+    static constexpr uint32_t tree_bytes = (1u << dl) * 8;
+    static constexpr uint32_t hist_bytes = ((2u << dl) + 4) * 4;
+    static constexpr uint32_t total =
+        key_bytes + off_bytes + bpos_bytes + own_bytes + tree_bytes + hist_bytes + 32 * 4;
+    static_assert((1u << dl) * 12 <= off_bytes + bpos_bytes, "tree scratch does not fit");
+};
+
+template <uint32_t THREADS, uint32_t ITEMS, bool EQUAL>
+__global__ void __launch_bounds__(THREADS) k_local(SortArgs A, const Seg* __restrict__ segs) {
+    using L = LocalSmem<THREADS, ITEMS>;
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint64_t* key1 = reinterpret_cast<uint64_t*>(sm);
+    uint64_t* sample = key1;
+    uint32_t* off1 = reinterpret_cast<uint32_t*>(sm + L::key_bytes);
+    int32_t* na = reinterpret_cast<int32_t*>(off1);
+    int32_t* nb = na + (1u << L::dl);
+    uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << L::dl));
+    uint16_t* bpos = reinterpret_cast<uint16_t*>(sm + L::key_bytes + L::off_bytes);
+    uint8_t* own = sm + L::key_bytes + L::off_bytes + L::bpos_bytes;
+    uint64_t* tree = reinterpret_cast<uint64_t*>(own + L::own_bytes);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(own + L::own_bytes + L::tree_bytes);
+    uint32_t* warp_sums = hist + (L::hist_bytes / 4);
+    __shared__ EmitScratch es;
+
+    const Seg s = segs[blockIdx.x];
+    const uint32_t dcap = A.dmax < L::dl ? A.dmax : L::dl;
+    uint32_t d = ceil_log2((s.size + 7) / 8);
+    d = d < 1 ? 1 : (d > dcap ? dcap : d);
+    const uint32_t v = (1u << d) - 1, k = 2 * v + 1;
+    uint32_t m = A.alpha * v;
+    if (m > L::maxn) m = L::maxn;
+    uint32_t M = 1;
+    while (M < m) M <<= 1;
+    const uint32_t* __restrict__ goff = A.off[s.side] + s.begin;
+    const uint64_t* __restrict__ gkey = A.key[s.side] + s.begin;
+
+    // the segment in registers (coalesced), sample from global (L2)
+    uint64_t rk[ITEMS];
+    uint32_t ro[ITEMS];
+#pragma unroll
+    for (uint32_t j = 0; j < ITEMS; ++j) {
+        uint32_t i = threadIdx.x + j * THREADS;
+        rk[j] = i < s.size ? gkey[i] : 0;
+        ro[j] = i < s.size ? goff[i] : 0;
+    }
+    const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
+    for (uint32_t t = threadIdx.x; t < M; t += THREADS)
+        sample[t] = t < m ? gkey[sample_index(sseed, t, s.size)] : ~0ull;
+    __syncthreads();
+    bitonic_sort_smem<THREADS>(sample, M);
+    build_tree_levels<THREADS>(sample, m, d, tree, na, nb, nf);
+    for (uint32_t b = threadIdx.x; b <= k; b += THREADS) hist[b] = 0;
+    __syncthreads();
+
+    // classify + rank (warp-aggregated shared-memory histogram)
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t rb[ITEMS], rr[ITEMS];
+#pragma unroll
+    for (uint32_t j = 0; j < ITEMS; ++j) {
+        uint32_t i = threadIdx.x + j * THREADS;
+        bool act = i < s.size;
+        uint32_t b = act ? classify<EQUAL>(rk[j], tree, d) : 0xFFFFFFFFu;
+        uint32_t peers = __match_any_sync(0xffffffffu, b);
+        uint32_t leader = __ffs(peers) - 1;
+        uint32_t r = 0;
+        if (act && lane == leader) r = atomicAdd(&hist[b], __popc(peers));
+        rb[j] = b;
+        rr[j] = __shfl_sync(0xffffffffu, r, leader) + __popc(peers & lanemask_lt());
+    }
+    __syncthreads();
+    block_exclusive_scan<THREADS>(hist, k, warp_sums);
+    emit_block<THREADS, true>(A, s, hist, k, tree, d, &es);
+
+    // distribute: finished buckets -> final slots; children -> other side;
+    // small buckets -> shared memory for the warp base case
+    unsigned long long fetches = 0;
+    const uint32_t ns = s.side ^ 1u;
+#pragma unroll
+    for (uint32_t j = 0; j < ITEMS; ++j) {
+        uint32_t i = threadIdx.x + j * THREADS;
+        if (i >= s.size) continue;
+        uint32_t b = rb[j];
+        uint32_t start = hist[b], end = hist[b + 1], cnt = end - start;
+        uint32_t p = start + rr[j];
+        bool odd = b & 1;
+        bool fin = cnt == 1 || (odd && has_zero_byte(rk[j]));
+        bpos[p] = static_cast<uint16_t>(b);
+        bool mine = !fin && cnt <= A.small_max;
+        own[p] = mine;
+        uint32_t dst = s.begin + p;
+        if (fin) {
+            A.out[dst] = ro[j];
+            if (odd && A.lcp && p + 1 < end) A.lcp[dst] = s.depth + zero_index(rk[j]);
+        } else if (mine) {
+            key1[p] = rk[j];
+            off1[p] = ro[j];
+        } else if (odd) {
+            A.off[ns][dst] = ro[j];
+            A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(ro[j]) + s.depth + 8);
+            ++fetches;
+        } else {
+            A.off[ns][dst] = ro[j];
+            A.key[ns][dst] = rk[j];
+        }
+    }
+    __syncthreads();
+
+    // warp base case over 64-entry windows
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t nchunks = (s.size + 31) / 32;
+    for (uint32_t c = warp; c < nchunks; c += THREADS / 32)
+        window_base_case(A, s, 32 * c, key1, off1, bpos, hist, own, lane, fetches);
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
     if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
 }

@@ -27,6 +27,9 @@ CONFIGS = {
     "tiny_tiers": SampleSortConfig(v=15, small_max=8, narrow_max=64, seed=3),
     "wide_everywhere": SampleSortConfig(v=255, small_max=32, narrow_max=32, seed=5),
     "alpha8": SampleSortConfig(v=1023, alpha=8, small_max=16, narrow_max=2048),
+    "local_only": SampleSortConfig(v=255, local_max=4096, narrow_max=4096, seed=7),
+    "no_local": SampleSortConfig(local_max=32, seed=11),
+    "local_small8": SampleSortConfig(v=63, small_max=8, local_max=256, narrow_max=1024),
 }
 
 
@@ -258,7 +261,12 @@ def test_eq1_audit(cfg):
     parallel_sample_sort(arena, h, 2, cfg=cfg, audit=audit)
     assert violations == []
     assert seen and all(0 <= lo < hi <= h.size for lo, hi, _ in seen)
-    assert sum(hi - lo for lo, hi, d in seen if d == 0) <= h.size
+    # children of one level are disjoint (segments of later levels nest inside)
+    first = {}
+    for lo, hi, d in seen:
+        first.setdefault(lo, (hi, d))
+    spans = sorted((lo, hi) for lo, (hi, _) in first.items())
+    assert all(a_hi <= b_lo or b_hi <= a_hi for (_, a_hi), (b_lo, b_hi) in zip(spans, spans[1:]))
     assert O.first_unsorted(arena, h) == -1
     assert np.array_equal(np.sort(h), np.sort(orig))
 
