@@ -44,7 +44,7 @@ int fail(int code, const char* fmt, ...) {
     } while (0)
 
 struct Cfg {
-    uint32_t v, alpha, classifier, small_max, local_max, narrow_max, flags, dmax;
+    uint32_t v, alpha, classifier, small_max, local_max, narrow_max, flags, dmax, wide_dcap;
     uint64_t seed;
 };
 
@@ -58,6 +58,12 @@ int resolve(const s5_config* c, Cfg* o) {
     o->small_max = c && c->small_max ? c->small_max : 32;
     o->narrow_max = c && c->narrow_max ? c->narrow_max : kNarrowMaxSize;
     o->local_max = c && c->local_max ? c->local_max : LocalCfg::maxn;
+    uint32_t wv = c && c->wide_v ? c->wide_v : 2047;
+    uint32_t wd = 0;
+    while (wd < 31 && ((1u << wd) - 1) < wv) ++wd;
+    if (((1u << wd) - 1) != wv || wd > kWideDMax)
+        return fail(S5_E_INVALID, "wide_v must be 2**d - 1 with d <= %u, got %u", kWideDMax, wv);
+    o->wide_dcap = wd;
     o->flags = c ? c->flags : 0;
     o->seed = c ? c->seed : 1;
     uint32_t d = 0;
@@ -126,6 +132,7 @@ int set_smem(K kernel, int bytes) {
 
 constexpr int kWideTreeSmem = kWideSampleCap * 8 + (1 << kWideDMax) * 12;
 constexpr int kWideSmem = (1 << kWideDMax) * 8 + ((2 << kWideDMax) + 2) * 4;
+inline int wide_smem(uint32_t dcap) { return (1 << dcap) * 8 + ((2 << dcap) + 2) * 4; }
 
 int init_attributes() {
     static std::once_flag once;
@@ -264,6 +271,8 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
     A.small_max = c.small_max;
     A.local_max = c.local_max;
+    A.wide_dcap = c.wide_dcap;
+    A.wide_target = std::max<uint32_t>(16, c.local_max / 2);
     A.narrow_max = c.narrow_max;
     A.dmax = c.dmax;
     A.alpha = c.alpha;
@@ -356,13 +365,14 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             // upper bound on CTAs; surplus CTAs exit on ctl->wide_ctas
             uint32_t ub = static_cast<uint32_t>(std::min<uint64_t>(
                 uint64_t(m[WIDE]) * kWideCtasMax, n / kWideChunkMin + m[WIDE]));
+            const int wsm = wide_smem(c.wide_dcap);
             prof.begin(S5_K_WIDE_COUNT);
             if (c.classifier)
-                k_wide_count<true><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
+                k_wide_count<true><<<ub, kWideThreads, wsm, st>>>(A, P);
             else
-                k_wide_count<false><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
+                k_wide_count<false><<<ub, kWideThreads, wsm, st>>>(A, P);
             prof.end();
-            dim3 cg(m[WIDE], ((2u << std::min(c.dmax, kWideDMax)) + 1023) / 1024);
+            dim3 cg(m[WIDE], ((2u << std::min(c.dmax, c.wide_dcap)) + 1023) / 1024);
             prof.begin(S5_K_WIDE_COLSCAN);
             k_wide_colscan<<<cg, 1024, 0, st>>>(A, P);
             prof.end();
@@ -371,9 +381,9 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             prof.end();
             prof.begin(S5_K_WIDE_SCATTER);
             if (c.classifier)
-                k_wide_scatter<true><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
+                k_wide_scatter<true><<<ub, kWideThreads, wsm, st>>>(A, P);
             else
-                k_wide_scatter<false><<<ub, kWideThreads, kWideSmem, st>>>(A, P);
+                k_wide_scatter<false><<<ub, kWideThreads, wsm, st>>>(A, P);
             prof.end();
         }
         if (m[NARROW]) {

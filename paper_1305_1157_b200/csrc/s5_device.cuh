@@ -99,6 +99,31 @@ __device__ __forceinline__ uint32_t classify(uint64_t k, const uint64_t* t, uint
     }
 }
 
+// IW interleaved descents (pS^5-Unroll interleaves three, samplesort.py:44,
+// :59-73): independent dependency chains keep the shared-memory pipe busy.
+template <bool EQUAL, int IW>
+__device__ __forceinline__ void classify_iw(const uint64_t (&k)[IW], const uint64_t* t,
+                                            uint32_t d, uint32_t (&b)[IW]) {
+    if (!EQUAL) {
+        uint32_t i[IW];
+#pragma unroll
+        for (int j = 0; j < IW; ++j) i[j] = 1;
+        for (uint32_t l = 0; l < d; ++l) {
+#pragma unroll
+            for (int j = 0; j < IW; ++j) i[j] = 2 * i[j] + (k[j] > t[i[j]] ? 1u : 0u);
+        }
+        const uint32_t v = (1u << d) - 1;
+#pragma unroll
+        for (int j = 0; j < IW; ++j) {
+            uint32_t c = i[j] - (1u << d);
+            b[j] = 2 * c + ((c < v && t[node_of_rank(c, d)] == k[j]) ? 1u : 0u);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < IW; ++j) b[j] = classify<true>(k[j], t, d);
+    }
+}
+
 // Stateless sample RNG: splitmix64 finaliser over (seed, segment, index).
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

@@ -51,7 +51,9 @@ struct SortArgs {
     uint32_t cap[NCLS];
     Ctl* ctl;
     uint32_t small_max, local_max, narrow_max;
-    uint32_t dmax;  // log2(cfg.v + 1)
+    uint32_t dmax;         // log2(cfg.v + 1)
+    uint32_t wide_dcap;    // wide steps use d <= wide_dcap (<= kWideDMax)
+    uint32_t wide_target;  // wide steps aim at children of about this size
     uint32_t alpha;
     uint64_t seed;
 };
@@ -63,8 +65,10 @@ constexpr uint32_t kNarrowSampleCap = 8192;
 constexpr uint32_t kWideThreads = 1024;
 constexpr uint32_t kWideDMax = 13;            // v <= 8191, k <= 16383
 constexpr uint32_t kWideSampleCap = 16384;
-constexpr uint32_t kWideChunkMin = 65536;     // strings per CTA at least
-constexpr uint32_t kWideCtasMax = 296;        // 2 waves of 148 SMs
+constexpr uint32_t kWideChunkMin = 16384;     // strings per CTA at least
+constexpr uint32_t kWideCtasMax = 1184;       // 8 waves of 148 SMs
+constexpr uint32_t kWideFrontier = 1u << 20;  // max C x k open bucket cursors
+constexpr int kWideItems = 4;                 // interleaved descents per thread
 
 __host__ __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) {
     uint32_t d = 0;
@@ -776,12 +780,21 @@ struct WideGeom {
     uint32_t d, v, k, C;
 };
 
-__device__ __forceinline__ WideGeom wide_geom(const Seg& s, uint32_t dmax) {
+// Wide step geometry: the fan-out aims at children of ~wide_target strings
+// (the next level then finishes them in k_local), capped at wide_dcap; the
+// CTA count keeps each CTA's contiguous chunk >= kWideChunkMin strings and the
+// write frontier (C x k cursors) small enough to stay resident in L2.
+__device__ __forceinline__ WideGeom wide_geom(const Seg& s, const SortArgs& A) {
     WideGeom g;
-    g.d = choose_d(s.size, dmax < kWideDMax ? dmax : kWideDMax);
+    uint32_t dcap = A.dmax < A.wide_dcap ? A.dmax : A.wide_dcap;
+    uint32_t d = ceil_log2((s.size + A.wide_target - 1) / A.wide_target);
+    g.d = d < 1 ? 1 : (d > dcap ? dcap : d);
     g.v = (1u << g.d) - 1;
     g.k = 2 * g.v + 1;
-    g.C = wide_ctas(s.size);
+    uint32_t c = (s.size + kWideChunkMin - 1) / kWideChunkMin;
+    uint32_t cmax = kWideFrontier / g.k;
+    cmax = cmax < 1 ? 1 : (cmax > kWideCtasMax ? kWideCtasMax : cmax);
+    g.C = c < 1 ? 1 : (c > cmax ? cmax : c);
     return g;
 }
 
@@ -796,7 +809,7 @@ __global__ void __launch_bounds__(1024) k_wide_plan(SortArgs A, WidePlan P) {
         uint32_t i = base + threadIdx.x;
         unsigned long long x[3] = {0, 0, 0};
         if (i < P.nsegs) {
-            WideGeom g = wide_geom(P.segs[i], A.dmax);
+            WideGeom g = wide_geom(P.segs[i], A);
             x[0] = g.C;
             x[1] = g.v + 1;
             x[2] = static_cast<unsigned long long>(g.C) * g.k + g.k + 1;
@@ -857,7 +870,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_tree(SortArgs A, WideP
     int32_t* nb = na + (1u << kWideDMax);
     uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << kWideDMax));
     const Seg s = P.segs[blockIdx.x];
-    const WideGeom g = wide_geom(s, A.dmax);
+    const WideGeom g = wide_geom(s, A);
     uint32_t m = A.alpha * g.v;
     if (m > kWideSampleCap) m = kWideSampleCap;
     uint32_t M = 1;
@@ -888,10 +901,10 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_count(SortArgs A, Wide
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;
     uint64_t* tree = reinterpret_cast<uint64_t*>(sm);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(sm + (1u << kWideDMax) * 8);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(sm + (1u << A.wide_dcap) * 8);
     const uint32_t si = find_seg(P.cta_start, P.nsegs, G);
     const Seg s = P.segs[si];
-    const WideGeom g = wide_geom(s, A.dmax);
+    const WideGeom g = wide_geom(s, A);
     const uint32_t c = G - P.cta_start[si];
     const uint32_t chunk = (s.size + g.C - 1) / g.C;
     const uint32_t lo = c * chunk;
@@ -902,12 +915,23 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_count(SortArgs A, Wide
     __syncthreads();
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
     const uint32_t lane = threadIdx.x & 31;
-    for (uint32_t base = lo; base < hi; base += kWideThreads) {
-        uint32_t i = base + threadIdx.x;
-        bool act = i < hi;
-        uint32_t b = act ? classify<EQUAL>(key[i], tree, g.d) : 0xFFFFFFFFu;
-        uint32_t peers = __match_any_sync(0xffffffffu, b);
-        if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[b], __popc(peers));
+    constexpr int IW = kWideItems;
+    for (uint32_t base = lo; base < hi; base += IW * kWideThreads) {
+        uint64_t kk[IW];
+        uint32_t b[IW];
+#pragma unroll
+        for (int j = 0; j < IW; ++j) {
+            uint32_t i = base + j * kWideThreads + threadIdx.x;
+            kk[j] = i < hi ? key[i] : 0;
+        }
+        classify_iw<EQUAL, IW>(kk, tree, g.d, b);
+#pragma unroll
+        for (int j = 0; j < IW; ++j) {
+            bool act = base + j * kWideThreads + threadIdx.x < hi;
+            uint32_t bb = act ? b[j] : 0xFFFFFFFFu;
+            uint32_t peers = __match_any_sync(0xffffffffu, bb);
+            if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[bb], __popc(peers));
+        }
     }
     __syncthreads();
     uint32_t* row = P.hist_pool + P.hist_off[si] + static_cast<uint64_t>(c) * g.k;
@@ -920,7 +944,7 @@ __global__ void __launch_bounds__(1024) k_wide_colscan(SortArgs A, WidePlan P) {
     if (A.ctl->wide_ctas == 0) return;
     const uint32_t si = blockIdx.x;
     const Seg s = P.segs[si];
-    const WideGeom g = wide_geom(s, A.dmax);
+    const WideGeom g = wide_geom(s, A);
     const uint32_t b = blockIdx.y * blockDim.x + threadIdx.x;
     if (b >= g.k) return;
     uint32_t* rows = P.hist_pool + P.hist_off[si];
@@ -950,7 +974,7 @@ __global__ void __launch_bounds__(1024) k_wide_bscan(SortArgs A, WidePlan P) {
     if (A.ctl->wide_ctas == 0) return;
     const uint32_t si = blockIdx.x;
     const Seg s = P.segs[si];
-    const WideGeom g = wide_geom(s, A.dmax);
+    const WideGeom g = wide_geom(s, A);
     uint32_t* starts = P.hist_pool + P.hist_off[si] + static_cast<uint64_t>(g.C) * g.k;
     block_exclusive_scan<1024>(starts, g.k, warp_sums);
     const uint64_t* tree = P.tree_pool + P.tree_off[si];
@@ -965,10 +989,10 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_scatter(SortArgs A, Wi
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;
     uint64_t* tree = reinterpret_cast<uint64_t*>(sm);
-    uint32_t* cur = reinterpret_cast<uint32_t*>(sm + (1u << kWideDMax) * 8);
+    uint32_t* cur = reinterpret_cast<uint32_t*>(sm + (1u << A.wide_dcap) * 8);
     const uint32_t si = find_seg(P.cta_start, P.nsegs, G);
     const Seg s = P.segs[si];
-    const WideGeom g = wide_geom(s, A.dmax);
+    const WideGeom g = wide_geom(s, A);
     const uint32_t c = G - P.cta_start[si];
     const uint32_t chunk = (s.size + g.C - 1) / g.C;
     const uint32_t lo = c * chunk;
@@ -988,22 +1012,32 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_scatter(SortArgs A, Wi
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
     const uint32_t lane = threadIdx.x & 31;
     unsigned long long fetches = 0;
-    for (uint32_t base = lo; base < hi; base += kWideThreads) {
-        uint32_t i = base + threadIdx.x;
-        bool act = i < hi;
-        uint64_t kk = act ? key[i] : 0;
-        uint32_t o = act ? off[i] : 0;
-        uint32_t b = act ? classify<EQUAL>(kk, tree, g.d) : 0xFFFFFFFFu;
-        uint32_t peers = __match_any_sync(0xffffffffu, b);
-        uint32_t leader = __ffs(peers) - 1;
-        uint32_t r = 0;
-        if (act && lane == leader) r = atomicAdd(&cur[b], __popc(peers));
-        r = __shfl_sync(0xffffffffu, r, leader);
-        if (act) {
-            bool fin = r >> 31;
-            uint32_t p = (r & 0x7FFFFFFFu) + __popc(peers & lanemask_lt());
-            uint32_t end = fin && (b & 1) ? starts[b + 1] : 0;
-            place(A, s, b, fin, p, end, o, kk, fetches);
+    constexpr int IW = kWideItems;
+    for (uint32_t base = lo; base < hi; base += IW * kWideThreads) {
+        uint64_t kk[IW];
+        uint32_t oo[IW], bb[IW];
+#pragma unroll
+        for (int j = 0; j < IW; ++j) {
+            uint32_t i = base + j * kWideThreads + threadIdx.x;
+            kk[j] = i < hi ? key[i] : 0;
+            oo[j] = i < hi ? off[i] : 0;
+        }
+        classify_iw<EQUAL, IW>(kk, tree, g.d, bb);
+#pragma unroll
+        for (int j = 0; j < IW; ++j) {
+            bool act = base + j * kWideThreads + threadIdx.x < hi;
+            uint32_t b = act ? bb[j] : 0xFFFFFFFFu;
+            uint32_t peers = __match_any_sync(0xffffffffu, b);
+            uint32_t leader = __ffs(peers) - 1;
+            uint32_t r = 0;
+            if (act && lane == leader) r = atomicAdd(&cur[b], __popc(peers));
+            r = __shfl_sync(0xffffffffu, r, leader);
+            if (act) {
+                bool fin = r >> 31;
+                uint32_t p = (r & 0x7FFFFFFFu) + __popc(peers & lanemask_lt());
+                uint32_t end = fin && (b & 1) ? starts[b + 1] : 0;
+                place(A, s, b, fin, p, end, oo[j], kk[j], fetches);
+            }
         }
     }
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
