@@ -177,7 +177,7 @@ def run_ours(args):
     dev = torch.device("cuda", torch.cuda.current_device())
     arena, h0, gen_s = workload(args.config, args.n)
     n = h0.size
-    cfg = SampleSortConfig(classifier=args.classifier)
+    cfg = make_cfg(args)
     t_up = time.perf_counter()
     arena.device(dev)
     torch.cuda.synchronize()
@@ -233,7 +233,7 @@ def run_ours(args):
     D = distinguishing_prefix(arena, d_h, d_lcp)
 
     # per-kernel device times: separate profiled steps (CUDA events per launch)
-    pcfg = SampleSortConfig(classifier=args.classifier)
+    pcfg = make_cfg(args)
     prof_stats = []
     for _ in range(max(1, min(args.steps, 3))):
         ps = _lib.S5Stats()
@@ -299,7 +299,7 @@ def run_ours(args):
                    "n": int(n), "arena_bytes": int(arena.data.size), "D": int(D),
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "256 MiB L2 flush + handle restore before every step (untimed)",
-                   "classifier": args.classifier},
+                   "classifier": args.classifier, "overrides": args.cfg},
         "d_chars_per_s": world * D / (ms_per_step * 1e-3),
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak if peak else None,
@@ -323,6 +323,8 @@ def run_ours(args):
         "wall_s_timed_region": wall,
         "step_ms": [round(x, 4) for x in step_ms],
         "levels": st["levels"],
+        "tiers_per_level": {t: st[f"{t}_elems"] for t in ("wide", "narrow", "local", "small")},
+        "key_fetches": st["key_fetches"], "boundary_lcps": st["boundary_lcps"],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(arena, h0, args)
@@ -330,6 +332,15 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def make_cfg(args):
+    from paper_1305_1157_b200.samplesort import SampleSortConfig
+    kw = {"classifier": args.classifier}
+    for item in args.cfg:
+        k, _, v = item.partition("=")
+        kw[k] = int(v) if v.lstrip("-").isdigit() else v
+    return SampleSortConfig(**kw)
 
 
 def one_step_prof(arena, d_h, d_h0, d_lcp, cfg, stats, l2_flush):
@@ -373,6 +384,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--classifier", default="unroll", choices=["unroll", "equal"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cfg", action="append", default=[],
+                    help="SampleSortConfig override key=value (tuning), repeatable")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

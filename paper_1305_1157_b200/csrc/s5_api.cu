@@ -50,6 +50,8 @@ struct Cfg {
 
 constexpr uint32_t kLocalThreads = 512, kLocalItems = 8;
 using LocalCfg = LocalSmem<kLocalThreads, kLocalItems>;
+constexpr uint32_t kLocalSThreads = 128, kLocalSItems = 8;
+using LocalSCfg = LocalSmem<kLocalSThreads, kLocalSItems>;
 
 int resolve(const s5_config* c, Cfg* o) {
     o->v = c && c->v ? c->v : 8191;
@@ -101,7 +103,8 @@ Layout make_layout(uint64_t n, const Cfg& c) {
         return p;
     };
     L.cap[SMALL] = static_cast<uint32_t>(n / 2 + 1);
-    L.cap[LOCAL] = static_cast<uint32_t>(n / (c.small_max + 1) + 1);
+    L.cap[LOCAL_S] = static_cast<uint32_t>(n / (c.small_max + 1) + 1);
+    L.cap[LOCAL] = static_cast<uint32_t>(n / (std::min(c.local_max, LocalSCfg::maxn) + 1) + 1);
     L.cap[NARROW] = static_cast<uint32_t>(n / (c.local_max + 1) + 1);
     L.cap[WIDE] = static_cast<uint32_t>(n / (c.narrow_max + 1) + 1);
     for (int s = 0; s < 2; ++s) L.off[s] = take(n * 4);
@@ -148,6 +151,8 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_build_tree, 227 * 1024);
         if (!rc) rc = set_smem(k_local<kLocalThreads, kLocalItems, false>, LocalCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalThreads, kLocalItems, true>, LocalCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalSThreads, kLocalSItems, false>, LocalSCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalSThreads, kLocalSItems, true>, LocalSCfg::total);
     });
     return rc;
 }
@@ -271,6 +276,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
     A.small_max = c.small_max;
     A.local_max = c.local_max;
+    A.local_s_max = std::min(c.local_max, LocalSCfg::maxn);
     A.wide_dcap = c.wide_dcap;
     A.wide_target = std::max<uint32_t>(16, c.local_max / 2);
     A.narrow_max = c.narrow_max;
@@ -314,13 +320,19 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         if (h.err & ERR_POOL) return fail(S5_E_INTERNAL, "wide pool overflow");
         fetches_total = h.fetches;
         hints_total = h.hints;
-        uint32_t m[NCLS] = {h.n_list[0], h.n_list[1], h.n_list[2], h.n_list[3]};
-        if (!m[0] && !m[1] && !m[2] && !m[3]) break;
+        uint32_t m[NCLS];
+        uint64_t live = 0, live_elems = 0;
+        for (int q = 0; q < NCLS; ++q) {
+            m[q] = h.n_list[q];
+            live += m[q];
+            live_elems += h.elems[q];
+        }
+        if (!live) break;
         if (level >= 100000) return fail(S5_E_INTERNAL, "no progress");
         if (audit && level > 0) {
             // debug replay of the reference's audit hook (samplesort.py:235-236, :431-432):
             // the children emitted by the previous level, with both sides' offsets
-            std::vector<Seg> hs(uint64_t(m[0]) + m[1] + m[2] + m[3]);
+            std::vector<Seg> hs(live);
             std::vector<uint32_t> side0(n), side1(n);
             uint64_t at = 0;
             for (int q = 0; q < NCLS; ++q) {
@@ -339,9 +351,9 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             stats->wide_elems[level] = h.elems[WIDE];
             stats->narrow_elems[level] = h.elems[NARROW];
             stats->small_elems[level] = h.elems[SMALL];
-            stats->local_elems[level] = h.elems[LOCAL];
-            stats->local_steps += m[LOCAL];
-            stats->n_per_pass[level] = h.elems[0] + h.elems[1] + h.elems[2] + h.elems[3];
+            stats->local_elems[level] = h.elems[LOCAL] + h.elems[LOCAL_S];
+            stats->local_steps += m[LOCAL] + m[LOCAL_S];
+            stats->n_per_pass[level] = live_elems;
             stats->wide_steps += m[WIDE];
             stats->narrow_steps += m[NARROW];
             stats->small_segments += m[SMALL];
@@ -392,6 +404,16 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
                 k_narrow<true><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
             else
                 k_narrow<false><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
+            prof.end();
+        }
+        if (m[LOCAL_S]) {
+            prof.begin(S5_K_LOCAL_S);
+            if (c.classifier)
+                k_local<kLocalSThreads, kLocalSItems, true>
+                    <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, st>>>(A, segs[LOCAL_S]);
+            else
+                k_local<kLocalSThreads, kLocalSItems, false>
+                    <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, st>>>(A, segs[LOCAL_S]);
             prof.end();
         }
         if (m[LOCAL]) {

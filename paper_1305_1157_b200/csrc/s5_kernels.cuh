@@ -27,10 +27,9 @@ struct Seg {
 
 // Device control block: next-level list counters, error bits, statistics.
 struct Ctl {
-    uint32_t n_list[4];  // next-level wide, narrow, small, local segment counts
+    uint32_t n_list[5];  // next-level wide, narrow, small, local, local_s segment counts
     uint32_t err;        // bit0 handle range, bit1 list overflow, bit2 pool overflow
-    uint32_t pad0;
-    unsigned long long elems[4];  // strings in next-level wide/narrow/small/local lists
+    unsigned long long elems[5];  // strings in next-level lists, per class
     unsigned long long fetches;   // arena key gathers
     unsigned long long hints;     // boundary LCP hints written
     uint32_t wide_ctas;           // plan: CTAs of the current wide launch
@@ -39,7 +38,7 @@ struct Ctl {
 };
 
 enum : uint32_t { ERR_RANGE = 1, ERR_LIST = 2, ERR_POOL = 4 };
-enum : int { WIDE = 0, NARROW = 1, SMALL = 2, LOCAL = 3, NCLS = 4 };
+enum : int { WIDE = 0, NARROW = 1, SMALL = 2, LOCAL = 3, LOCAL_S = 4, NCLS = 5 };
 
 struct SortArgs {
     const uint8_t* arena;
@@ -50,7 +49,7 @@ struct SortArgs {
     Seg* next[NCLS];
     uint32_t cap[NCLS];
     Ctl* ctl;
-    uint32_t small_max, local_max, narrow_max;
+    uint32_t small_max, local_s_max, local_max, narrow_max;
     uint32_t dmax;         // log2(cfg.v + 1)
     uint32_t wide_dcap;    // wide steps use d <= wide_dcap (<= kWideDMax)
     uint32_t wide_target;  // wide steps aim at children of about this size
@@ -88,10 +87,16 @@ __host__ __device__ __forceinline__ uint32_t wide_ctas(uint32_t size) {
     return c < 1 ? 1 : (c > kWideCtasMax ? kWideCtasMax : c);
 }
 
+__device__ __forceinline__ int size_class(const SortArgs& A, uint32_t size) {
+    return size <= A.small_max     ? SMALL
+         : size <= A.local_s_max   ? LOCAL_S
+         : size <= A.local_max     ? LOCAL
+         : size <= A.narrow_max    ? NARROW : WIDE;
+}
+
 __device__ __forceinline__ void emit_child(const SortArgs& A, uint32_t begin, uint32_t size,
                                            uint32_t depth, uint32_t side) {
-    int cls = size <= A.small_max ? SMALL
-            : size <= A.local_max ? LOCAL : (size <= A.narrow_max ? NARROW : WIDE);
+    int cls = size_class(A, size);
     uint32_t idx = atomicAdd(&A.ctl->n_list[cls], 1u);
     if (idx < A.cap[cls]) {
         A.next[cls][idx] = Seg{begin, size, depth, side};
@@ -220,11 +225,6 @@ __device__ void block_exclusive_scan(uint32_t* h, uint32_t k, uint32_t* warp_sum
     __syncthreads();
 }
 
-__device__ __forceinline__ int size_class(const SortArgs& A, uint32_t size) {
-    return size <= A.small_max ? SMALL
-         : size <= A.local_max ? LOCAL : (size <= A.narrow_max ? NARROW : WIDE);
-}
-
 struct EmitScratch {
     uint32_t cnt[NCLS];
     uint32_t base[NCLS];
@@ -251,7 +251,7 @@ __device__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* star
     if (threadIdx.x == 0) es->hints = 0;
     __syncthreads();
     uint32_t my_hints = 0;
-    unsigned long long my_elems[NCLS] = {0, 0, 0, 0};
+    unsigned long long my_elems[NCLS] = {};
     for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
         uint32_t st = starts[b], cnt = starts[b + 1] - st;
         if (!cnt) continue;
