@@ -504,156 +504,90 @@ __global__ void __launch_bounds__(256) k_small(SortArgs A, const Seg* __restrict
 // local tier: one CTA finishes a segment of <= THREADS*ITEMS strings.  The
 // strings stay in registers while the CTA samples, builds its splitter tree
 // and classifies them; the bucketed copy goes to shared memory, and every
-// bucket of <= small_max strings is sorted right there by the warp-window
-// base case (below) and written to its final slot with its LCPs.  Only
-// larger buckets leave as children.  Fuses a sequential S^5 step
-// (samplesort.py:213-238) with the base case that follows it.
+// bucket of <= small_max strings is finished right there by a rank sort on
+// the cached keys with refills (the base case) and written to its final slots
+// with its LCPs.  Only larger buckets leave as children.  Fuses a sequential
+// S^5 step (samplesort.py:213-238) with the base case that follows it
+// (basesort.py:123-173).
 
-// Bitonic network over a 64-entry warp window, two entries per lane
-// (positions lane and lane+32), ascending by (hi, key).
-__device__ __forceinline__ void warp_bitonic64(uint32_t (&h)[2], uint64_t (&k)[2],
-                                               uint32_t (&o)[2], uint32_t lane) {
+// Ascending bitonic sort of 64 keys held two per lane (positions lane and
+// lane+32) of one warp, in registers.
+__device__ __forceinline__ void warp_sort64(uint64_t& a, uint64_t& b, uint32_t lane) {
 #pragma unroll
     for (uint32_t K = 2; K <= 64; K <<= 1) {
 #pragma unroll
         for (uint32_t J = K >> 1; J > 0; J >>= 1) {
-            if (J == 32) {  // K == 64: positions lane / lane+32 in this thread
-                if (comp_less(h[1], k[1], h[0], k[0])) {
-                    uint32_t th = h[0]; h[0] = h[1]; h[1] = th;
-                    uint64_t tk = k[0]; k[0] = k[1]; k[1] = tk;
-                    uint32_t to = o[0]; o[0] = o[1]; o[1] = to;
-                }
+            if (J == 32) {
+                if (b < a) { uint64_t t = a; a = b; b = t; }
             } else {
-#pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    uint32_t i = lane + 32u * t;
-                    uint32_t oh = __shfl_xor_sync(0xffffffffu, h[t], J);
-                    uint64_t ok = __shfl_xor_sync(0xffffffffu, k[t], J);
-                    uint32_t oo = __shfl_xor_sync(0xffffffffu, o[t], J);
-                    bool up = (i & K) == 0;
-                    bool lower = (lane & J) == 0;
-                    bool take = (lower == up) ? comp_less(oh, ok, h[t], k[t])
-                                              : comp_less(h[t], k[t], oh, ok);
-                    if (take) { h[t] = oh; k[t] = ok; o[t] = oo; }
-                }
+                uint64_t oa = __shfl_xor_sync(0xffffffffu, a, J);
+                uint64_t ob = __shfl_xor_sync(0xffffffffu, b, J);
+                bool lower = (lane & J) == 0;
+                bool upa = (lane & K) == 0, upb = ((lane + 32) & K) == 0;
+                a = (lower == upa) ? (oa < a ? oa : a) : (oa > a ? oa : a);
+                b = (lower == upb) ? (ob < b ? ob : b) : (ob > b ? ob : b);
             }
         }
     }
 }
 
-// Warp base case over the window [base, base+64) of a bucketed segment: it
-// owns every small bucket that STARTS in [base, base+32) (such a bucket ends
-// before base+63).  Entries sort by (bucket << 8 | run, key); a run is a group
-// of equal unterminated keys that is refilled at depth+8 and re-sorted
-// (the mkqs equal-partition refill, basesort.py:146-150); each adjacent pair's
-// LCP is emitted when resolved, as in k_small.
-__device__ __forceinline__ void window_base_case(const SortArgs& A, const Seg& s, uint32_t base,
-                                                 const uint64_t* key1, const uint32_t* off1,
-                                                 const uint16_t* bpos, const uint32_t* starts,
-                                                 const uint8_t* own, uint32_t lane,
-                                                 unsigned long long& fetches) {
-    uint32_t h[2], o[2];
-    uint64_t k[2];
-    bool valid[2], pair_ok[2];
-    uint32_t bkt[2];
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        uint32_t p = base + lane + 32u * t;
-        bool in = p < s.size;
-        uint32_t b = in ? bpos[p] : 0xFFFFu;
-        bkt[t] = b;
-        valid[t] = in && own[p] && starts[b] >= base && starts[b] < base + 32;
-        h[t] = in ? (b << 8) : 0xFFFFFFFFu;
-        k[t] = valid[t] ? key1[p] : 0ull;
-        o[t] = valid[t] ? off1[p] : 0u;
+// Sort s[0..M) (M a multiple of 64) with tmp[0..M) as scratch: every warp
+// sorts 64-key runs in registers, then each key lands at its index in its run
+// plus its bound in every other run (a stable R-way merge by ranking:
+// upper bound in earlier runs, lower bound in later ones).  Three barriers
+// instead of the O(log^2 M) of a shared-memory bitonic network.
+template <uint32_t THREADS>
+__device__ void sort_sample(uint64_t* s, uint64_t* tmp, uint32_t M) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t runs = M / 64;
+    for (uint32_t r = warp; r < runs; r += THREADS / 32) {
+        uint64_t a = s[r * 64 + lane], b = s[r * 64 + 32 + lane];
+        warp_sort64(a, b, lane);
+        s[r * 64 + lane] = a;
+        s[r * 64 + 32 + lane] = b;
     }
-    if (!__any_sync(0xffffffffu, valid[0] || valid[1])) return;
-    // pair (p, p+1) is internal to an owned bucket
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        uint32_t nb = __shfl_down_sync(0xffffffffu, bkt[t], 1);
-        bool nvalid = __shfl_down_sync(0xffffffffu, valid[t], 1);
-        if (t == 0) {
-            uint32_t nb31 = __shfl_sync(0xffffffffu, bkt[1], 0);
-            bool nv31 = __shfl_sync(0xffffffffu, valid[1], 0);
-            if (lane == 31) { nb = nb31; nvalid = nv31; }
-        } else if (lane == 31) {
-            nvalid = false;
-        }
-        pair_ok[t] = valid[t] && nvalid && nb == bkt[t];
-    }
-    bool resolved[2] = {!pair_ok[0], !pair_ok[1]};
-    uint64_t lcpv[2] = {0, 0};
-    uint64_t depth = s.depth;
-    for (;;) {
-        warp_bitonic64(h, k, o, lane);
-        uint64_t nk[2];
-        uint32_t nh[2];
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            nk[t] = __shfl_down_sync(0xffffffffu, k[t], 1);
-            nh[t] = __shfl_down_sync(0xffffffffu, h[t], 1);
-        }
-        uint64_t k1_0 = __shfl_sync(0xffffffffu, k[1], 0);
-        uint32_t h1_0 = __shfl_sync(0xffffffffu, h[1], 0);
-        if (lane == 31) { nk[0] = k1_0; nh[0] = h1_0; }
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            if (!resolved[t] && nh[t] == h[t]) {
-                if (k[t] != nk[t]) {
-                    lcpv[t] = depth + diff_bytes(k[t], nk[t]);
-                    resolved[t] = true;
-                } else if (has_zero_byte(k[t])) {
-                    lcpv[t] = depth + zero_index(k[t]);
-                    resolved[t] = true;
-                }
+    __syncthreads();
+    if (runs <= 1) return;
+    for (uint32_t i = threadIdx.x; i < M; i += THREADS) {
+        const uint32_t r = i >> 6;
+        const uint64_t x = s[i];
+        uint32_t rank = i & 63;
+        for (uint32_t q = 0; q < runs; ++q) {
+            if (q == r) continue;
+            const uint64_t* run = s + q * 64;
+            uint32_t lo = 0, hi = 64;
+            if (q < r) {
+                while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (run[mid] <= x) lo = mid + 1; else hi = mid; }
+            } else {
+                while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (run[mid] < x) lo = mid + 1; else hi = mid; }
             }
+            rank += lo;
         }
-        uint64_t U = static_cast<uint64_t>(__ballot_sync(0xffffffffu, !resolved[0])) |
-                     (static_cast<uint64_t>(__ballot_sync(0xffffffffu, !resolved[1])) << 32);
-        if (!U) break;
-        uint64_t S = ~(U << 1);  // bit p: position p starts a run
-        depth += 8;
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            uint32_t p = lane + 32u * t;
-            uint64_t le = p == 63 ? ~0ull : ((2ull << p) - 1);
-            uint32_t run_start = 63u - static_cast<uint32_t>(__clzll(static_cast<long long>(S & le)));
-            bool active = ((U >> p) & 1) || (p > 0 && ((U >> (p - 1)) & 1));
-            if (active) {
-                k[t] = load_key(A.arena, static_cast<uint64_t>(o[t]) + depth);
-                ++fetches;
-            }
-            if (h[t] != 0xFFFFFFFFu) h[t] = (h[t] & ~0xFFu) | run_start;
-        }
+        tmp[rank] = x;
     }
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        uint32_t p = base + lane + 32u * t;
-        if (valid[t]) {
-            A.out[s.begin + p] = o[t];
-            if (pair_ok[t] && A.lcp) A.lcp[s.begin + p] = static_cast<int64_t>(lcpv[t]);
-        }
-    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < M; i += THREADS) s[i] = tmp[i];
+    __syncthreads();
 }
 
 template <uint32_t THREADS, uint32_t ITEMS>
 struct LocalSmem {
     static constexpr uint32_t maxn = THREADS * ITEMS;
     static constexpr uint32_t dl = 31 - __builtin_clz(maxn / 8);  // v+1 <= maxn/8
-    static constexpr uint32_t key_bytes = maxn * 8;                 // key1 | sample
+    static constexpr uint32_t key_bytes = maxn * 8;                 // key1 | sample + tmp
     static constexpr uint32_t off_bytes = maxn * 4;                 // off1 | tree scratch
-    static constexpr uint32_t bpos_bytes = maxn * 2;
-    static constexpr uint32_t own_bytes = maxn;
+    static constexpr uint32_t u16_bytes = maxn * 2;                 // bpos, perm, perm2
+    static constexpr uint32_t u8_bytes = maxn;                      // own, res
     static constexpr uint32_t tree_bytes = (1u << dl) * 8;
     static constexpr uint32_t hist_bytes = ((2u << dl) + 4) * 4;
-    static constexpr uint32_t total =
-        key_bytes + off_bytes + bpos_bytes + own_bytes + tree_bytes + hist_bytes + 32 * 4;
-    static_assert((1u << dl) * 12 <= off_bytes + bpos_bytes, "tree scratch does not fit");
+    static constexpr uint32_t total = key_bytes + off_bytes + 3 * u16_bytes + 2 * u8_bytes +
+                                      tree_bytes + hist_bytes + 32 * 4;
+    static_assert((1u << dl) * 12 <= off_bytes, "tree scratch does not fit");
 };
 
 template <uint32_t THREADS, uint32_t ITEMS, bool EQUAL>
-__global__ void __launch_bounds__(THREADS) k_local(SortArgs A, const Seg* __restrict__ segs) {
+__global__ void __launch_bounds__(THREADS, (THREADS >= 512 ? 2 : 4))
+k_local(SortArgs A, const Seg* __restrict__ segs) {
     using L = LocalSmem<THREADS, ITEMS>;
     extern __shared__ __align__(16) uint8_t sm[];
     uint64_t* key1 = reinterpret_cast<uint64_t*>(sm);
@@ -663,9 +597,12 @@ __global__ void __launch_bounds__(THREADS) k_local(SortArgs A, const Seg* __rest
     int32_t* nb = na + (1u << L::dl);
     uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << L::dl));
     uint16_t* bpos = reinterpret_cast<uint16_t*>(sm + L::key_bytes + L::off_bytes);
-    uint8_t* own = sm + L::key_bytes + L::off_bytes + L::bpos_bytes;
-    uint64_t* tree = reinterpret_cast<uint64_t*>(own + L::own_bytes);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(own + L::own_bytes + L::tree_bytes);
+    uint16_t* perm = bpos + L::maxn;
+    uint16_t* perm2 = perm + L::maxn;
+    uint8_t* own = reinterpret_cast<uint8_t*>(perm2 + L::maxn);
+    uint8_t* res = own + L::maxn;
+    uint64_t* tree = reinterpret_cast<uint64_t*>(res + L::maxn);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(tree) + L::tree_bytes);
     uint32_t* warp_sums = hist + (L::hist_bytes / 4);
     __shared__ EmitScratch es;
 
@@ -675,9 +612,8 @@ __global__ void __launch_bounds__(THREADS) k_local(SortArgs A, const Seg* __rest
     d = d < 1 ? 1 : (d > dcap ? dcap : d);
     const uint32_t v = (1u << d) - 1, k = 2 * v + 1;
     uint32_t m = A.alpha * v;
-    if (m > L::maxn) m = L::maxn;
-    uint32_t M = 1;
-    while (M < m) M <<= 1;
+    if (m > L::maxn / 2) m = L::maxn / 2;
+    const uint32_t M = (m + 63) & ~63u;
     const uint32_t* __restrict__ goff = A.off[s.side] + s.begin;
     const uint64_t* __restrict__ gkey = A.key[s.side] + s.begin;
 
@@ -694,41 +630,41 @@ __global__ void __launch_bounds__(THREADS) k_local(SortArgs A, const Seg* __rest
     for (uint32_t t = threadIdx.x; t < M; t += THREADS)
         sample[t] = t < m ? gkey[sample_index(sseed, t, s.size)] : ~0ull;
     __syncthreads();
-    bitonic_sort_smem<THREADS>(sample, M);
+    sort_sample<THREADS>(sample, sample + M, M);
     build_tree_levels<THREADS>(sample, m, d, tree, na, nb, nf);
     for (uint32_t b = threadIdx.x; b <= k; b += THREADS) hist[b] = 0;
     __syncthreads();
 
     // classify + rank (warp-aggregated shared-memory histogram)
     const uint32_t lane = threadIdx.x & 31;
-    uint32_t rb[ITEMS], rr[ITEMS];
+    uint32_t rbr[ITEMS];  // bucket | rank-in-bucket << 11
 #pragma unroll
     for (uint32_t j = 0; j < ITEMS; ++j) {
         uint32_t i = threadIdx.x + j * THREADS;
         bool act = i < s.size;
-        uint32_t b = act ? classify<EQUAL>(rk[j], tree, d) : 0xFFFFFFFFu;
+        uint32_t b = act ? classify<EQUAL>(rk[j], tree, d) : 0x7FFu;
         uint32_t peers = __match_any_sync(0xffffffffu, b);
         uint32_t leader = __ffs(peers) - 1;
         uint32_t r = 0;
         if (act && lane == leader) r = atomicAdd(&hist[b], __popc(peers));
-        rb[j] = b;
-        rr[j] = __shfl_sync(0xffffffffu, r, leader) + __popc(peers & lanemask_lt());
+        r = __shfl_sync(0xffffffffu, r, leader) + __popc(peers & lanemask_lt());
+        rbr[j] = b | (r << 11);
     }
     __syncthreads();
     block_exclusive_scan<THREADS>(hist, k, warp_sums);
     emit_block<THREADS, true>(A, s, hist, k, tree, d, &es);
 
     // distribute: finished buckets -> final slots; children -> other side;
-    // small buckets -> shared memory for the warp base case
+    // small buckets -> shared memory for the base case
     unsigned long long fetches = 0;
     const uint32_t ns = s.side ^ 1u;
 #pragma unroll
     for (uint32_t j = 0; j < ITEMS; ++j) {
         uint32_t i = threadIdx.x + j * THREADS;
         if (i >= s.size) continue;
-        uint32_t b = rb[j];
+        uint32_t b = rbr[j] & 0x7FFu;
         uint32_t start = hist[b], end = hist[b + 1], cnt = end - start;
-        uint32_t p = start + rr[j];
+        uint32_t p = start + (rbr[j] >> 11);
         bool odd = b & 1;
         bool fin = cnt == 1 || (odd && has_zero_byte(rk[j]));
         bpos[p] = static_cast<uint16_t>(b);
@@ -752,11 +688,94 @@ __global__ void __launch_bounds__(THREADS) k_local(SortArgs A, const Seg* __rest
     }
     __syncthreads();
 
-    // warp base case over 64-entry windows
-    const uint32_t warp = threadIdx.x >> 5;
-    const uint32_t nchunks = (s.size + 31) / 32;
-    for (uint32_t c = warp; c < nchunks; c += THREADS / 32)
-        window_base_case(A, s, 32 * c, key1, off1, bpos, hist, own, lane, fetches);
+    // base case: rank sort inside every owned bucket by cached key
+    for (uint32_t p = threadIdx.x; p < s.size; p += THREADS) {
+        if (!own[p]) continue;
+        const uint32_t b = bpos[p], bs = hist[b], be = hist[b + 1];
+        const uint64_t x = key1[p];
+        uint32_t r = 0;
+        for (uint32_t q = bs; q < be; ++q) {
+            uint64_t y = key1[q];
+            r += (y < x) || (y == x && q < p);
+        }
+        perm[bs + r] = static_cast<uint16_t>(p);
+    }
+    __syncthreads();
+    // resolve adjacent pairs; equal unterminated keys form runs that are
+    // refilled at depth+8 and re-ranked (the mkqs equal-partition refill,
+    // basesort.py:146-150), until every pair is resolved:
+    //   keys differ            -> lcp = depth + equal leading bytes
+    //   keys equal, terminated -> identical strings, lcp = depth + |rest|
+    uint64_t depth = s.depth;
+    bool any = false;
+    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
+        if (!own[q]) continue;
+        const uint32_t be = hist[bpos[q] + 1];
+        uint8_t rv = 1;
+        if (q + 1 < be) {
+            uint64_t ka = key1[perm[q]], kb = key1[perm[q + 1]];
+            if (ka != kb) {
+                if (A.lcp) A.lcp[s.begin + q] = depth + diff_bytes(ka, kb);
+            } else if (has_zero_byte(ka)) {
+                if (A.lcp) A.lcp[s.begin + q] = depth + zero_index(ka);
+            } else {
+                rv = 0;
+                any = true;
+            }
+        }
+        res[q] = rv;
+    }
+    while (__syncthreads_or(any)) {
+        depth += 8;
+        any = false;
+        for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
+            if (!own[q]) continue;
+            const uint32_t bs = hist[bpos[q]];
+            if (res[q] == 0 || (q > bs && res[q - 1] == 0)) {
+                const uint32_t a = perm[q];
+                key1[a] = load_key(A.arena, static_cast<uint64_t>(off1[a]) + depth);
+                ++fetches;
+            }
+        }
+        __syncthreads();
+        for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
+            if (!own[q]) continue;
+            const uint32_t bs = hist[bpos[q]];
+            if (!(res[q] == 0 || (q > bs && res[q - 1] == 0))) continue;
+            uint32_t rs = q, re = q;
+            while (rs > bs && res[rs - 1] == 0) --rs;
+            while (res[re] == 0) ++re;
+            const uint64_t x = key1[perm[q]];
+            uint32_t r = 0;
+            for (uint32_t t = rs; t <= re; ++t) {
+                uint64_t y = key1[perm[t]];
+                r += (y < x) || (y == x && t < q);
+            }
+            perm2[rs + r] = perm[q];
+        }
+        __syncthreads();
+        for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
+            if (!own[q]) continue;
+            const uint32_t bs = hist[bpos[q]];
+            if (res[q] == 0 || (q > bs && res[q - 1] == 0)) perm[q] = perm2[q];
+        }
+        __syncthreads();
+        for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
+            if (!own[q] || res[q]) continue;
+            uint64_t ka = key1[perm[q]], kb = key1[perm[q + 1]];
+            if (ka != kb) {
+                if (A.lcp) A.lcp[s.begin + q] = depth + diff_bytes(ka, kb);
+                res[q] = 1;
+            } else if (has_zero_byte(ka)) {
+                if (A.lcp) A.lcp[s.begin + q] = depth + zero_index(ka);
+                res[q] = 1;
+            } else {
+                any = true;
+            }
+        }
+    }
+    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS)
+        if (own[q]) A.out[s.begin + q] = off1[perm[q]];
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
     if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
 }
