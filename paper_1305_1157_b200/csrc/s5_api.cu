@@ -89,7 +89,7 @@ uint64_t align_up(uint64_t x, uint64_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
     uint64_t off[2], key[2], lists[2][NCLS], cta_start, tree_off, hist_off, tree_pool, hist_pool,
-        ctl, total;
+        ctl, hints, total;
     uint32_t cap[NCLS];
     uint64_t tree_cap, hist_cap;
 };
@@ -120,6 +120,7 @@ Layout make_layout(uint64_t n, const Cfg& c) {
     L.hist_cap = n + n / 2 + 3 * uint64_t(L.cap[WIDE]) + 65536;
     L.tree_pool = take(L.tree_cap * 8);
     L.hist_pool = take(L.hist_cap * 4);
+    L.hints = take(n * sizeof(uint2));
     L.ctl = take(sizeof(Ctl));
     L.total = at;
     return L;
@@ -272,6 +273,8 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     }
     A.out = d_handles;
     A.lcp = d_lcp;
+    A.hint_list = reinterpret_cast<uint2*>(ws + L.hints);
+    A.hint_cap = static_cast<uint32_t>(n);
     for (int q = 0; q < NCLS; ++q) A.cap[q] = L.cap[q];
     A.ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
     A.small_max = c.small_max;
@@ -436,7 +439,9 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     }
     if (d_lcp && !(c.flags & 1)) {
         prof.begin(S5_K_LCP_FIX);
-        k_lcp_fix<<<grid_for(n - 1, 256), 256, 0, st>>>(d_arena, d_handles, d_lcp, n - 1);
+        if (hints_total)
+            k_lcp_fix<<<grid_for(hints_total, 256), 256, 0, st>>>(d_arena, d_handles, d_lcp,
+                                                                  A.hint_list, hints_total);
         prof.end();
         S5_CUDA(cudaGetLastError());
     }

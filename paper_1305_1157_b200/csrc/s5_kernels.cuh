@@ -4,7 +4,8 @@
 //   arena   u8[N + pad]                     read-only, 8-byte aligned
 //   off[2]  u32[n]  key[2] u64[n]           ping-pong (offset, cached 8-byte key)
 //   out     i64[n]  (the caller's handles)  final order, written once per string
-//   lcp     i64[n-1]                        exact values or -(depth+1) hints
+//   lcp     i64[n-1]                        exact LCPs; bucket boundaries whose
+//           neighbours finish in different CTAs are listed in hint_list
 // A segment {begin, size, depth, side} is a range of off/key[side] whose
 // strings share `depth` leading bytes and whose keys hold bytes
 // [depth, depth+8).  Each level processes every live segment once:
@@ -31,7 +32,7 @@ struct Ctl {
     uint32_t err;        // bit0 handle range, bit1 list overflow, bit2 pool overflow
     unsigned long long elems[5];  // strings in next-level lists, per class
     unsigned long long fetches;   // arena key gathers
-    unsigned long long hints;     // boundary LCP hints written
+    unsigned long long hints;     // boundary LCP hints appended to the hint list
     uint32_t wide_ctas;           // plan: CTAs of the current wide launch
     uint32_t pad;
     unsigned long long tree_words, hist_words;  // plan: pool use of the current level
@@ -46,6 +47,8 @@ struct SortArgs {
     uint64_t* key[2];
     int64_t* out;
     int64_t* lcp;
+    uint2* hint_list;      // (position, depth) of LCPs left for k_lcp_fix
+    uint32_t hint_cap;
     Seg* next[NCLS];
     uint32_t cap[NCLS];
     Ctl* ctl;
@@ -230,7 +233,25 @@ struct EmitScratch {
     uint32_t base[NCLS];
     unsigned long long elems[NCLS];
     unsigned long long hints;
+    unsigned long long hint_base;
 };
+
+__device__ __forceinline__ void push_hint(const SortArgs& A, EmitScratch* es, uint32_t pos,
+                                          uint32_t depth) {
+    unsigned long long slot = es->hint_base + atomicAdd(&es->hints, 1ull);
+    if (slot < A.hint_cap) A.hint_list[slot] = make_uint2(pos, depth);
+    else atomicOr(&A.ctl->err, ERR_LIST);
+}
+
+// reserve es->hints list slots for this CTA (all threads call)
+__device__ __forceinline__ void reserve_hints(const SortArgs& A, EmitScratch* es) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        es->hint_base = es->hints ? atomicAdd(&A.ctl->hints, es->hints) : 0;
+        es->hints = 0;
+    }
+    __syncthreads();
+}
 
 // Per-bucket epilogue of one S^5 step, aggregated per CTA: LCP hint at every
 // bucket's left boundary (bucket_layout boundaries, classifier.py:284-304),
@@ -255,10 +276,7 @@ __device__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* star
     for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
         uint32_t st = starts[b], cnt = starts[b + 1] - st;
         if (!cnt) continue;
-        if (st > 0 && A.lcp) {
-            A.lcp[s.begin + st - 1] = -static_cast<int64_t>(s.depth) - 1;
-            ++my_hints;
-        }
+        if (!KEEP_SMALL && st > 0 && A.lcp) ++my_hints;
         bool odd = b & 1;
         bool fin = cnt == 1 || (odd && has_zero_byte(tree[node_of_rank(b >> 1, d)]));
         if (!fin && !(KEEP_SMALL && cnt <= A.small_max)) {
@@ -278,10 +296,14 @@ __device__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* star
         if (es->elems[q]) atomicAdd(&A.ctl->elems[q], es->elems[q]);
         es->cnt[q] = 0;
     }
-    if (threadIdx.x == 0 && es->hints) atomicAdd(&A.ctl->hints, es->hints);
+    if (threadIdx.x == 0) {
+        es->hint_base = es->hints ? atomicAdd(&A.ctl->hints, es->hints) : 0;
+        es->hints = 0;
+    }
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
         uint32_t st = starts[b], cnt = starts[b + 1] - st;
+        if (!KEEP_SMALL && cnt && st > 0 && A.lcp) push_hint(A, es, s.begin + st - 1, s.depth);
         if (cnt < 2 || (KEEP_SMALL && cnt <= A.small_max)) continue;
         bool odd = b & 1;
         if (odd && has_zero_byte(tree[node_of_rank(b >> 1, d)])) continue;
@@ -570,6 +592,47 @@ __device__ void sort_sample(uint64_t* s, uint64_t* tmp, uint32_t M) {
     __syncthreads();
 }
 
+// A tie of exactly two equal keys at sorted positions q, q+1 (its neighbours
+// inside the bucket hold other keys): finish it with a direct walk over both
+// strings instead of further CTA-wide refill rounds -- the common case for
+// duplicates (config 4 reads, 13 refills each).
+__device__ __forceinline__ bool lone_tie(const uint64_t* key1, const uint16_t* perm, uint32_t q,
+                                         uint32_t bs, uint32_t be, uint64_t k) {
+    return (q == bs || key1[perm[q - 1]] != k) && (q + 2 >= be || key1[perm[q + 2]] != k);
+}
+
+__device__ __forceinline__ void resolve_pair(const SortArgs& A, const Seg& s,
+                                             const uint64_t* key1, const uint32_t* off1,
+                                             uint16_t* perm, uint32_t q, uint64_t depth,
+                                             unsigned long long& fetches) {
+    const uint16_t pa = perm[q], pb = perm[q + 1];
+    const uint64_t a = off1[pa], b = off1[pb];
+    for (;; depth += 8) {
+        uint64_t ka = load_key(A.arena, a + depth), kb = load_key(A.arena, b + depth);
+        fetches += 2;
+        if (ka != kb) {
+            if (ka > kb) {
+                perm[q] = pb;
+                perm[q + 1] = pa;
+            }
+            if (A.lcp) A.lcp[s.begin + q] = depth + diff_bytes(ka, kb);
+            return;
+        }
+        if (has_zero_byte(ka)) {
+            if (A.lcp) A.lcp[s.begin + q] = depth + zero_index(ka);
+            return;
+        }
+    }
+}
+
+// bucket b of a k_local step left the CTA as a child segment
+__device__ __forceinline__ bool local_child(const SortArgs& A, const uint32_t* starts,
+                                            const uint64_t* tree, uint32_t d, uint32_t b) {
+    uint32_t cnt = starts[b + 1] - starts[b];
+    if (cnt <= A.small_max) return false;
+    return !((b & 1) && has_zero_byte(tree[node_of_rank(b >> 1, d)]));
+}
+
 template <uint32_t THREADS, uint32_t ITEMS>
 struct LocalSmem {
     static constexpr uint32_t maxn = THREADS * ITEMS;
@@ -674,6 +737,8 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         if (fin) {
             A.out[dst] = ro[j];
             if (odd && A.lcp && p + 1 < end) A.lcp[dst] = s.depth + zero_index(rk[j]);
+            off1[p] = ro[j];
+            perm[p] = static_cast<uint16_t>(p);
         } else if (mine) {
             key1[p] = rk[j];
             off1[p] = ro[j];
@@ -710,7 +775,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     bool any = false;
     for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
         if (!own[q]) continue;
-        const uint32_t be = hist[bpos[q] + 1];
+        const uint32_t b = bpos[q], bs = hist[b], be = hist[b + 1];
         uint8_t rv = 1;
         if (q + 1 < be) {
             uint64_t ka = key1[perm[q]], kb = key1[perm[q + 1]];
@@ -718,6 +783,8 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
                 if (A.lcp) A.lcp[s.begin + q] = depth + diff_bytes(ka, kb);
             } else if (has_zero_byte(ka)) {
                 if (A.lcp) A.lcp[s.begin + q] = depth + zero_index(ka);
+            } else if (lone_tie(key1, perm, q, bs, be, ka)) {
+                resolve_pair(A, s, key1, off1, perm, q, depth + 8, fetches);
             } else {
                 rv = 0;
                 any = true;
@@ -763,11 +830,15 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
             if (!own[q] || res[q]) continue;
             uint64_t ka = key1[perm[q]], kb = key1[perm[q + 1]];
+            const uint32_t b = bpos[q];
             if (ka != kb) {
                 if (A.lcp) A.lcp[s.begin + q] = depth + diff_bytes(ka, kb);
                 res[q] = 1;
             } else if (has_zero_byte(ka)) {
                 if (A.lcp) A.lcp[s.begin + q] = depth + zero_index(ka);
+                res[q] = 1;
+            } else if (lone_tie(key1, perm, q, hist[b], hist[b + 1], ka)) {
+                resolve_pair(A, s, key1, off1, perm, q, depth + 8, fetches);
                 res[q] = 1;
             } else {
                 any = true;
@@ -776,6 +847,33 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     }
     for (uint32_t q = threadIdx.x; q < s.size; q += THREADS)
         if (own[q]) A.out[s.begin + q] = off1[perm[q]];
+
+    // LCPs at bucket boundaries: exact when both neighbours were finished in
+    // this CTA (their keys at s.depth differ); otherwise a hint for k_lcp_fix
+    if (A.lcp) {
+        if (threadIdx.x == 0) es.hints = 0;
+        __syncthreads();
+        uint32_t my_hints = 0;
+        for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
+            uint32_t st = hist[b];
+            if (st == 0 || hist[b + 1] == st) continue;
+            if (local_child(A, hist, tree, d, b) || local_child(A, hist, tree, d, bpos[st - 1])) {
+                ++my_hints;
+            } else {
+                uint64_t ka = load_key(A.arena, static_cast<uint64_t>(off1[perm[st - 1]]) + s.depth);
+                uint64_t kb = load_key(A.arena, static_cast<uint64_t>(off1[perm[st]]) + s.depth);
+                A.lcp[s.begin + st - 1] = s.depth + diff_bytes(ka, kb);
+            }
+        }
+        if (my_hints) atomicAdd(&es.hints, static_cast<unsigned long long>(my_hints));
+        reserve_hints(A, &es);
+        for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
+            uint32_t st = hist[b];
+            if (st == 0 || hist[b + 1] == st) continue;
+            if (local_child(A, hist, tree, d, b) || local_child(A, hist, tree, d, bpos[st - 1]))
+                push_hint(A, &es, s.begin + st - 1, s.depth);
+        }
+    }
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
     if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
 }
@@ -1068,18 +1166,18 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_scatter(SortArgs A, Wi
 // at the recorded depth (they were classified into different buckets).
 
 __global__ void k_lcp_fix(const uint8_t* __restrict__ arena, const int64_t* __restrict__ out,
-                          int64_t* __restrict__ lcp, uint64_t m) {
+                          int64_t* __restrict__ lcp, const uint2* __restrict__ hints,
+                          uint64_t m) {
     uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < m;
          i += stride) {
-        int64_t v = lcp[i];
-        if (v >= 0) continue;
-        uint64_t d = static_cast<uint64_t>(-v - 1);
-        uint64_t a = static_cast<uint64_t>(out[i]), b = static_cast<uint64_t>(out[i + 1]);
+        const uint2 h = hints[i];
+        uint64_t d = h.y;
+        uint64_t a = static_cast<uint64_t>(out[h.x]), b = static_cast<uint64_t>(out[h.x + 1]);
         for (;;) {
             uint64_t ka = load_key(arena, a + d), kb = load_key(arena, b + d);
-            if (ka != kb) { lcp[i] = static_cast<int64_t>(d + diff_bytes(ka, kb)); break; }
-            if (has_zero_byte(ka)) { lcp[i] = static_cast<int64_t>(d + zero_index(ka)); break; }
+            if (ka != kb) { lcp[h.x] = static_cast<int64_t>(d + diff_bytes(ka, kb)); break; }
+            if (has_zero_byte(ka)) { lcp[h.x] = static_cast<int64_t>(d + zero_index(ka)); break; }
             d += 8;
         }
     }
