@@ -231,14 +231,21 @@ __device__ void block_exclusive_scan(uint32_t* h, uint32_t k, uint32_t* warp_sum
 struct EmitScratch {
     uint32_t cnt[NCLS];
     uint32_t base[NCLS];
-    unsigned long long elems[NCLS];
-    unsigned long long hints;
+    uint32_t elems[NCLS];
+    uint32_t hints;
     unsigned long long hint_base;
 };
 
+// whole-warp sum, one native 32-bit shared atomic per warp (64-bit shared
+// atomics compile to CAS spin loops)
+__device__ __forceinline__ void warp_add(uint32_t* dst, uint32_t v) {
+    v = __reduce_add_sync(0xffffffffu, v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(dst, v);
+}
+
 __device__ __forceinline__ void push_hint(const SortArgs& A, EmitScratch* es, uint32_t pos,
                                           uint32_t depth) {
-    unsigned long long slot = es->hint_base + atomicAdd(&es->hints, 1ull);
+    unsigned long long slot = es->hint_base + atomicAdd(&es->hints, 1u);
     if (slot < A.hint_cap) A.hint_list[slot] = make_uint2(pos, depth);
     else atomicOr(&A.ctl->err, ERR_LIST);
 }
@@ -247,7 +254,8 @@ __device__ __forceinline__ void push_hint(const SortArgs& A, EmitScratch* es, ui
 __device__ __forceinline__ void reserve_hints(const SortArgs& A, EmitScratch* es) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        es->hint_base = es->hints ? atomicAdd(&A.ctl->hints, es->hints) : 0;
+        es->hint_base = es->hints ? atomicAdd(&A.ctl->hints,
+                                              static_cast<unsigned long long>(es->hints)) : 0;
         es->hints = 0;
     }
     __syncthreads();
@@ -272,7 +280,7 @@ __device__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* star
     if (threadIdx.x == 0) es->hints = 0;
     __syncthreads();
     uint32_t my_hints = 0;
-    unsigned long long my_elems[NCLS] = {};
+    uint32_t my_elems[NCLS] = {};
     for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
         uint32_t st = starts[b], cnt = starts[b + 1] - st;
         if (!cnt) continue;
@@ -285,19 +293,19 @@ __device__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* star
             my_elems[cls] += cnt;
         }
     }
-    if (my_hints) atomicAdd(&es->hints, static_cast<unsigned long long>(my_hints));
-    for (int q = 0; q < NCLS; ++q)
-        if (my_elems[q]) atomicAdd(&es->elems[q], my_elems[q]);
+    warp_add(&es->hints, my_hints);
+    for (int q = 0; q < NCLS; ++q) warp_add(&es->elems[q], my_elems[q]);
     __syncthreads();
     if (threadIdx.x < NCLS) {
         uint32_t q = threadIdx.x, c = es->cnt[q];
         es->base[q] = c ? atomicAdd(&A.ctl->n_list[q], c) : 0;
         if (c && es->base[q] + c > A.cap[q]) atomicOr(&A.ctl->err, ERR_LIST);
-        if (es->elems[q]) atomicAdd(&A.ctl->elems[q], es->elems[q]);
+        if (es->elems[q]) atomicAdd(&A.ctl->elems[q], static_cast<unsigned long long>(es->elems[q]));
         es->cnt[q] = 0;
     }
     if (threadIdx.x == 0) {
-        es->hint_base = es->hints ? atomicAdd(&A.ctl->hints, es->hints) : 0;
+        es->hint_base = es->hints ? atomicAdd(&A.ctl->hints,
+                                              static_cast<unsigned long long>(es->hints)) : 0;
         es->hints = 0;
     }
     __syncthreads();
@@ -437,7 +445,8 @@ k_narrow(SortArgs A, const Seg* __restrict__ segs) {
         bool fin = (end - start == 1) || ((b & 1) && has_zero_byte(kk));
         place(A, s, b, fin, start + r, end, off[i], kk, fetches);
     }
-    if (fetches) atomicAdd(&A.ctl->fetches, fetches);
+    for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
+    if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
 }
 
 // ---------------------------------------------------------------------------
@@ -865,7 +874,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
                 A.lcp[s.begin + st - 1] = s.depth + diff_bytes(ka, kb);
             }
         }
-        if (my_hints) atomicAdd(&es.hints, static_cast<unsigned long long>(my_hints));
+        warp_add(&es.hints, my_hints);
         reserve_hints(A, &es);
         for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
             uint32_t st = hist[b];

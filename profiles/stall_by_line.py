@@ -25,49 +25,77 @@ def sass_samples(rep, kregex, skip):
     hdr = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
     h = rows[hdr]
     si = h.index("Warp Stall Sampling (All Samples)")
-    cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
+    cols = [(i, c) for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
+    src = h.index("Source")
+
+    def num(x):
+        try:
+            return int(float(x.replace(",", "") or 0))
+        except ValueError:
+            return 0
     recs = []
     for r in rows[hdr + 1:]:
         if len(r) <= si:
             continue
-        d = dict(zip(h, r))
-        recs.append((int(d[h[si]] or 0), {c: int(d[c] or 0) for c in cols}, d["Source"].strip()))
+        recs.append((num(r[si]), {c: num(r[i]) if i < len(r) else 0 for i, c in cols},
+                     r[src].strip()))
     return name, recs
 
 
-def line_map(lib, mangled):
+def line_maps(lib):
+    """{mangled function: {offset: "file:line"}} from the library's cubin."""
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp,
                    capture_output=True)
-    cubins = [os.path.join(tmp, f) for f in os.listdir(tmp) if f.endswith(".cubin")]
-    offs = {}
-    for cb in cubins:
-        txt = subprocess.run(["nvdisasm", "-g", "-c", "-fun", mangled, cb], capture_output=True,
-                             text=True).stdout
-        line = None
+    maps = {}
+    for f in os.listdir(tmp):
+        if not f.endswith(".cubin"):
+            continue
+        txt = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, f)],
+                             capture_output=True, text=True).stdout
+        fun, line = None, None
         for ln in txt.splitlines():
+            m = re.match(r"^\.text\.(\S+):", ln)
+            if m:
+                fun, line = m.group(1), None
+                maps[fun] = {}
+                continue
             m = re.search(r'//## File ".*?/([^/"]+)", line (\d+)', ln)
             if m:
                 line = f"{m.group(1)}:{m.group(2)}"
                 continue
             m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
-            if m and line:
-                offs[int(m.group(1), 16)] = line
-        if offs:
-            break
-    return offs
+            if m and fun and line:
+                maps[fun][int(m.group(1), 16)] = line
+    return maps
+
+
+def demangle(names):
+    out = subprocess.run(["cu++filt"], input="\n".join(names), capture_output=True,
+                         text=True).stdout.splitlines()
+    return dict(zip(names, out))
+
+
+def norm(x):
+    return re.sub(r"\s+|\(unsigned int\)|\(bool\)|s5::", "", x.split("(")[0]
+                  if "(" in x.split("<")[0] else x.split(")(")[0])
 
 
 def main():
     rep, kre, skip = sys.argv[1], sys.argv[2], int(sys.argv[3])
     lib = sys.argv[4] if len(sys.argv) > 4 else "paper_1305_1157_b200/libs5.so"
     name, recs = sass_samples(rep, kre, skip)
-    syms = subprocess.run(["cuobjdump", "-symbols", lib], capture_output=True, text=True).stdout
-    # mangled name of the profiled kernel: match template args loosely
-    cands = re.findall(r"(_ZN2s5\w+)", syms)
-    key = re.sub(r"[^a-z_]", "", name.split("(")[0].split("::")[-1].split("<")[0])
-    mangled = next((c for c in cands if key in c), None)
-    offs = line_map(lib, mangled) if mangled else {}
+    maps = line_maps(lib)
+    dem = demangle(list(maps))
+    want = re.sub(r"\s+|\(unsigned int\)|\(bool\)|s5::", "", name).split("(s5")[0]
+    want = want.split("(SortArgs")[0].split("(const")[0]
+    mangled = None
+    for mg, dn in dem.items():
+        d = re.sub(r"\s+|\(unsigned int\)|\(bool\)|s5::", "", dn)
+        if d.split("(")[0] == want.split("(")[0]:
+            mangled = mg
+            break
+    offs = maps.get(mangled, {})
     agg = collections.Counter()
     reasons = collections.defaultdict(collections.Counter)
     total = 0
