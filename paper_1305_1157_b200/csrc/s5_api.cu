@@ -60,7 +60,7 @@ int resolve(const s5_config* c, Cfg* o) {
     o->small_max = c && c->small_max ? c->small_max : 32;
     o->narrow_max = c && c->narrow_max ? c->narrow_max : kNarrowMaxSize;
     o->local_max = c && c->local_max ? c->local_max : LocalCfg::maxn;
-    uint32_t wv = c && c->wide_v ? c->wide_v : 2047;
+    uint32_t wv = c && c->wide_v ? c->wide_v : 511;
     uint32_t wd = 0;
     while (wd < 31 && ((1u << wd) - 1) < wv) ++wd;
     if (((1u << wd) - 1) != wv || wd > kWideDMax)
@@ -89,7 +89,7 @@ uint64_t align_up(uint64_t x, uint64_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
     uint64_t off[2], key[2], lists[2][NCLS], cta_start, tree_off, hist_off, tree_pool, hist_pool,
-        ctl, hints, total;
+        ctl, hints, bkt, total;
     uint32_t cap[NCLS];
     uint64_t tree_cap, hist_cap;
 };
@@ -121,6 +121,7 @@ Layout make_layout(uint64_t n, const Cfg& c) {
     L.tree_pool = take(L.tree_cap * 8);
     L.hist_pool = take(L.hist_cap * 4);
     L.hints = take(n * sizeof(uint2));
+    L.bkt = take(n * 2);
     L.ctl = take(sizeof(Ctl));
     L.total = at;
     return L;
@@ -134,7 +135,7 @@ int set_smem(K kernel, int bytes) {
     return 0;
 }
 
-constexpr int kWideTreeSmem = kWideSampleCap * 8 + (1 << kWideDMax) * 12;
+constexpr int kWideTreeSmem = 2 * kWideSampleCap * 8 + (1 << kWideDMax) * 12;
 constexpr int kWideSmem = (1 << kWideDMax) * 8 + ((2 << kWideDMax) + 2) * 4;
 inline int wide_smem(uint32_t dcap) { return (1 << dcap) * 8 + ((2 << dcap) + 2) * 4; }
 
@@ -147,8 +148,7 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_wide_tree, kWideTreeSmem);
         if (!rc) rc = set_smem(k_wide_count<false>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_count<true>, kWideSmem);
-        if (!rc) rc = set_smem(k_wide_scatter<false>, kWideSmem);
-        if (!rc) rc = set_smem(k_wide_scatter<true>, kWideSmem);
+        if (!rc) rc = set_smem(k_wide_scatter, WideScatterSmem::total);
         if (!rc) rc = set_smem(k_build_tree, 227 * 1024);
         if (!rc) rc = set_smem(k_local<kLocalThreads, kLocalItems, false>, LocalCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalThreads, kLocalItems, true>, LocalCfg::total);
@@ -294,6 +294,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     P.tree_pool = reinterpret_cast<uint64_t*>(ws + L.tree_pool);
     P.hist_pool = reinterpret_cast<uint32_t*>(ws + L.hist_pool);
     P.tree_cap = L.tree_cap;
+    P.bkt = reinterpret_cast<uint16_t*>(ws + L.bkt);
     P.hist_cap = L.hist_cap;
 
     // level 0: cached keys at the common depth, root segment
@@ -395,10 +396,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             k_wide_bscan<<<m[WIDE], 1024, 0, st>>>(A, P);
             prof.end();
             prof.begin(S5_K_WIDE_SCATTER);
-            if (c.classifier)
-                k_wide_scatter<true><<<ub, kWideThreads, wsm, st>>>(A, P);
-            else
-                k_wide_scatter<false><<<ub, kWideThreads, wsm, st>>>(A, P);
+            k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::total, st>>>(A, P);
             prof.end();
         }
         if (m[NARROW]) {
@@ -628,8 +626,8 @@ int s5_classify(const uint64_t* d_keys, uint64_t n, const uint64_t* d_in_order, 
                 uint32_t classifier, uint16_t* d_buckets, void* stream) {
     uint32_t d = 0;
     while (d < 31 && ((1u << d) - 1) < v) ++d;
-    if (v < 1 || ((1u << d) - 1) != v || d > kWideDMax)
-        return fail(S5_E_INVALID, "need 2**d - 1 splitters (d <= %u), got %u", kWideDMax, v);
+    if (v < 1 || ((1u << d) - 1) != v || d > kMaxTreeD)
+        return fail(S5_E_INVALID, "need 2**d - 1 splitters (d <= %u), got %u", kMaxTreeD, v);
     if (!n) return 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int smem = (1 << d) * 8;
@@ -649,8 +647,8 @@ int s5_build_tree(const uint64_t* d_sorted_sample, uint32_t m, uint32_t v,
                   uint64_t* d_level_order, uint64_t* d_in_order, void* stream) {
     uint32_t d = 0;
     while (d < 31 && ((1u << d) - 1) < v) ++d;
-    if (v < 1 || ((1u << d) - 1) != v || d > kWideDMax)
-        return fail(S5_E_INVALID, "need 2**d - 1 splitters (d <= %u), got %u", kWideDMax, v);
+    if (v < 1 || ((1u << d) - 1) != v || d > kMaxTreeD)
+        return fail(S5_E_INVALID, "need 2**d - 1 splitters (d <= %u), got %u", kMaxTreeD, v);
     if (m < 1) return fail(S5_E_INVALID, "empty sample");
     uint64_t smem = uint64_t(m) * 8 + (uint64_t(1) << d) * 12;
     if (smem > 227 * 1024) return fail(S5_E_INVALID, "sample too large for one CTA");

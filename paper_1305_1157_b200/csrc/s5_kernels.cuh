@@ -64,9 +64,11 @@ constexpr uint32_t kNarrowThreads = 512;
 constexpr uint32_t kNarrowDMax = 10;          // v <= 1023, k <= 2047
 constexpr uint32_t kNarrowMaxSize = 16384;    // tags fit 14-bit ranks
 constexpr uint32_t kNarrowSampleCap = 8192;
-constexpr uint32_t kWideThreads = 1024;
-constexpr uint32_t kWideDMax = 13;            // v <= 8191, k <= 16383
-constexpr uint32_t kWideSampleCap = 16384;
+constexpr uint32_t kWideThreads = 512;
+constexpr uint32_t kWideDMax = 10;            // v <= 1023, k <= 2047
+constexpr uint32_t kWideTile = 4096;          // scatter tile staged in shared memory
+constexpr uint32_t kWideSampleCap = 8192;
+constexpr uint32_t kMaxTreeD = 13;            // standalone tree / classify surfaces
 constexpr uint32_t kWideChunkMin = 16384;     // strings per CTA at least
 constexpr uint32_t kWideCtasMax = 1184;       // 8 waves of 148 SMs
 constexpr uint32_t kWideFrontier = 1u << 20;  // max C x k open bucket cursors
@@ -899,6 +901,7 @@ struct WidePlan {
     uint64_t* hist_off;    // [nsegs]  u32 words into hist_pool: C rows of k, then k+1 starts
     uint64_t* tree_pool;
     uint32_t* hist_pool;
+    uint16_t* bkt;         // [n] bucket of every string of the level's wide segments
     uint64_t tree_cap, hist_cap;
 };
 
@@ -992,21 +995,20 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_tree(SortArgs A, WideP
     extern __shared__ __align__(16) uint8_t sm[];
     if (A.ctl->wide_ctas == 0) return;
     uint64_t* sample = reinterpret_cast<uint64_t*>(sm);
-    int32_t* na = reinterpret_cast<int32_t*>(sm + kWideSampleCap * 8);
+    int32_t* na = reinterpret_cast<int32_t*>(sm + 2 * kWideSampleCap * 8);
     int32_t* nb = na + (1u << kWideDMax);
     uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << kWideDMax));
     const Seg s = P.segs[blockIdx.x];
     const WideGeom g = wide_geom(s, A);
     uint32_t m = A.alpha * g.v;
     if (m > kWideSampleCap) m = kWideSampleCap;
-    uint32_t M = 1;
-    while (M < m) M <<= 1;
+    const uint32_t M = (m + 63) & ~63u;
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
     const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
     for (uint32_t t = threadIdx.x; t < M; t += kWideThreads)
         sample[t] = t < m ? key[sample_index(sseed, t, s.size)] : ~0ull;
     __syncthreads();
-    bitonic_sort_smem<kWideThreads>(sample, M);
+    sort_sample<kWideThreads>(sample, sample + M, M);
     build_tree_levels<kWideThreads>(sample, m, g.d, P.tree_pool + P.tree_off[blockIdx.x], na, nb, nf);
 }
 
@@ -1021,8 +1023,10 @@ __device__ __forceinline__ uint32_t find_seg(const uint32_t* cta_start, uint32_t
 }
 
 // Per-CTA histogram of a contiguous chunk (stage 2, samplesort.py:383-400).
+// Every string's bucket is kept (u16, 2 B) so the scatter does not classify
+// again.
 template <bool EQUAL>
-__global__ void __launch_bounds__(kWideThreads, 1) k_wide_count(SortArgs A, WidePlan P) {
+__global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePlan P) {
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;
@@ -1040,7 +1044,7 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_count(SortArgs A, Wide
     for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) hist[b] = 0;
     __syncthreads();
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
-    const uint32_t lane = threadIdx.x & 31;
+    uint16_t* __restrict__ bkt = P.bkt + s.begin;
     constexpr int IW = kWideItems;
     for (uint32_t base = lo; base < hi; base += IW * kWideThreads) {
         uint64_t kk[IW];
@@ -1048,15 +1052,16 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_count(SortArgs A, Wide
 #pragma unroll
         for (int j = 0; j < IW; ++j) {
             uint32_t i = base + j * kWideThreads + threadIdx.x;
-            kk[j] = i < hi ? key[i] : 0;
+            kk[j] = i < hi ? __ldcs(key + i) : 0;
         }
         classify_iw<EQUAL, IW>(kk, tree, g.d, b);
 #pragma unroll
         for (int j = 0; j < IW; ++j) {
-            bool act = base + j * kWideThreads + threadIdx.x < hi;
-            uint32_t bb = act ? b[j] : 0xFFFFFFFFu;
-            uint32_t peers = __match_any_sync(0xffffffffu, bb);
-            if (act && lane == __ffs(peers) - 1) atomicAdd(&hist[bb], __popc(peers));
+            uint32_t i = base + j * kWideThreads + threadIdx.x;
+            if (i < hi) {
+                atomicAdd(&hist[b[j]], 1u);
+                bkt[i] = static_cast<uint16_t>(b[j]);
+            }
         }
     }
     __syncthreads();
@@ -1109,13 +1114,27 @@ __global__ void __launch_bounds__(1024) k_wide_bscan(SortArgs A, WidePlan P) {
 }
 
 // Out-of-place distribution with per-CTA cursors (stage 4, samplesort.py:412-417).
-template <bool EQUAL>
-__global__ void __launch_bounds__(kWideThreads, 1) k_wide_scatter(SortArgs A, WidePlan P) {
+// Tiles of kWideTile strings are first grouped by bucket in shared memory, so
+// each bucket's run of a tile leaves as consecutive addresses (coalesced,
+// whole sectors) instead of one scattered 4 B + 8 B store per string.
+struct WideScatterSmem {
+    static constexpr uint32_t kcap = 2u << kWideDMax;
+    static constexpr uint32_t words = 4 * kcap + 8;
+    static constexpr uint32_t total = words * 4 + kWideTile * (8 + 4 + 2) + 64 * 4;
+};
+
+__global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WidePlan P) {
     extern __shared__ __align__(16) uint8_t sm[];
+    using W = WideScatterSmem;
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;
-    uint64_t* tree = reinterpret_cast<uint64_t*>(sm);
-    uint32_t* cur = reinterpret_cast<uint32_t*>(sm + (1u << A.wide_dcap) * 8);
+    uint64_t* sk = reinterpret_cast<uint64_t*>(sm);
+    uint32_t* so = reinterpret_cast<uint32_t*>(sk + kWideTile);
+    uint16_t* sb = reinterpret_cast<uint16_t*>(so + kWideTile);
+    uint32_t* cur = reinterpret_cast<uint32_t*>(sb + kWideTile);
+    uint32_t* cnt = cur + W::kcap;
+    uint32_t* gb = cnt + W::kcap + 4;
+    uint32_t* warp_sums = gb + W::kcap + 4;
     const uint32_t si = find_seg(P.cta_start, P.nsegs, G);
     const Seg s = P.segs[si];
     const WideGeom g = wide_geom(s, A);
@@ -1123,48 +1142,65 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_scatter(SortArgs A, Wi
     const uint32_t chunk = (s.size + g.C - 1) / g.C;
     const uint32_t lo = c * chunk;
     const uint32_t hi = min(s.size, lo + chunk);
-    const uint64_t* tsrc = P.tree_pool + P.tree_off[si];
+    const uint64_t* tree = P.tree_pool + P.tree_off[si];
     const uint32_t* rows = P.hist_pool + P.hist_off[si];
     const uint32_t* starts = rows + static_cast<uint64_t>(g.C) * g.k;
-    for (uint32_t i = threadIdx.x; i <= g.v; i += kWideThreads) tree[i] = tsrc[i];
-    __syncthreads();
     for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) {
-        uint32_t st = starts[b], cnt = starts[b + 1] - st;
-        bool fin = cnt == 1 || ((b & 1) && has_zero_byte(tree[node_of_rank(b >> 1, g.d)]));
+        uint32_t st = starts[b], n_b = starts[b + 1] - st;
+        bool fin = n_b == 1 || ((b & 1) && has_zero_byte(tree[node_of_rank(b >> 1, g.d)]));
         cur[b] = (st + rows[static_cast<uint64_t>(c) * g.k + b]) | (fin ? 0x80000000u : 0u);
     }
-    __syncthreads();
     const uint32_t* __restrict__ off = A.off[s.side] + s.begin;
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
+    const uint16_t* __restrict__ bkt = P.bkt + s.begin;
     const uint32_t lane = threadIdx.x & 31;
     unsigned long long fetches = 0;
-    constexpr int IW = kWideItems;
-    for (uint32_t base = lo; base < hi; base += IW * kWideThreads) {
-        uint64_t kk[IW];
-        uint32_t oo[IW], bb[IW];
+    constexpr uint32_t IT = kWideTile / kWideThreads;
+    for (uint32_t base = lo; base < hi; base += kWideTile) {
+        for (uint32_t b = threadIdx.x; b <= g.k; b += kWideThreads) cnt[b] = 0;
+        __syncthreads();
+        uint64_t kk[IT];
+        uint32_t oo[IT], br[IT];  // bucket | rank-in-tile << 16
 #pragma unroll
-        for (int j = 0; j < IW; ++j) {
+        for (uint32_t j = 0; j < IT; ++j) {
             uint32_t i = base + j * kWideThreads + threadIdx.x;
-            kk[j] = i < hi ? key[i] : 0;
-            oo[j] = i < hi ? off[i] : 0;
-        }
-        classify_iw<EQUAL, IW>(kk, tree, g.d, bb);
-#pragma unroll
-        for (int j = 0; j < IW; ++j) {
-            bool act = base + j * kWideThreads + threadIdx.x < hi;
-            uint32_t b = act ? bb[j] : 0xFFFFFFFFu;
-            uint32_t peers = __match_any_sync(0xffffffffu, b);
-            uint32_t leader = __ffs(peers) - 1;
-            uint32_t r = 0;
-            if (act && lane == leader) r = atomicAdd(&cur[b], __popc(peers));
-            r = __shfl_sync(0xffffffffu, r, leader);
-            if (act) {
-                bool fin = r >> 31;
-                uint32_t p = (r & 0x7FFFFFFFu) + __popc(peers & lanemask_lt());
-                uint32_t end = fin && (b & 1) ? starts[b + 1] : 0;
-                place(A, s, b, fin, p, end, oo[j], kk[j], fetches);
+            if (i < hi) {
+                kk[j] = __ldcs(key + i);
+                oo[j] = __ldcs(off + i);
+                uint32_t b = bkt[i];
+                br[j] = b | (atomicAdd(&cnt[b], 1u) << 16);
             }
         }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) {
+            uint32_t r = cur[b];
+            gb[b] = r;
+            cur[b] = r + cnt[b];
+        }
+        __syncthreads();
+        block_exclusive_scan<kWideThreads>(cnt, g.k, warp_sums);
+#pragma unroll
+        for (uint32_t j = 0; j < IT; ++j) {
+            uint32_t i = base + j * kWideThreads + threadIdx.x;
+            if (i < hi) {
+                uint32_t b = br[j] & 0xFFFFu;
+                uint32_t p = cnt[b] + (br[j] >> 16);
+                sk[p] = kk[j];
+                so[p] = oo[j];
+                sb[p] = static_cast<uint16_t>(b);
+            }
+        }
+        __syncthreads();
+        const uint32_t m = min(kWideTile, hi - base);
+        for (uint32_t t = threadIdx.x; t < m; t += kWideThreads) {
+            uint32_t b = sb[t];
+            uint32_t r = gb[b];
+            bool fin = r >> 31;
+            uint32_t p = (r & 0x7FFFFFFFu) + (t - cnt[b]);
+            uint32_t end = fin && (b & 1) ? starts[b + 1] : 0;
+            place(A, s, b, fin, p, end, so[t], sk[t], fetches);
+        }
+        __syncthreads();
     }
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
     if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
