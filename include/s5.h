@@ -54,7 +54,7 @@ typedef struct {
     uint32_t flags;       /* bit0: skip LCP fix-up (debug); bit1: per-kernel timing */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
-    uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 8191 (2047) */
+    uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (255)  */
 } s5_config;
 
 /* Per-call statistics (Counters, counters.py:8-37; SURVEY 8(d) n_p log). */

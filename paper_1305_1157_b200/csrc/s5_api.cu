@@ -60,7 +60,7 @@ int resolve(const s5_config* c, Cfg* o) {
     o->small_max = c && c->small_max ? c->small_max : 32;
     o->narrow_max = c && c->narrow_max ? c->narrow_max : kNarrowMaxSize;
     o->local_max = c && c->local_max ? c->local_max : LocalCfg::maxn;
-    uint32_t wv = c && c->wide_v ? c->wide_v : 511;
+    uint32_t wv = c && c->wide_v ? c->wide_v : 255;
     uint32_t wd = 0;
     while (wd < 31 && ((1u << wd) - 1) < wv) ++wd;
     if (((1u << wd) - 1) != wv || wd > kWideDMax)

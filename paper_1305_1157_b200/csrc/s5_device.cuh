@@ -38,6 +38,32 @@ __device__ __forceinline__ uint64_t load_key(const uint8_t* __restrict__ arena, 
     return bswap64(w);
 }
 
+// Keys at pos and pos+8 from three aligned loads (16 string bytes per call);
+// a terminator in the first window zeroes the second.  Needs >= 24 readable
+// bytes past pos (the arena carries a 64-byte zero pad).
+__device__ __forceinline__ void load_key2(const uint8_t* __restrict__ arena, uint64_t pos,
+                                          uint64_t& k0, uint64_t& k1) {
+    const uint64_t* p = reinterpret_cast<const uint64_t*>(arena + (pos & ~7ull));
+    uint64_t w0 = __ldg(p), w1 = __ldg(p + 1), w2 = __ldg(p + 2);
+    uint32_t sh = static_cast<uint32_t>(pos & 7) * 8;
+    uint64_t x0 = sh ? (w0 >> sh) | (w1 << (64 - sh)) : w0;
+    uint64_t x1 = sh ? (w1 >> sh) | (w2 << (64 - sh)) : w1;
+    uint64_t t0 = (x0 - kOnes) & ~x0 & kHighs;
+    if (t0) {
+        uint32_t j = (__ffsll(static_cast<long long>(t0)) - 1) >> 3;
+        x0 &= (1ull << (8 * j)) - 1;
+        x1 = 0;
+    } else {
+        uint64_t t1 = (x1 - kOnes) & ~x1 & kHighs;
+        if (t1) {
+            uint32_t j = (__ffsll(static_cast<long long>(t1)) - 1) >> 3;
+            x1 &= (1ull << (8 * j)) - 1;
+        }
+    }
+    k0 = bswap64(x0);
+    k1 = bswap64(x1);
+}
+
 // Index (0..8) of the first zero byte of an MSB-first key; 8 if none.
 __device__ __forceinline__ uint32_t zero_index(uint64_t key) {
     uint64_t w = bswap64(key);

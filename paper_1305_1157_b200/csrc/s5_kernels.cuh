@@ -612,28 +612,49 @@ __device__ __forceinline__ bool lone_tie(const uint64_t* key1, const uint16_t* p
     return (q == bs || key1[perm[q - 1]] != k) && (q + 2 >= be || key1[perm[q + 2]] != k);
 }
 
+constexpr uint32_t kTieGroupMax = 16;
+
+// strings.py:64-74 (_compare_from) + :56-61 (_lcp_pair) in one walk from a
+// depth both strings are known to share, 16 bytes per step.
+__device__ __forceinline__ int walk_compare(const uint8_t* __restrict__ arena, uint64_t a,
+                                            uint64_t b, uint64_t depth, uint64_t* lcp_out,
+                                            unsigned long long& fetches) {
+    for (;; depth += 16) {
+        uint64_t a0, a1, b0, b1;
+        load_key2(arena, a + depth, a0, a1);
+        load_key2(arena, b + depth, b0, b1);
+        fetches += 2;
+        if (a0 != b0) {
+            if (lcp_out) *lcp_out = depth + diff_bytes(a0, b0);
+            return a0 < b0 ? -1 : 1;
+        }
+        if (has_zero_byte(a0)) {
+            if (lcp_out) *lcp_out = depth + zero_index(a0);
+            return 0;
+        }
+        if (a1 != b1) {
+            if (lcp_out) *lcp_out = depth + 8 + diff_bytes(a1, b1);
+            return a1 < b1 ? -1 : 1;
+        }
+        if (has_zero_byte(a1)) {
+            if (lcp_out) *lcp_out = depth + 8 + zero_index(a1);
+            return 0;
+        }
+    }
+}
+
 __device__ __forceinline__ void resolve_pair(const SortArgs& A, const Seg& s,
                                              const uint64_t* key1, const uint32_t* off1,
                                              uint16_t* perm, uint32_t q, uint64_t depth,
                                              unsigned long long& fetches) {
     const uint16_t pa = perm[q], pb = perm[q + 1];
-    const uint64_t a = off1[pa], b = off1[pb];
-    for (;; depth += 8) {
-        uint64_t ka = load_key(A.arena, a + depth), kb = load_key(A.arena, b + depth);
-        fetches += 2;
-        if (ka != kb) {
-            if (ka > kb) {
-                perm[q] = pb;
-                perm[q + 1] = pa;
-            }
-            if (A.lcp) A.lcp[s.begin + q] = depth + diff_bytes(ka, kb);
-            return;
-        }
-        if (has_zero_byte(ka)) {
-            if (A.lcp) A.lcp[s.begin + q] = depth + zero_index(ka);
-            return;
-        }
+    uint64_t l;
+    int c = walk_compare(A.arena, off1[pa], off1[pb], depth, &l, fetches);
+    if (c > 0) {
+        perm[q] = pb;
+        perm[q + 1] = pa;
     }
+    if (A.lcp) A.lcp[s.begin + q] = l;
 }
 
 // bucket b of a k_local step left the CTA as a child segment
@@ -797,11 +818,54 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
             } else if (lone_tie(key1, perm, q, bs, be, ka)) {
                 resolve_pair(A, s, key1, off1, perm, q, depth + 8, fetches);
             } else {
-                rv = 0;
-                any = true;
+                // tie group of >= 3 equal keys: small ones are ordered below
+                // by direct string comparison, larger ones by refill rounds
+                uint32_t gs = q, ge = q + 1;
+                while (gs > bs && key1[perm[gs - 1]] == ka) --gs;
+                while (ge + 1 < be && key1[perm[ge + 1]] == ka) ++ge;
+                if (ge - gs + 1 <= kTieGroupMax) {
+                    rv = 2;
+                } else {
+                    rv = 0;
+                    any = true;
+                }
             }
         }
         res[q] = rv;
+    }
+    // small tie groups: rank every member by direct comparison with the others
+    // (order among identical strings is free), then one walk per adjacent pair
+    // for its LCP -- no CTA-wide refill rounds
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
+        if (!own[q]) continue;
+        const uint32_t bs = hist[bpos[q]];
+        if (!(res[q] == 2 || (q > bs && res[q - 1] == 2))) continue;
+        uint32_t gs = q, ge = q;
+        while (gs > bs && res[gs - 1] == 2) --gs;
+        while (res[ge] == 2) ++ge;
+        const uint64_t a = off1[perm[q]];
+        uint32_t r = 0;
+        for (uint32_t t = gs; t <= ge; ++t) {
+            if (t == q) continue;
+            int c = walk_compare(A.arena, a, off1[perm[t]], depth + 8, nullptr, fetches);
+            r += c > 0 || (c == 0 && t < q);
+        }
+        perm2[gs + r] = perm[q];
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
+        if (!own[q]) continue;
+        const uint32_t bs = hist[bpos[q]];
+        if (res[q] == 2 || (q > bs && res[q - 1] == 2)) perm[q] = perm2[q];
+    }
+    __syncthreads();
+    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
+        if (!own[q] || res[q] != 2) continue;
+        uint64_t l;
+        walk_compare(A.arena, off1[perm[q]], off1[perm[q + 1]], depth + 8, &l, fetches);
+        if (A.lcp) A.lcp[s.begin + q] = l;
+        res[q] = 1;
     }
     while (__syncthreads_or(any)) {
         depth += 8;

@@ -53,7 +53,7 @@ class SampleSortConfig:
     small_max: int = 32
     narrow_max: int = 16384
     local_max: int = 4096
-    wide_v: int = 2047
+    wide_v: int = 255
 
     def to_c(self) -> _lib.S5Config:
         if self.classifier not in ("unroll", "equal"):
