@@ -564,43 +564,57 @@ __device__ __forceinline__ void warp_sort64(uint64_t& a, uint64_t& b, uint32_t l
     }
 }
 
-// Sort s[0..M) (M a multiple of 64) with tmp[0..M) as scratch: every warp
-// sorts 64-key runs in registers, then each key lands at its index in its run
-// plus its bound in every other run (a stable R-way merge by ranking:
-// upper bound in earlier runs, lower bound in later ones).  Three barriers
-// instead of the O(log^2 M) of a shared-memory bitonic network.
+// Stages J = jtop..1 of a bitonic merge with block size K on the 64 entries
+// at positions base + lane (a) and base + 32 + lane (b) of one warp, in
+// registers; ascending where (position & K) == 0.
+__device__ __forceinline__ void bitonic_reg_stages(uint64_t& a, uint64_t& b, uint32_t lane,
+                                                   uint32_t base, uint32_t K, uint32_t jtop) {
+    const bool upa = ((base + lane) & K) == 0, upb = ((base + 32 + lane) & K) == 0;
+    for (uint32_t J = jtop; J > 0; J >>= 1) {
+        if (J == 32) {
+            if ((a > b) == upa) { uint64_t t = a; a = b; b = t; }
+        } else {
+            uint64_t oa = __shfl_xor_sync(0xffffffffu, a, J);
+            uint64_t ob = __shfl_xor_sync(0xffffffffu, b, J);
+            bool lower = (lane & J) == 0;
+            a = (lower == upa) ? (oa < a ? oa : a) : (oa > a ? oa : a);
+            b = (lower == upb) ? (ob < b ? ob : b) : (ob > b ? ob : b);
+        }
+    }
+}
+
+// Ascending sort of s[0..M), M a power of two >= 64: bitonic network whose
+// stages with partner distance <= 32 run in registers (one warp per 64
+// entries, shuffles), only the wider stages go through shared memory --
+// log2(M/64) * (log2(M) - 5) / 2 + log2(M/64) barriers in total.
 template <uint32_t THREADS>
-__device__ void sort_sample(uint64_t* s, uint64_t* tmp, uint32_t M) {
+__device__ void sort_sample(uint64_t* s, uint32_t M) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t runs = M / 64;
     for (uint32_t r = warp; r < runs; r += THREADS / 32) {
         uint64_t a = s[r * 64 + lane], b = s[r * 64 + 32 + lane];
-        warp_sort64(a, b, lane);
+        for (uint32_t K = 2; K <= 64; K <<= 1) bitonic_reg_stages(a, b, lane, r * 64, K, K >> 1);
         s[r * 64 + lane] = a;
         s[r * 64 + 32 + lane] = b;
     }
     __syncthreads();
-    if (runs <= 1) return;
-    for (uint32_t i = threadIdx.x; i < M; i += THREADS) {
-        const uint32_t r = i >> 6;
-        const uint64_t x = s[i];
-        uint32_t rank = i & 63;
-        for (uint32_t q = 0; q < runs; ++q) {
-            if (q == r) continue;
-            const uint64_t* run = s + q * 64;
-            uint32_t lo = 0, hi = 64;
-            if (q < r) {
-                while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (run[mid] <= x) lo = mid + 1; else hi = mid; }
-            } else {
-                while (lo < hi) { uint32_t mid = (lo + hi) >> 1; if (run[mid] < x) lo = mid + 1; else hi = mid; }
+    for (uint32_t K = 128; K <= M; K <<= 1) {
+        for (uint32_t J = K >> 1; J >= 64; J >>= 1) {
+            for (uint32_t i = threadIdx.x; i < M / 2; i += THREADS) {
+                uint32_t lo = ((i & ~(J - 1)) << 1) | (i & (J - 1)), hi = lo + J;
+                uint64_t x = s[lo], y = s[hi];
+                if ((x > y) == ((lo & K) == 0)) { s[lo] = y; s[hi] = x; }
             }
-            rank += lo;
+            __syncthreads();
         }
-        tmp[rank] = x;
+        for (uint32_t r = warp; r < runs; r += THREADS / 32) {
+            uint64_t a = s[r * 64 + lane], b = s[r * 64 + 32 + lane];
+            bitonic_reg_stages(a, b, lane, r * 64, K, 32);
+            s[r * 64 + lane] = a;
+            s[r * 64 + 32 + lane] = b;
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < M; i += THREADS) s[i] = tmp[i];
-    __syncthreads();
 }
 
 // A tie of exactly two equal keys at sorted positions q, q+1 (its neighbours
@@ -708,7 +722,8 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     const uint32_t v = (1u << d) - 1, k = 2 * v + 1;
     uint32_t m = A.alpha * v;
     if (m > L::maxn / 2) m = L::maxn / 2;
-    const uint32_t M = (m + 63) & ~63u;
+    uint32_t M = 64;
+    while (M < m) M <<= 1;
     const uint32_t* __restrict__ goff = A.off[s.side] + s.begin;
     const uint64_t* __restrict__ gkey = A.key[s.side] + s.begin;
 
@@ -725,7 +740,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     for (uint32_t t = threadIdx.x; t < M; t += THREADS)
         sample[t] = t < m ? gkey[sample_index(sseed, t, s.size)] : ~0ull;
     __syncthreads();
-    sort_sample<THREADS>(sample, sample + M, M);
+    sort_sample<THREADS>(sample, M);
     build_tree_levels<THREADS>(sample, m, d, tree, na, nb, nf);
     for (uint32_t b = threadIdx.x; b <= k; b += THREADS) hist[b] = 0;
     __syncthreads();
@@ -1066,13 +1081,14 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_tree(SortArgs A, WideP
     const WideGeom g = wide_geom(s, A);
     uint32_t m = A.alpha * g.v;
     if (m > kWideSampleCap) m = kWideSampleCap;
-    const uint32_t M = (m + 63) & ~63u;
+    uint32_t M = 64;
+    while (M < m) M <<= 1;
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
     const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
     for (uint32_t t = threadIdx.x; t < M; t += kWideThreads)
         sample[t] = t < m ? key[sample_index(sseed, t, s.size)] : ~0ull;
     __syncthreads();
-    sort_sample<kWideThreads>(sample, sample + M, M);
+    sort_sample<kWideThreads>(sample, M);
     build_tree_levels<kWideThreads>(sample, m, g.d, P.tree_pool + P.tree_off[blockIdx.x], na, nb, nf);
 }
 
