@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define S5_ARENA_PAD 64
+#define S5_ARENA_PAD 128
 
 enum {
     S5_OK = 0,

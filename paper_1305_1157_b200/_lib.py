@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "libs5.so")
 CSRC = os.path.join(_HERE, "csrc")
 
-S5_ARENA_PAD = 64
+S5_ARENA_PAD = 128
 S5_MAX_LEVELS = 128
 
 ERRORS = {

@@ -629,30 +629,33 @@ __device__ __forceinline__ bool lone_tie(const uint64_t* key1, const uint16_t* p
 constexpr uint32_t kTieGroupMax = 16;
 
 // strings.py:64-74 (_compare_from) + :56-61 (_lcp_pair) in one walk from a
-// depth both strings are known to share, 16 bytes per step.
+// depth both strings are known to share, 64 bytes per step: the step's 24
+// loads are independent, so a long common prefix (config-4 duplicate reads,
+// 100 bytes) costs two memory latencies instead of thirteen.  Reads at most
+// 88 bytes past the terminator (S5_ARENA_PAD = 128).
+constexpr uint32_t kWalkKeys = 8;
+
 __device__ __forceinline__ int walk_compare(const uint8_t* __restrict__ arena, uint64_t a,
                                             uint64_t b, uint64_t depth, uint64_t* lcp_out,
                                             unsigned long long& fetches) {
-    for (;; depth += 16) {
-        uint64_t a0, a1, b0, b1;
-        load_key2(arena, a + depth, a0, a1);
-        load_key2(arena, b + depth, b0, b1);
+    for (;; depth += 8 * kWalkKeys) {
+        uint64_t ka[kWalkKeys], kb[kWalkKeys];
+#pragma unroll
+        for (uint32_t t = 0; t < kWalkKeys / 2; ++t) {
+            load_key2(arena, a + depth + 16 * t, ka[2 * t], ka[2 * t + 1]);
+            load_key2(arena, b + depth + 16 * t, kb[2 * t], kb[2 * t + 1]);
+        }
         fetches += 2;
-        if (a0 != b0) {
-            if (lcp_out) *lcp_out = depth + diff_bytes(a0, b0);
-            return a0 < b0 ? -1 : 1;
-        }
-        if (has_zero_byte(a0)) {
-            if (lcp_out) *lcp_out = depth + zero_index(a0);
-            return 0;
-        }
-        if (a1 != b1) {
-            if (lcp_out) *lcp_out = depth + 8 + diff_bytes(a1, b1);
-            return a1 < b1 ? -1 : 1;
-        }
-        if (has_zero_byte(a1)) {
-            if (lcp_out) *lcp_out = depth + 8 + zero_index(a1);
-            return 0;
+#pragma unroll
+        for (uint32_t t = 0; t < kWalkKeys; ++t) {
+            if (ka[t] != kb[t]) {
+                if (lcp_out) *lcp_out = depth + 8 * t + diff_bytes(ka[t], kb[t]);
+                return ka[t] < kb[t] ? -1 : 1;
+            }
+            if (has_zero_byte(ka[t])) {
+                if (lcp_out) *lcp_out = depth + 8 * t + zero_index(ka[t]);
+                return 0;
+            }
         }
     }
 }
@@ -859,14 +862,21 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         uint32_t gs = q, ge = q;
         while (gs > bs && res[gs - 1] == 2) --gs;
         while (res[ge] == 2) ++ge;
+        // rank by (string, position); the LCP with the successor in that order
+        // is the largest LCP with any greater member (sorted-order LCPs only
+        // shrink with distance), so the same walks give the pair LCP
         const uint64_t a = off1[perm[q]];
         uint32_t r = 0;
+        uint64_t succ = 0;
         for (uint32_t t = gs; t <= ge; ++t) {
             if (t == q) continue;
-            int c = walk_compare(A.arena, a, off1[perm[t]], depth + 8, nullptr, fetches);
-            r += c > 0 || (c == 0 && t < q);
+            uint64_t l;
+            int c = walk_compare(A.arena, a, off1[perm[t]], depth + 8, &l, fetches);
+            if (c > 0 || (c == 0 && t < q)) ++r;
+            else if (l > succ) succ = l;
         }
         perm2[gs + r] = perm[q];
+        if (A.lcp && gs + r < ge) A.lcp[s.begin + gs + r] = succ;
     }
     __syncthreads();
     for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
@@ -875,13 +885,8 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         if (res[q] == 2 || (q > bs && res[q - 1] == 2)) perm[q] = perm2[q];
     }
     __syncthreads();
-    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
-        if (!own[q] || res[q] != 2) continue;
-        uint64_t l;
-        walk_compare(A.arena, off1[perm[q]], off1[perm[q + 1]], depth + 8, &l, fetches);
-        if (A.lcp) A.lcp[s.begin + q] = l;
-        res[q] = 1;
-    }
+    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS)
+        if (own[q] && res[q] == 2) res[q] = 1;
     while (__syncthreads_or(any)) {
         depth += 8;
         any = false;
@@ -1242,14 +1247,18 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
         uint64_t kk[IT];
         uint32_t oo[IT], br[IT];  // bucket | rank-in-tile << 16
 #pragma unroll
-        for (uint32_t j = 0; j < IT; ++j) {
+        for (uint32_t j = 0; j < IT; ++j) {  // all loads in flight first
             uint32_t i = base + j * kWideThreads + threadIdx.x;
             if (i < hi) {
                 kk[j] = __ldcs(key + i);
                 oo[j] = __ldcs(off + i);
-                uint32_t b = bkt[i];
-                br[j] = b | (atomicAdd(&cnt[b], 1u) << 16);
+                br[j] = __ldcs(bkt + i);
             }
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < IT; ++j) {
+            uint32_t i = base + j * kWideThreads + threadIdx.x;
+            if (i < hi) br[j] |= atomicAdd(&cnt[br[j]], 1u) << 16;
         }
         __syncthreads();
         for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) {

@@ -18,7 +18,7 @@ import numpy as np
 #: characters per packed key word (strings.py:26)
 WORD_CHARS = 8
 #: zero bytes appended to the device mirror of every arena
-ARENA_PAD = 64
+ARENA_PAD = 128
 
 
 class EmptyInput(ValueError):
