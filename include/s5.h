@@ -55,6 +55,8 @@ typedef struct {
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
     uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (255)  */
+    uint32_t wide_target; /* multi-CTA steps aim at children of this size (0: local_max/2) */
+    uint32_t reserved;
 } s5_config;
 
 /* Per-call statistics (Counters, counters.py:8-37; SURVEY 8(d) n_p log). */

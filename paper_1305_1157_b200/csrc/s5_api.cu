@@ -45,6 +45,7 @@ int fail(int code, const char* fmt, ...) {
 
 struct Cfg {
     uint32_t v, alpha, classifier, small_max, local_max, narrow_max, flags, dmax, wide_dcap;
+    uint32_t wide_target;
     uint64_t seed;
 };
 
@@ -66,6 +67,7 @@ int resolve(const s5_config* c, Cfg* o) {
     if (((1u << wd) - 1) != wv || wd > kWideDMax)
         return fail(S5_E_INVALID, "wide_v must be 2**d - 1 with d <= %u, got %u", kWideDMax, wv);
     o->wide_dcap = wd;
+    o->wide_target = c ? c->wide_target : 0;
     o->flags = c ? c->flags : 0;
     o->seed = c ? c->seed : 1;
     uint32_t d = 0;
@@ -281,7 +283,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.local_max = c.local_max;
     A.local_s_max = std::min(c.local_max, LocalSCfg::maxn);
     A.wide_dcap = c.wide_dcap;
-    A.wide_target = std::max<uint32_t>(16, c.local_max / 2);
+    A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max / 2);
     A.narrow_max = c.narrow_max;
     A.dmax = c.dmax;
     A.alpha = c.alpha;

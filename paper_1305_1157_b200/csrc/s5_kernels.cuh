@@ -638,6 +638,29 @@ constexpr uint32_t kWalkKeys = 8;
 __device__ __forceinline__ int walk_compare(const uint8_t* __restrict__ arena, uint64_t a,
                                             uint64_t b, uint64_t depth, uint64_t* lcp_out,
                                             unsigned long long& fetches) {
+    {   // first 16 bytes: most ties are decided here, keep the traffic small
+        uint64_t a0, a1, b0, b1;
+        load_key2(arena, a + depth, a0, a1);
+        load_key2(arena, b + depth, b0, b1);
+        fetches += 2;
+        if (a0 != b0) {
+            if (lcp_out) *lcp_out = depth + diff_bytes(a0, b0);
+            return a0 < b0 ? -1 : 1;
+        }
+        if (has_zero_byte(a0)) {
+            if (lcp_out) *lcp_out = depth + zero_index(a0);
+            return 0;
+        }
+        if (a1 != b1) {
+            if (lcp_out) *lcp_out = depth + 8 + diff_bytes(a1, b1);
+            return a1 < b1 ? -1 : 1;
+        }
+        if (has_zero_byte(a1)) {
+            if (lcp_out) *lcp_out = depth + 8 + zero_index(a1);
+            return 0;
+        }
+        depth += 16;
+    }
     for (;; depth += 8 * kWalkKeys) {
         uint64_t ka[kWalkKeys], kb[kWalkKeys];
 #pragma unroll
