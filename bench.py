@@ -160,6 +160,89 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_distributed(args):
+    """N > 1 (torchrun): one global sort of the config's n strings across the
+    ranks -- sample-sort partitioning + NCCL all-to-all + local S^5
+    (paper_1305_1157_b200.distributed).  Strong scaling: n is fixed."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1305_1157_b200 import datasets
+    from paper_1305_1157_b200.distributed import GpuBackend, distributed_sample_sort
+    from paper_1305_1157_b200.strings import first_unsorted
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    arena, h0, _ = workload(args.config, args.n)
+    n = h0.size
+    cfg = make_cfg(args)
+    arena.device(dev)
+    lo, hi = n * rank // world, n * (rank + 1) // world
+    shard_host = np.ascontiguousarray(h0[lo:hi])
+    shard = torch.from_numpy(shard_host).to(dev)
+    be = GpuBackend(arena, cfg)
+    l2_flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        distributed_sample_sort(arena, shard.clone(), backend=be)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    times = []
+    res = None
+    for _ in range(args.steps):
+        d = shard.clone()
+        l2_flush.zero_()
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        res = distributed_sample_sort(arena, d, backend=be)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        times.append(ev0.elapsed_time(ev1))
+    clk = clocks.stop()
+    t = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_per_step = float(t.item()) / args.steps
+    ok = torch.tensor([1 if first_unsorted(arena, res.handles) == -1 else 0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    # e2e: host shard in, host slice + LCP out
+    e2e = []
+    for _ in range(max(1, args.steps // 2)):
+        dist.barrier()
+        t0 = time.perf_counter()
+        d = torch.from_numpy(shard_host).to(dev)
+        r = distributed_sample_sort(arena, d, backend=be)
+        out_h, out_l = r.handles.cpu().numpy(), r.lcp.cpu().numpy()
+        e2e.append(time.perf_counter() - t0)
+    te = torch.tensor([sum(e2e) / len(e2e)], dtype=torch.float64, device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        D = datasets.EXPECTED.get(args.config, (0, 0, 0))[2] if args.n is None else None
+        line = {
+            "metric": METRIC, "value": n / (ms_per_step * 1e-3), "unit": "strings/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"config{args.config}: {datasets.DESCRIPTION[args.config]}",
+                       "n": int(n), "arena_bytes": int(arena.data.size),
+                       "parallelism": f"dp{world}: sample-sort partition, NCCL all-to-all, local S^5",
+                       "l2": "256 MiB L2 flush before every step (untimed)"},
+            "d_chars_per_s": D / (ms_per_step * 1e-3) if D else None,
+            "e2e": {"value": n / float(te.item()), "unit": "strings/s",
+                    "h2d_bytes_per_step": int(8 * n), "d2h_bytes_per_step": int(16 * n - 8),
+                    "note": "host shards in, host slices + LCP out, all ranks"},
+            "sorted_ok": bool(ok.item()), "slice_sizes": res.counts, "clocks": clk,
+            "gpu_launches": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -391,6 +474,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif dist_env()[0] > 1:
+        run_distributed(args)
     else:
         run_ours(args)
 

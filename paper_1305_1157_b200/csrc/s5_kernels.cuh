@@ -635,7 +635,7 @@ constexpr uint32_t kTieGroupMax = 16;
 // 88 bytes past the terminator (S5_ARENA_PAD = 128).
 constexpr uint32_t kWalkKeys = 8;
 
-__device__ __forceinline__ int walk_compare(const uint8_t* __restrict__ arena, uint64_t a,
+__device__ __noinline__ int walk_compare(const uint8_t* __restrict__ arena, uint64_t a,
                                             uint64_t b, uint64_t depth, uint64_t* lcp_out,
                                             unsigned long long& fetches) {
     {   // first 16 bytes: most ties are decided here, keep the traffic small
@@ -697,6 +697,26 @@ __device__ __forceinline__ void resolve_pair(const SortArgs& A, const Seg& s,
     if (A.lcp) A.lcp[s.begin + q] = l;
 }
 
+// block-wide min and max of one u64 per thread (all threads call)
+template <uint32_t THREADS>
+__device__ __forceinline__ void block_minmax(uint64_t& mn, uint64_t& mx, uint64_t (*red)[32]) {
+    for (uint32_t x = 16; x > 0; x >>= 1) {
+        uint64_t a = __shfl_xor_sync(0xffffffffu, mn, x), b = __shfl_xor_sync(0xffffffffu, mx, x);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+    }
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { red[0][w] = mn; red[1][w] = mx; }
+    __syncthreads();
+    mn = red[0][0];
+    mx = red[1][0];
+    for (uint32_t q = 1; q < THREADS / 32; ++q) {
+        mn = red[0][q] < mn ? red[0][q] : mn;
+        mx = red[1][q] > mx ? red[1][q] : mx;
+    }
+    __syncthreads();
+}
+
 // bucket b of a k_local step left the CTA as a child segment
 __device__ __forceinline__ bool local_child(const SortArgs& A, const uint32_t* starts,
                                             const uint64_t* tree, uint32_t d, uint32_t b) {
@@ -741,7 +761,8 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     uint32_t* warp_sums = hist + (L::hist_bytes / 4);
     __shared__ EmitScratch es;
 
-    const Seg s = segs[blockIdx.x];
+    Seg s = segs[blockIdx.x];
+    __shared__ uint64_t red[2][32];
     const uint32_t dcap = A.dmax < L::dl ? A.dmax : L::dl;
     uint32_t d = ceil_log2((s.size + 7) / 8);
     d = d < 1 ? 1 : (d > dcap ? dcap : d);
@@ -762,9 +783,62 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         rk[j] = i < s.size ? gkey[i] : 0;
         ro[j] = i < s.size ? goff[i] : 0;
     }
+    // common-prefix skip: when the smallest and largest key share >= 4 bytes
+    // every string does, so the depth advances by that much in-CTA (the
+    // equality-bucket chain of long shared prefixes, classifier.py:297-303,
+    // without a level per 8 bytes); all-identical terminated keys finish here
+    unsigned long long fetches = 0;
+    const uint32_t seg_depth0 = s.depth;
+    for (;;) {
+        uint64_t mn = ~0ull, mx = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < ITEMS; ++j) {
+            if (threadIdx.x + j * THREADS < s.size) {
+                mn = rk[j] < mn ? rk[j] : mn;
+                mx = rk[j] > mx ? rk[j] : mx;
+            }
+        }
+        block_minmax<THREADS>(mn, mx, red);
+        uint32_t L;
+        if (mn == mx) {
+            if (has_zero_byte(mn)) {  // identical strings: any order, lcp = |s|
+#pragma unroll
+                for (uint32_t j = 0; j < ITEMS; ++j) {
+                    uint32_t i = threadIdx.x + j * THREADS;
+                    if (i < s.size) {
+                        A.out[s.begin + i] = ro[j];
+                        if (A.lcp && i + 1 < s.size) A.lcp[s.begin + i] = s.depth + zero_index(mn);
+                    }
+                }
+                for (uint32_t x = 16; x > 0; x >>= 1)
+                    fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
+                if ((threadIdx.x & 31) == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
+                return;
+            }
+            L = 8;
+        } else {
+            L = diff_bytes(mn, mx);
+        }
+        if (L < 4) break;
+        s.depth += L;
+#pragma unroll
+        for (uint32_t j = 0; j < ITEMS; ++j) {
+            if (threadIdx.x + j * THREADS < s.size) {
+                rk[j] = load_key(A.arena, static_cast<uint64_t>(ro[j]) + s.depth);
+                ++fetches;
+            }
+        }
+    }
     const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
-    for (uint32_t t = threadIdx.x; t < M; t += THREADS)
-        sample[t] = t < m ? gkey[sample_index(sseed, t, s.size)] : ~0ull;
+    for (uint32_t t = threadIdx.x; t < M; t += THREADS) {
+        uint64_t x = ~0ull;
+        if (t < m) {
+            uint32_t idx = sample_index(sseed, t, s.size);
+            x = s.depth == seg_depth0 ? gkey[idx]
+                                      : load_key(A.arena, static_cast<uint64_t>(goff[idx]) + s.depth);
+        }
+        sample[t] = x;
+    }
     __syncthreads();
     sort_sample<THREADS>(sample, M);
     build_tree_levels<THREADS>(sample, m, d, tree, na, nb, nf);
@@ -792,7 +866,6 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
 
     // distribute: finished buckets -> final slots; children -> other side;
     // small buckets -> shared memory for the base case
-    unsigned long long fetches = 0;
     const uint32_t ns = s.side ^ 1u;
 #pragma unroll
     for (uint32_t j = 0; j < ITEMS; ++j) {
