@@ -626,7 +626,50 @@ __device__ __forceinline__ bool lone_tie(const uint64_t* key1, const uint16_t* p
     return (q == bs || key1[perm[q - 1]] != k) && (q + 2 >= be || key1[perm[q + 2]] != k);
 }
 
-constexpr uint32_t kTieGroupMax = 16;
+// A tie group of g <= 32 equal unterminated keys at sorted positions
+// gs..gs+g-1 of an owned bucket, finished by one warp: the k_small loop on
+// (run, key) starting one word deeper; writes its pair LCPs and its order.
+__device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uint32_t gs,
+                                            const uint32_t* off1, uint16_t* perm,
+                                            const uint8_t* res, uint64_t depth, uint32_t lane,
+                                            unsigned long long& fetches) {
+    uint32_t ge = gs;
+    while (res[ge] == 2) ++ge;
+    const uint32_t g = ge - gs + 1;
+    const bool valid = lane < g;
+    const bool pair_valid = lane + 1 < g;
+    uint32_t e = valid ? perm[gs + lane] : 0u;
+    uint32_t run = valid ? 0u : 0xFFFFFFFFu;
+    uint64_t k = ~0ull;
+    bool resolved = false, active = valid;
+    for (;;) {
+        depth += 8;
+        if (active) {
+            k = load_key(A.arena, static_cast<uint64_t>(off1[e]) + depth);
+            ++fetches;
+        }
+        warp_bitonic(run, k, e, lane);
+        uint64_t nk = __shfl_down_sync(0xffffffffu, k, 1);
+        uint32_t nrun = __shfl_down_sync(0xffffffffu, run, 1);
+        if (pair_valid && !resolved && nrun == run) {
+            if (k != nk) {
+                if (A.lcp) A.lcp[s.begin + gs + lane] = depth + diff_bytes(k, nk);
+                resolved = true;
+            } else if (has_zero_byte(k)) {
+                if (A.lcp) A.lcp[s.begin + gs + lane] = depth + zero_index(k);
+                resolved = true;
+            }
+        }
+        uint32_t unres = __ballot_sync(0xffffffffu, pair_valid && !resolved);
+        if (!unres) break;
+        bool prev_unres = lane > 0 && ((unres >> (lane - 1)) & 1u);
+        uint32_t starts = __ballot_sync(0xffffffffu, !prev_unres);
+        uint32_t le = starts & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
+        active = ((unres >> lane) & 1u) || prev_unres;
+        if (valid) run = 31u - __clz(le);
+    }
+    if (valid) perm[gs + lane] = static_cast<uint16_t>(e);
+}
 
 // strings.py:64-74 (_compare_from) + :56-61 (_lcp_pair) in one walk from a
 // depth both strings are known to share, 64 bytes per step: the step's 24
@@ -741,7 +784,7 @@ struct LocalSmem {
 };
 
 template <uint32_t THREADS, uint32_t ITEMS, bool EQUAL>
-__global__ void __launch_bounds__(THREADS, (THREADS >= 512 ? 2 : 4))
+__global__ void __launch_bounds__(THREADS, (THREADS >= 512 ? 2 : 8))
 k_local(SortArgs A, const Seg* __restrict__ segs) {
     using L = LocalSmem<THREADS, ITEMS>;
     extern __shared__ __align__(16) uint8_t sm[];
@@ -912,13 +955,14 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         perm[bs + r] = static_cast<uint16_t>(p);
     }
     __syncthreads();
-    // resolve adjacent pairs; equal unterminated keys form runs that are
-    // refilled at depth+8 and re-ranked (the mkqs equal-partition refill,
-    // basesort.py:146-150), until every pair is resolved:
+    // resolve adjacent pairs at the segment depth:
     //   keys differ            -> lcp = depth + equal leading bytes
     //   keys equal, terminated -> identical strings, lcp = depth + |rest|
-    uint64_t depth = s.depth;
-    bool any = false;
+    //   exactly two equal keys -> one direct string walk (resolve_pair)
+    //   >= 3 equal keys        -> a tie group, finished by one warp below
+    const uint64_t depth = s.depth;
+    __shared__ uint32_t ngroups;
+    if (threadIdx.x == 0) ngroups = 0;
     for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
         if (!own[q]) continue;
         const uint32_t b = bpos[q], bs = hist[b], be = hist[b + 1];
@@ -932,110 +976,24 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
             } else if (lone_tie(key1, perm, q, bs, be, ka)) {
                 resolve_pair(A, s, key1, off1, perm, q, depth + 8, fetches);
             } else {
-                // tie group of >= 3 equal keys: small ones are ordered below
-                // by direct string comparison, larger ones by refill rounds
-                uint32_t gs = q, ge = q + 1;
-                while (gs > bs && key1[perm[gs - 1]] == ka) --gs;
-                while (ge + 1 < be && key1[perm[ge + 1]] == ka) ++ge;
-                if (ge - gs + 1 <= kTieGroupMax) {
-                    rv = 2;
-                } else {
-                    rv = 0;
-                    any = true;
-                }
+                rv = 2;
             }
         }
         res[q] = rv;
     }
-    // small tie groups: rank every member by direct comparison with the others
-    // (order among identical strings is free), then one walk per adjacent pair
-    // for its LCP -- no CTA-wide refill rounds
     __syncthreads();
     for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
-        if (!own[q]) continue;
-        const uint32_t bs = hist[bpos[q]];
-        if (!(res[q] == 2 || (q > bs && res[q - 1] == 2))) continue;
-        uint32_t gs = q, ge = q;
-        while (gs > bs && res[gs - 1] == 2) --gs;
-        while (res[ge] == 2) ++ge;
-        // rank by (string, position); the LCP with the successor in that order
-        // is the largest LCP with any greater member (sorted-order LCPs only
-        // shrink with distance), so the same walks give the pair LCP
-        const uint64_t a = off1[perm[q]];
-        uint32_t r = 0;
-        uint64_t succ = 0;
-        for (uint32_t t = gs; t <= ge; ++t) {
-            if (t == q) continue;
-            uint64_t l;
-            int c = walk_compare(A.arena, a, off1[perm[t]], depth + 8, &l, fetches);
-            if (c > 0 || (c == 0 && t < q)) ++r;
-            else if (l > succ) succ = l;
-        }
-        perm2[gs + r] = perm[q];
-        if (A.lcp && gs + r < ge) A.lcp[s.begin + gs + r] = succ;
+        if (own[q] && res[q] == 2 && (q == hist[bpos[q]] || res[q - 1] != 2))
+            perm2[atomicAdd(&ngroups, 1u)] = static_cast<uint16_t>(q);
     }
     __syncthreads();
-    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
-        if (!own[q]) continue;
-        const uint32_t bs = hist[bpos[q]];
-        if (res[q] == 2 || (q > bs && res[q - 1] == 2)) perm[q] = perm2[q];
-    }
+    // one warp per tie group (<= small_max strings): bitonic sort of
+    // (run, key) with refills at depth+8, pair LCPs emitted when resolved
+    // (the mkqs equal-partition refill, basesort.py:146-150, without
+    // CTA-wide rounds)
+    for (uint32_t g = threadIdx.x >> 5; g < ngroups; g += THREADS / 32)
+        tie_group_warp(A, s, perm2[g], off1, perm, res, depth, lane, fetches);
     __syncthreads();
-    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS)
-        if (own[q] && res[q] == 2) res[q] = 1;
-    while (__syncthreads_or(any)) {
-        depth += 8;
-        any = false;
-        for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
-            if (!own[q]) continue;
-            const uint32_t bs = hist[bpos[q]];
-            if (res[q] == 0 || (q > bs && res[q - 1] == 0)) {
-                const uint32_t a = perm[q];
-                key1[a] = load_key(A.arena, static_cast<uint64_t>(off1[a]) + depth);
-                ++fetches;
-            }
-        }
-        __syncthreads();
-        for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
-            if (!own[q]) continue;
-            const uint32_t bs = hist[bpos[q]];
-            if (!(res[q] == 0 || (q > bs && res[q - 1] == 0))) continue;
-            uint32_t rs = q, re = q;
-            while (rs > bs && res[rs - 1] == 0) --rs;
-            while (res[re] == 0) ++re;
-            const uint64_t x = key1[perm[q]];
-            uint32_t r = 0;
-            for (uint32_t t = rs; t <= re; ++t) {
-                uint64_t y = key1[perm[t]];
-                r += (y < x) || (y == x && t < q);
-            }
-            perm2[rs + r] = perm[q];
-        }
-        __syncthreads();
-        for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
-            if (!own[q]) continue;
-            const uint32_t bs = hist[bpos[q]];
-            if (res[q] == 0 || (q > bs && res[q - 1] == 0)) perm[q] = perm2[q];
-        }
-        __syncthreads();
-        for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
-            if (!own[q] || res[q]) continue;
-            uint64_t ka = key1[perm[q]], kb = key1[perm[q + 1]];
-            const uint32_t b = bpos[q];
-            if (ka != kb) {
-                if (A.lcp) A.lcp[s.begin + q] = depth + diff_bytes(ka, kb);
-                res[q] = 1;
-            } else if (has_zero_byte(ka)) {
-                if (A.lcp) A.lcp[s.begin + q] = depth + zero_index(ka);
-                res[q] = 1;
-            } else if (lone_tie(key1, perm, q, hist[b], hist[b + 1], ka)) {
-                resolve_pair(A, s, key1, off1, perm, q, depth + 8, fetches);
-                res[q] = 1;
-            } else {
-                any = true;
-            }
-        }
-    }
     for (uint32_t q = threadIdx.x; q < s.size; q += THREADS)
         if (own[q]) A.out[s.begin + q] = off1[perm[q]];
 
