@@ -326,22 +326,19 @@ def run_ours(args):
     kern = {}
     for ps in prof_stats:
         for name, rec in ps["kernels"].items():
-            k = kern.setdefault(name, {"ms": 0.0, "launches": 0})
+            k = kern.setdefault(name, {"ms": 0.0, "launches": 0, "strings": 0})
             k["ms"] += rec["ms"] / len(prof_stats)
             k["launches"] += rec["launches"] / len(prof_stats)
+            k["strings"] += rec["strings"] / len(prof_stats)
     peak, peak_src = hbm_peak()
     n_p = st["n_per_pass"]
     B_alg = 16 * sum(n_p) + D  # 16 B per string per S^5 level / base-case pass
-    # dominant kernel and its algorithmic bytes: 16 B (8-B pointer read + write)
-    # per string it moves per launch, + D for the arena-reading kernels' share
-    per_kernel_strings = {
-        "k_narrow": sum(st["narrow_elems"]), "k_small": sum(st["small_elems"]),
-        "k_wide_scatter": sum(st["wide_elems"]), "k_wide_count": sum(st["wide_elems"]),
-        "k_gather": n,
-    }
-    dom = max(kern.items(), key=lambda kv: kv[1]["ms"]) if kern else ("none", {"ms": 0, "launches": 1})
+    # dominant kernel and its algorithmic bytes: 16 B (8-B pointer read + write,
+    # SURVEY 8(d)) per string it moves, strings counted by the library per launch
+    dom = max(kern.items(), key=lambda kv: kv[1]["ms"]) if kern else \
+        ("none", {"ms": 0, "launches": 1, "strings": 0})
     dom_name, dom_rec = dom
-    strings = per_kernel_strings.get(dom_name, 0)
+    strings = dom_rec["strings"]
     launches = max(dom_rec["launches"], 1)
     per_launch_bytes = 16.0 * strings / launches
     per_launch_ms = dom_rec["ms"] / launches
@@ -396,6 +393,8 @@ def run_ours(args):
                           "floor_frac": (16 * n + D) / (ms_per_step * 1e-3) / 1e9 / peak},
         "n_per_pass": n_p,
         "kernels_ms_per_step": {k: round(v["ms"], 4) for k, v in sorted(kern.items())},
+        "kernels_strings_per_step": {k: int(v["strings"]) for k, v in sorted(kern.items())},
+        "launch_recs": prof_stats[-1].get("launch_recs", []) if args.launch_recs else None,
         "e2e": {"value": world * n / e2e_s, "unit": "strings/s",
                 "h2d_bytes_per_step": int(8 * n), "d2h_bytes_per_step": int(8 * n + 8 * (n - 1)),
                 "ms_per_step": 1e3 * e2e_s,
@@ -467,6 +466,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--classifier", default="unroll", choices=["unroll", "equal"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--launch-recs", action="store_true",
+                    help="add per-launch (kernel, level, strings, ms) records")
     ap.add_argument("--cfg", action="append", default=[],
                     help="SampleSortConfig override key=value (tuning), repeatable")
     args = ap.parse_args()

@@ -51,7 +51,7 @@ typedef struct {
     uint32_t classifier;  /* 0 = "unroll", 1 = "equal" (samplesort.py:43)      */
     uint32_t small_max;   /* segments <= small_max: warp base case (<= 32)      */
     uint32_t narrow_max;  /* segments <= narrow_max: one-CTA S^5 step (<=16384) */
-    uint32_t flags;       /* bit0: skip LCP fix-up (debug); bit1: per-kernel timing */
+    uint32_t flags;       /* bit0: skip LCP fix-up (debug); bit1: per-kernel timing; bit2: no common-prefix skip */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
     uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (255)  */
@@ -61,6 +61,14 @@ typedef struct {
 
 /* Per-call statistics (Counters, counters.py:8-37; SURVEY 8(d) n_p log). */
 #define S5_MAX_LEVELS 128
+#define S5_MAX_LAUNCH_RECS 512
+typedef struct {
+    uint32_t kernel;   /* S5_K_* */
+    uint32_t level;
+    uint64_t strings;  /* strings the launch processed */
+    float ms;          /* device time (CUDA events on the stream) */
+    float pad_;
+} s5_launch_rec;
 typedef struct {
     uint32_t levels;                     /* level-synchronous passes run          */
     uint32_t pad_;
@@ -82,6 +90,10 @@ typedef struct {
     uint32_t kern_launches[16];
     uint64_t local_elems[S5_MAX_LEVELS]; /* of which in one-CTA S^5 + base case    */
     uint64_t local_steps;                /* one-CTA S^5 + base-case segments      */
+    uint64_t kern_strings[16];           /* strings processed per kernel (S5_K_*)  */
+    uint32_t n_launch_recs;              /* flags bit1: per-launch records        */
+    uint32_t pad3_;
+    s5_launch_rec launch_recs[S5_MAX_LAUNCH_RECS];
 } s5_stats;
 
 enum {

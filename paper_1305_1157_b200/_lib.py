@@ -35,6 +35,14 @@ class S5Config(C.Structure):
                 ("wide_target", C.c_uint32), ("reserved", C.c_uint32)]
 
 
+S5_MAX_LAUNCH_RECS = 512
+
+
+class S5LaunchRec(C.Structure):
+    _fields_ = [("kernel", C.c_uint32), ("level", C.c_uint32), ("strings", C.c_uint64),
+                ("ms", C.c_float), ("pad_", C.c_float)]
+
+
 class S5Stats(C.Structure):
     _fields_ = [("levels", C.c_uint32), ("pad_", C.c_uint32),
                 ("n_per_pass", C.c_uint64 * S5_MAX_LEVELS),
@@ -46,7 +54,9 @@ class S5Stats(C.Structure):
                 ("boundary_lcps", C.c_uint64), ("launches", C.c_uint64),
                 ("ms_total", C.c_float), ("pad2_", C.c_float),
                 ("kern_ms", C.c_float * 16), ("kern_launches", C.c_uint32 * 16),
-                ("local_elems", C.c_uint64 * S5_MAX_LEVELS), ("local_steps", C.c_uint64)]
+                ("local_elems", C.c_uint64 * S5_MAX_LEVELS), ("local_steps", C.c_uint64),
+                ("kern_strings", C.c_uint64 * 16), ("n_launch_recs", C.c_uint32),
+                ("pad3_", C.c_uint32), ("launch_recs", S5LaunchRec * S5_MAX_LAUNCH_RECS)]
 
     def as_dict(self) -> dict:
         L = min(self.levels, S5_MAX_LEVELS)
@@ -62,8 +72,12 @@ class S5Stats(C.Structure):
             "small_segments": int(self.small_segments), "key_fetches": int(self.key_fetches),
             "boundary_lcps": int(self.boundary_lcps), "ms_total": float(self.ms_total),
             "launches": int(self.launches),
+            "launch_recs": [(KERNELS[r.kernel] if r.kernel < len(KERNELS) else str(r.kernel),
+                             int(r.level), int(r.strings), round(float(r.ms), 4))
+                            for r in self.launch_recs[:min(self.n_launch_recs, S5_MAX_LAUNCH_RECS)]],
             "kernels": {KERNELS[i]: {"ms": float(self.kern_ms[i]),
-                                     "launches": int(self.kern_launches[i])}
+                                     "launches": int(self.kern_launches[i]),
+                                     "strings": int(self.kern_strings[i])}
                         for i in range(len(KERNELS)) if self.kern_launches[i]},
         }
 

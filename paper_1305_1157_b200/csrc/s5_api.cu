@@ -186,13 +186,16 @@ struct Prof {
     cudaStream_t st = nullptr;
     uint64_t launches = 0;
     uint32_t count[16] = {};
-    struct Rec { int k; cudaEvent_t a, b; };
+    struct Rec { int k; uint32_t level; uint64_t strings; cudaEvent_t a, b; };
     std::vector<Rec> recs;
-    void begin(int k) {
+    uint64_t elems[16] = {};
+    uint32_t level = 0;
+    void begin(int k, uint64_t strings = 0) {
         ++launches;
         ++count[k];
+        elems[k] += strings;
         if (!on) return;
-        Rec r{k, nullptr, nullptr};
+        Rec r{k, level, strings, nullptr, nullptr};
         cudaEventCreate(&r.a);
         cudaEventCreate(&r.b);
         cudaEventRecord(r.a, st);
@@ -204,18 +207,28 @@ struct Prof {
     void finish(s5_stats* stats) {
         if (stats) {
             stats->launches = launches;
-            for (int k = 0; k < 16; ++k) stats->kern_launches[k] = count[k];
+            for (int k = 0; k < 16; ++k) {
+                stats->kern_launches[k] = count[k];
+                stats->kern_strings[k] = elems[k];
+            }
         }
+        uint32_t nrec = 0;
         for (auto& r : recs) {
             float ms = 0;
             if (stats && cudaEventSynchronize(r.b) == cudaSuccess &&
-                cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess)
+                cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
                 stats->kern_ms[r.k] += ms;
+                if (nrec < S5_MAX_LAUNCH_RECS)
+                    stats->launch_recs[nrec++] = s5_launch_rec{static_cast<uint32_t>(r.k), r.level,
+                                                               r.strings, ms, 0.0f};
+            }
             cudaEventDestroy(r.a);
             cudaEventDestroy(r.b);
         }
+        recs_total = recs.size();
         recs.clear();
     }
+    size_t recs_total = 0;
 };
 
 }  // namespace
@@ -287,6 +300,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.narrow_max = c.narrow_max;
     A.dmax = c.dmax;
     A.alpha = c.alpha;
+    A.flags = c.flags;
     A.seed = c.seed;
 
     WidePlan P{};
@@ -306,7 +320,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     Prof prof;
     prof.on = stats && (c.flags & 2);
     prof.st = st;
-    prof.begin(S5_K_GATHER);
+    prof.begin(S5_K_GATHER, n);
     k_gather<<<grid_for(n, 256), 256, 0, st>>>(d_handles, static_cast<uint32_t>(n), depth,
                                                 arena_len, A);
     prof.end();
@@ -318,6 +332,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     unsigned long long fetches_total = 0, hints_total = 0;
     uint32_t level = 0;
     for (;; ++level) {
+        prof.level = level;
         S5_CUDA(cudaMemcpyAsync(hp.ctl, A.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         S5_CUDA(cudaStreamSynchronize(st));
         Ctl h = *hp.ctl;
@@ -384,7 +399,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             uint32_t ub = static_cast<uint32_t>(std::min<uint64_t>(
                 uint64_t(m[WIDE]) * kWideCtasMax, n / kWideChunkMin + m[WIDE]));
             const int wsm = wide_smem(c.wide_dcap);
-            prof.begin(S5_K_WIDE_COUNT);
+            prof.begin(S5_K_WIDE_COUNT, h.elems[WIDE]);
             if (c.classifier)
                 k_wide_count<true><<<ub, kWideThreads, wsm, st>>>(A, P);
             else
@@ -397,12 +412,12 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             prof.begin(S5_K_WIDE_BSCAN);
             k_wide_bscan<<<m[WIDE], 1024, 0, st>>>(A, P);
             prof.end();
-            prof.begin(S5_K_WIDE_SCATTER);
+            prof.begin(S5_K_WIDE_SCATTER, h.elems[WIDE]);
             k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::total, st>>>(A, P);
             prof.end();
         }
         if (m[NARROW]) {
-            prof.begin(S5_K_NARROW);
+            prof.begin(S5_K_NARROW, h.elems[NARROW]);
             if (c.classifier)
                 k_narrow<true><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
             else
@@ -410,7 +425,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             prof.end();
         }
         if (m[LOCAL_S]) {
-            prof.begin(S5_K_LOCAL_S);
+            prof.begin(S5_K_LOCAL_S, h.elems[LOCAL_S]);
             if (c.classifier)
                 k_local<kLocalSThreads, kLocalSItems, true>
                     <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, st>>>(A, segs[LOCAL_S]);
@@ -420,7 +435,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             prof.end();
         }
         if (m[LOCAL]) {
-            prof.begin(S5_K_LOCAL);
+            prof.begin(S5_K_LOCAL, h.elems[LOCAL]);
             if (c.classifier)
                 k_local<kLocalThreads, kLocalItems, true>
                     <<<m[LOCAL], kLocalThreads, LocalCfg::total, st>>>(A, segs[LOCAL]);
@@ -431,14 +446,14 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         }
         if (m[SMALL]) {
             uint32_t blocks = (m[SMALL] + 7) / 8;
-            prof.begin(S5_K_SMALL);
+            prof.begin(S5_K_SMALL, h.elems[SMALL]);
             k_small<<<blocks, 256, 0, st>>>(A, segs[SMALL], m[SMALL]);
             prof.end();
         }
         S5_CUDA(cudaGetLastError());
     }
     if (d_lcp && !(c.flags & 1)) {
-        prof.begin(S5_K_LCP_FIX);
+        prof.begin(S5_K_LCP_FIX, hints_total);
         if (hints_total)
             k_lcp_fix<<<grid_for(hints_total, 256), 256, 0, st>>>(d_arena, d_handles, d_lcp,
                                                                   A.hint_list, hints_total);
@@ -456,6 +471,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         stats->boundary_lcps = hints_total;
     }
     prof.finish(stats);
+    if (stats) stats->n_launch_recs = static_cast<uint32_t>(std::min<size_t>(prof.recs_total, S5_MAX_LAUNCH_RECS));
     return 0;
 }
 

@@ -57,6 +57,7 @@ struct SortArgs {
     uint32_t wide_dcap;    // wide steps use d <= wide_dcap (<= kWideDMax)
     uint32_t wide_target;  // wide steps aim at children of about this size
     uint32_t alpha;
+    uint32_t flags;        // s5_config flags (bit2: no common-prefix skip)
     uint64_t seed;
 };
 
@@ -862,7 +863,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         } else {
             L = diff_bytes(mn, mx);
         }
-        if (L < 4) break;
+        if (L < 4 || (A.flags & 4)) break;
         s.depth += L;
 #pragma unroll
         for (uint32_t j = 0; j < ITEMS; ++j) {

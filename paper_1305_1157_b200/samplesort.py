@@ -55,12 +55,14 @@ class SampleSortConfig:
     local_max: int = 4096
     wide_v: int = 255
     wide_target: int = 0
+    flags: int = 0
 
     def to_c(self) -> _lib.S5Config:
         if self.classifier not in ("unroll", "equal"):
             raise ValueError(f"unknown classifier {self.classifier!r}")
         return _lib.S5Config(self.v, self.alpha, 1 if self.classifier == "equal" else 0,
-                             self.small_max, self.narrow_max, 0, self.seed, self.local_max,
+                             self.small_max, self.narrow_max, self.flags, self.seed,
+                             self.local_max,
                              self.wide_v, self.wide_target, 0)
 
 
