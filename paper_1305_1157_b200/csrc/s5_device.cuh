@@ -105,6 +105,7 @@ template <bool EQUAL>
 __device__ __forceinline__ uint32_t classify(uint64_t k, const uint64_t* t, uint32_t d) {
     if (!EQUAL) {
         uint32_t i = 1;
+#pragma unroll 1
         for (uint32_t l = 0; l < d; ++l) i = 2 * i + (k > t[i] ? 1u : 0u);
         uint32_t c = i - (1u << d);
         uint32_t b = 2 * c;
@@ -134,6 +135,7 @@ __device__ __forceinline__ void classify_iw(const uint64_t (&k)[IW], const uint6
         uint32_t i[IW];
 #pragma unroll
         for (int j = 0; j < IW; ++j) i[j] = 1;
+#pragma unroll 1
         for (uint32_t l = 0; l < d; ++l) {
 #pragma unroll
             for (int j = 0; j < IW; ++j) i[j] = 2 * i[j] + (k[j] > t[i[j]] ? 1u : 0u);

@@ -142,7 +142,7 @@ __device__ void bitonic_sort_smem(uint64_t* s, uint32_t M) {
 // searches (the sample is sorted), an empty range yields the fallback for the
 // whole subtree (D5).  Produces exactly the reference's splitters.
 template <uint32_t THREADS>
-__device__ void build_tree_levels(const uint64_t* sample, uint32_t m, uint32_t d,
+__device__ __noinline__ void build_tree_levels(const uint64_t* sample, uint32_t m, uint32_t d,
                                   uint64_t* tree, int32_t* na, int32_t* nb, uint32_t* nf) {
     if (threadIdx.x == 0) {
         na[1] = 0;
@@ -191,7 +191,7 @@ __device__ void build_tree_levels(const uint64_t* sample, uint32_t m, uint32_t d
 
 // Exclusive scan of h[0..k) in place, h[k] = total.  All threads call.
 template <uint32_t THREADS>
-__device__ void block_exclusive_scan(uint32_t* h, uint32_t k, uint32_t* warp_sums) {
+__device__ __noinline__ void block_exclusive_scan(uint32_t* h, uint32_t k, uint32_t* warp_sums) {
     const uint32_t per = (k + THREADS) / THREADS;  // covers k+1 slots
     uint32_t lo = threadIdx.x * per;
     uint32_t sum = 0;
@@ -274,7 +274,7 @@ __device__ __forceinline__ void reserve_hints(const SortArgs& A, EmitScratch* es
 // KEEP_SMALL: buckets of <= small_max strings are finished by the calling CTA
 // itself (k_local) instead of becoming children.
 template <uint32_t THREADS, bool KEEP_SMALL = false>
-__device__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* starts, uint32_t k,
+__device__ __noinline__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* starts, uint32_t k,
                            const uint64_t* tree, uint32_t d, EmitScratch* es) {
     if (threadIdx.x < NCLS) {
         es->cnt[threadIdx.x] = 0;
@@ -464,11 +464,12 @@ __device__ __forceinline__ bool comp_less(uint32_t ra, uint64_t ka, uint32_t rb,
     return ra < rb || (ra == rb && ka < kb);
 }
 
+template <bool UNROLL = true>
 __device__ __forceinline__ void warp_bitonic(uint32_t& run, uint64_t& key, uint32_t& off,
                                              uint32_t lane) {
-#pragma unroll
+#pragma unroll (UNROLL ? 5 : 1)
     for (uint32_t k = 2; k <= 32; k <<= 1) {
-#pragma unroll
+#pragma unroll (UNROLL ? 5 : 1)
         for (uint32_t j = k >> 1; j > 0; j >>= 1) {
             uint32_t orun = __shfl_xor_sync(0xffffffffu, run, j);
             uint64_t okey = __shfl_xor_sync(0xffffffffu, key, j);
@@ -571,6 +572,7 @@ __device__ __forceinline__ void warp_sort64(uint64_t& a, uint64_t& b, uint32_t l
 __device__ __forceinline__ void bitonic_reg_stages(uint64_t& a, uint64_t& b, uint32_t lane,
                                                    uint32_t base, uint32_t K, uint32_t jtop) {
     const bool upa = ((base + lane) & K) == 0, upb = ((base + 32 + lane) & K) == 0;
+#pragma unroll 1
     for (uint32_t J = jtop; J > 0; J >>= 1) {
         if (J == 32) {
             if ((a > b) == upa) { uint64_t t = a; a = b; b = t; }
@@ -589,11 +591,12 @@ __device__ __forceinline__ void bitonic_reg_stages(uint64_t& a, uint64_t& b, uin
 // entries, shuffles), only the wider stages go through shared memory --
 // log2(M/64) * (log2(M) - 5) / 2 + log2(M/64) barriers in total.
 template <uint32_t THREADS>
-__device__ void sort_sample(uint64_t* s, uint32_t M) {
+__device__ __noinline__ void sort_sample(uint64_t* s, uint32_t M) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t runs = M / 64;
     for (uint32_t r = warp; r < runs; r += THREADS / 32) {
         uint64_t a = s[r * 64 + lane], b = s[r * 64 + 32 + lane];
+#pragma unroll 1
         for (uint32_t K = 2; K <= 64; K <<= 1) bitonic_reg_stages(a, b, lane, r * 64, K, K >> 1);
         s[r * 64 + lane] = a;
         s[r * 64 + 32 + lane] = b;
@@ -649,7 +652,7 @@ __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uin
             k = load_key(A.arena, static_cast<uint64_t>(off1[e]) + depth);
             ++fetches;
         }
-        warp_bitonic(run, k, e, lane);
+        warp_bitonic<false>(run, k, e, lane);
         uint64_t nk = __shfl_down_sync(0xffffffffu, k, 1);
         uint32_t nrun = __shfl_down_sync(0xffffffffu, run, 1);
         if (pair_valid && !resolved && nrun == run) {
@@ -673,48 +676,18 @@ __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uin
 }
 
 // strings.py:64-74 (_compare_from) + :56-61 (_lcp_pair) in one walk from a
-// depth both strings are known to share, 64 bytes per step: the step's 24
-// loads are independent, so a long common prefix (config-4 duplicate reads,
-// 100 bytes) costs two memory latencies instead of thirteen.  Reads at most
-// 88 bytes past the terminator (S5_ARENA_PAD = 128).
-constexpr uint32_t kWalkKeys = 8;
-
+// depth both strings are known to share, 16 bytes per step.
 __device__ __noinline__ int walk_compare(const uint8_t* __restrict__ arena, uint64_t a,
-                                            uint64_t b, uint64_t depth, uint64_t* lcp_out,
-                                            unsigned long long& fetches) {
-    {   // first 16 bytes: most ties are decided here, keep the traffic small
-        uint64_t a0, a1, b0, b1;
-        load_key2(arena, a + depth, a0, a1);
-        load_key2(arena, b + depth, b0, b1);
-        fetches += 2;
-        if (a0 != b0) {
-            if (lcp_out) *lcp_out = depth + diff_bytes(a0, b0);
-            return a0 < b0 ? -1 : 1;
-        }
-        if (has_zero_byte(a0)) {
-            if (lcp_out) *lcp_out = depth + zero_index(a0);
-            return 0;
-        }
-        if (a1 != b1) {
-            if (lcp_out) *lcp_out = depth + 8 + diff_bytes(a1, b1);
-            return a1 < b1 ? -1 : 1;
-        }
-        if (has_zero_byte(a1)) {
-            if (lcp_out) *lcp_out = depth + 8 + zero_index(a1);
-            return 0;
-        }
-        depth += 16;
-    }
-    for (;; depth += 8 * kWalkKeys) {
-        uint64_t ka[kWalkKeys], kb[kWalkKeys];
-#pragma unroll
-        for (uint32_t t = 0; t < kWalkKeys / 2; ++t) {
-            load_key2(arena, a + depth + 16 * t, ka[2 * t], ka[2 * t + 1]);
-            load_key2(arena, b + depth + 16 * t, kb[2 * t], kb[2 * t + 1]);
-        }
+                                         uint64_t b, uint64_t depth, uint64_t* lcp_out,
+                                         unsigned long long& fetches) {
+#pragma unroll 1
+    for (;; depth += 16) {
+        uint64_t ka[2], kb[2];
+        load_key2(arena, a + depth, ka[0], ka[1]);
+        load_key2(arena, b + depth, kb[0], kb[1]);
         fetches += 2;
 #pragma unroll
-        for (uint32_t t = 0; t < kWalkKeys; ++t) {
+        for (uint32_t t = 0; t < 2; ++t) {
             if (ka[t] != kb[t]) {
                 if (lcp_out) *lcp_out = depth + 8 * t + diff_bytes(ka[t], kb[t]);
                 return ka[t] < kb[t] ? -1 : 1;
@@ -754,6 +727,7 @@ __device__ __forceinline__ void block_minmax(uint64_t& mn, uint64_t& mx, uint64_
     __syncthreads();
     mn = red[0][0];
     mx = red[1][0];
+#pragma unroll 1
     for (uint32_t q = 1; q < THREADS / 32; ++q) {
         mn = red[0][q] < mn ? red[0][q] : mn;
         mx = red[1][q] > mx ? red[1][q] : mx;
@@ -892,11 +866,12 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     // classify + rank (warp-aggregated shared-memory histogram)
     const uint32_t lane = threadIdx.x & 31;
     uint32_t rbr[ITEMS];  // bucket | rank-in-bucket << 11
+    classify_iw<EQUAL, ITEMS>(rk, tree, d, rbr);
 #pragma unroll
     for (uint32_t j = 0; j < ITEMS; ++j) {
         uint32_t i = threadIdx.x + j * THREADS;
         bool act = i < s.size;
-        uint32_t b = act ? classify<EQUAL>(rk[j], tree, d) : 0x7FFu;
+        uint32_t b = act ? rbr[j] : 0x7FFu;
         uint32_t peers = __match_any_sync(0xffffffffu, b);
         uint32_t leader = __ffs(peers) - 1;
         uint32_t r = 0;
@@ -908,37 +883,45 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     block_exclusive_scan<THREADS>(hist, k, warp_sums);
     emit_block<THREADS, true>(A, s, hist, k, tree, d, &es);
 
-    // distribute: finished buckets -> final slots; children -> other side;
-    // small buckets -> shared memory for the base case
-    const uint32_t ns = s.side ^ 1u;
+    // distribute: the bucketed copy goes to shared memory (registers -> smem),
+    // then one pass in position order sends finished buckets to their final
+    // slots and children to the other side (consecutive positions ->
+    // consecutive addresses), keeping small buckets for the base case
 #pragma unroll
     for (uint32_t j = 0; j < ITEMS; ++j) {
         uint32_t i = threadIdx.x + j * THREADS;
         if (i >= s.size) continue;
         uint32_t b = rbr[j] & 0x7FFu;
-        uint32_t start = hist[b], end = hist[b + 1], cnt = end - start;
-        uint32_t p = start + (rbr[j] >> 11);
-        bool odd = b & 1;
-        bool fin = cnt == 1 || (odd && has_zero_byte(rk[j]));
+        uint32_t p = hist[b] + (rbr[j] >> 11);
         bpos[p] = static_cast<uint16_t>(b);
-        bool mine = !fin && cnt <= A.small_max;
+        key1[p] = rk[j];
+        off1[p] = ro[j];
+    }
+    __syncthreads();
+    const uint32_t ns = s.side ^ 1u;
+#pragma unroll 1
+    for (uint32_t p = threadIdx.x; p < s.size; p += THREADS) {
+        const uint32_t b = bpos[p];
+        const uint32_t end = hist[b + 1], cnt = end - hist[b];
+        const uint64_t kk = key1[p];
+        const uint32_t o = off1[p];
+        const bool odd = b & 1;
+        const bool fin = cnt == 1 || (odd && has_zero_byte(kk));
+        const bool mine = !fin && cnt <= A.small_max;
         own[p] = mine;
-        uint32_t dst = s.begin + p;
+        const uint32_t dst = s.begin + p;
         if (fin) {
-            A.out[dst] = ro[j];
-            if (odd && A.lcp && p + 1 < end) A.lcp[dst] = s.depth + zero_index(rk[j]);
-            off1[p] = ro[j];
+            A.out[dst] = o;
+            if (odd && A.lcp && p + 1 < end) A.lcp[dst] = s.depth + zero_index(kk);
             perm[p] = static_cast<uint16_t>(p);
-        } else if (mine) {
-            key1[p] = rk[j];
-            off1[p] = ro[j];
-        } else if (odd) {
-            A.off[ns][dst] = ro[j];
-            A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(ro[j]) + s.depth + 8);
-            ++fetches;
-        } else {
-            A.off[ns][dst] = ro[j];
-            A.key[ns][dst] = rk[j];
+        } else if (!mine) {
+            A.off[ns][dst] = o;
+            if (odd) {
+                A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + s.depth + 8);
+                ++fetches;
+            } else {
+                A.key[ns][dst] = kk;
+            }
         }
     }
     __syncthreads();
@@ -1010,9 +993,9 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
             if (local_child(A, hist, tree, d, b) || local_child(A, hist, tree, d, bpos[st - 1])) {
                 ++my_hints;
             } else {
-                uint64_t ka = load_key(A.arena, static_cast<uint64_t>(off1[perm[st - 1]]) + s.depth);
-                uint64_t kb = load_key(A.arena, static_cast<uint64_t>(off1[perm[st]]) + s.depth);
-                A.lcp[s.begin + st - 1] = s.depth + diff_bytes(ka, kb);
+                // keys at s.depth of the two neighbours are still in key1
+                // (tie handling never overwrites them) and differ
+                A.lcp[s.begin + st - 1] = s.depth + diff_bytes(key1[perm[st - 1]], key1[perm[st]]);
             }
         }
         warp_add(&es.hints, my_hints);
