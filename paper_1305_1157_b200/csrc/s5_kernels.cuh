@@ -189,6 +189,69 @@ __device__ __noinline__ void build_tree_levels(const uint64_t* sample, uint32_t 
     }
 }
 
+// The same splitters as build_tree_levels without a barrier per level: every
+// node's sample range follows from the root by its path (bits of i below the
+// top one: 0 = left, 1 = right), so each thread walks the path of its own
+// nodes, repeating the equal-sample skips by binary search (broadcast reads).
+template <uint32_t THREADS>
+__device__ __noinline__ void build_tree_paths(const uint64_t* sample, uint32_t m, uint32_t d,
+                                              uint64_t* tree) {
+    const uint32_t v = (1u << d) - 1;
+    if (threadIdx.x == 0) tree[0] = 0;
+#pragma unroll 1
+    for (uint32_t i = threadIdx.x + 1; i <= v; i += THREADS) {
+        const uint32_t l = 31 - __clz(i);
+        int32_t a = 0, b = static_cast<int32_t>(m) - 1;
+        uint32_t f = 0;
+#pragma unroll 1
+        for (int32_t sdx = static_cast<int32_t>(l) - 1; sdx >= 0; --sdx) {
+            if (a > b) break;  // empty range: the whole subtree takes the fallback
+            const int32_t mm = (a + b) >> 1;
+            const uint64_t x = sample[mm];
+            if (((i >> sdx) & 1u) == 0) {
+                int32_t lo = a, hi = mm;  // first index in [a, mm] with sample >= x
+                while (lo < hi) {
+                    int32_t mid = (lo + hi) >> 1;
+                    if (sample[mid] < x) lo = mid + 1; else hi = mid;
+                }
+                b = lo - 1;
+            } else {
+                int32_t lo = mm + 1, hi = b + 1;  // first index in (mm, b] with sample > x
+                while (lo < hi) {
+                    int32_t mid = (lo + hi) >> 1;
+                    if (sample[mid] <= x) lo = mid + 1; else hi = mid;
+                }
+                a = lo;
+            }
+            f = static_cast<uint32_t>(mm);
+        }
+        tree[i] = a > b ? sample[f] : sample[(a + b) >> 1];
+    }
+    __syncthreads();
+}
+
+// Ascending sort of s[0..m) by rank counting (each key's position = number
+// of smaller keys, ties by index; all threads read the same key at a time,
+// a shared-memory broadcast): O(m^2 / THREADS) work, two barriers.  For the
+// small samples of k_local (m <= maxn/2).
+template <uint32_t THREADS>
+__device__ __noinline__ void sort_sample_rank(uint64_t* s, uint64_t* tmp, uint32_t m) {
+#pragma unroll 1
+    for (uint32_t i = threadIdx.x; i < m; i += THREADS) {
+        const uint64_t x = s[i];
+        uint32_t r = 0;
+#pragma unroll 4
+        for (uint32_t j = 0; j < m; ++j) {
+            const uint64_t y = s[j];
+            r += (y < x) || (y == x && j < i);
+        }
+        tmp[r] = x;
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < m; i += THREADS) s[i] = tmp[i];
+    __syncthreads();
+}
+
 // Exclusive scan of h[0..k) in place, h[k] = total.  All threads call.
 template <uint32_t THREADS>
 __device__ __noinline__ void block_exclusive_scan(uint32_t* h, uint32_t k, uint32_t* warp_sums) {
@@ -858,8 +921,8 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         sample[t] = x;
     }
     __syncthreads();
-    sort_sample<THREADS>(sample, M);
-    build_tree_levels<THREADS>(sample, m, d, tree, na, nb, nf);
+    sort_sample_rank<THREADS>(sample, sample + M, m);
+    build_tree_paths<THREADS>(sample, m, d, tree);
     for (uint32_t b = threadIdx.x; b <= k; b += THREADS) hist[b] = 0;
     __syncthreads();
 
