@@ -921,7 +921,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         sample[t] = x;
     }
     __syncthreads();
-    sort_sample_rank<THREADS>(sample, sample + M, m);
+    sort_sample<THREADS>(sample, M);
     build_tree_paths<THREADS>(sample, m, d, tree);
     for (uint32_t b = threadIdx.x; b <= k; b += THREADS) hist[b] = 0;
     __syncthreads();
