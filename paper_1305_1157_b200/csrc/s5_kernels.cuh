@@ -707,25 +707,39 @@ __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uin
     const bool pair_valid = lane + 1 < g;
     uint32_t e = valid ? perm[gs + lane] : 0u;
     uint32_t run = valid ? 0u : 0xFFFFFFFFu;
-    uint64_t k = ~0ull;
+    uint64_t k0 = ~0ull, k1 = ~0ull;
     bool resolved = false, active = valid;
-    for (;;) {
-        depth += 8;
+    depth += 8;  // the group's keys are equal at depth: start one word deeper
+    for (;; depth += 16) {  // 16 string bytes per round
         if (active) {
-            k = load_key(A.arena, static_cast<uint64_t>(off1[e]) + depth);
+            load_key2(A.arena, static_cast<uint64_t>(off1[e]) + depth, k0, k1);
             ++fetches;
         }
-        warp_bitonic<false>(run, k, e, lane);
-        uint64_t nk = __shfl_down_sync(0xffffffffu, k, 1);
+        // bitonic sort of (run, k0, k1), payload e
+#pragma unroll 1
+        for (uint32_t K = 2; K <= 32; K <<= 1) {
+#pragma unroll 1
+            for (uint32_t J = K >> 1; J > 0; J >>= 1) {
+                uint32_t orun = __shfl_xor_sync(0xffffffffu, run, J);
+                uint64_t o0 = __shfl_xor_sync(0xffffffffu, k0, J);
+                uint64_t o1 = __shfl_xor_sync(0xffffffffu, k1, J);
+                uint32_t oe = __shfl_xor_sync(0xffffffffu, e, J);
+                bool olt = orun < run || (orun == run && (o0 < k0 || (o0 == k0 && o1 < k1)));
+                bool mlt = run < orun || (run == orun && (k0 < o0 || (k0 == o0 && k1 < o1)));
+                bool take = (((lane & J) == 0) == ((lane & K) == 0)) ? olt : mlt;
+                if (take) { run = orun; k0 = o0; k1 = o1; e = oe; }
+            }
+        }
+        uint64_t n0 = __shfl_down_sync(0xffffffffu, k0, 1);
+        uint64_t n1 = __shfl_down_sync(0xffffffffu, k1, 1);
         uint32_t nrun = __shfl_down_sync(0xffffffffu, run, 1);
         if (pair_valid && !resolved && nrun == run) {
-            if (k != nk) {
-                if (A.lcp) A.lcp[s.begin + gs + lane] = depth + diff_bytes(k, nk);
-                resolved = true;
-            } else if (has_zero_byte(k)) {
-                if (A.lcp) A.lcp[s.begin + gs + lane] = depth + zero_index(k);
-                resolved = true;
-            }
+            uint64_t l = 0;
+            if (k0 != n0) { l = depth + diff_bytes(k0, n0); resolved = true; }
+            else if (has_zero_byte(k0)) { l = depth + zero_index(k0); resolved = true; }
+            else if (k1 != n1) { l = depth + 8 + diff_bytes(k1, n1); resolved = true; }
+            else if (has_zero_byte(k1)) { l = depth + 8 + zero_index(k1); resolved = true; }
+            if (resolved && A.lcp) A.lcp[s.begin + gs + lane] = l;
         }
         uint32_t unres = __ballot_sync(0xffffffffu, pair_valid && !resolved);
         if (!unres) break;
@@ -900,7 +914,9 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         } else {
             L = diff_bytes(mn, mx);
         }
-        if (L < 4 || (A.flags & 4)) break;
+        // default: skip whole equal words only; flags bit3 also skips a partial
+        // common prefix of >= 4 bytes; bit2 disables the skip
+        if ((A.flags & 4) || L < ((A.flags & 8) ? 4u : 8u)) break;
         s.depth += L;
 #pragma unroll
         for (uint32_t j = 0; j < ITEMS; ++j) {
