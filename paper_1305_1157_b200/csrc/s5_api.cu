@@ -53,6 +53,8 @@ constexpr uint32_t kLocalThreads = 512, kLocalItems = 8;
 using LocalCfg = LocalSmem<kLocalThreads, kLocalItems>;
 constexpr uint32_t kLocalSThreads = 128, kLocalSItems = 8;
 using LocalSCfg = LocalSmem<kLocalSThreads, kLocalSItems>;
+constexpr uint32_t kLocalMThreads = 256, kLocalMItems = 8;
+using LocalMCfg = LocalSmem<kLocalMThreads, kLocalMItems>;
 
 int resolve(const s5_config* c, Cfg* o) {
     o->v = c && c->v ? c->v : 8191;
@@ -106,7 +108,8 @@ Layout make_layout(uint64_t n, const Cfg& c) {
     };
     L.cap[SMALL] = static_cast<uint32_t>(n / 2 + 1);
     L.cap[LOCAL_S] = static_cast<uint32_t>(n / (c.small_max + 1) + 1);
-    L.cap[LOCAL] = static_cast<uint32_t>(n / (std::min(c.local_max, LocalSCfg::maxn) + 1) + 1);
+    L.cap[LOCAL_M] = static_cast<uint32_t>(n / (std::min(c.local_max, LocalSCfg::maxn) + 1) + 1);
+    L.cap[LOCAL] = static_cast<uint32_t>(n / (std::min(c.local_max, LocalMCfg::maxn) + 1) + 1);
     L.cap[NARROW] = static_cast<uint32_t>(n / (c.local_max + 1) + 1);
     L.cap[WIDE] = static_cast<uint32_t>(n / (c.narrow_max + 1) + 1);
     for (int s = 0; s < 2; ++s) L.off[s] = take(n * 4);
@@ -156,6 +159,8 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_local<kLocalThreads, kLocalItems, true>, LocalCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalSThreads, kLocalSItems, false>, LocalSCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalSThreads, kLocalSItems, true>, LocalSCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalMThreads, kLocalMItems, false>, LocalMCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalMThreads, kLocalMItems, true>, LocalMCfg::total);
     });
     return rc;
 }
@@ -295,6 +300,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.small_max = c.small_max;
     A.local_max = c.local_max;
     A.local_s_max = std::min(c.local_max, LocalSCfg::maxn);
+    A.local_m_max = std::min(c.local_max, LocalMCfg::maxn);
     A.wide_dcap = c.wide_dcap;
     A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max / 2);
     A.narrow_max = c.narrow_max;
@@ -372,8 +378,8 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             stats->wide_elems[level] = h.elems[WIDE];
             stats->narrow_elems[level] = h.elems[NARROW];
             stats->small_elems[level] = h.elems[SMALL];
-            stats->local_elems[level] = h.elems[LOCAL] + h.elems[LOCAL_S];
-            stats->local_steps += m[LOCAL] + m[LOCAL_S];
+            stats->local_elems[level] = h.elems[LOCAL] + h.elems[LOCAL_S] + h.elems[LOCAL_M];
+            stats->local_steps += m[LOCAL] + m[LOCAL_S] + m[LOCAL_M];
             stats->n_per_pass[level] = live_elems;
             stats->wide_steps += m[WIDE];
             stats->narrow_steps += m[NARROW];
@@ -432,6 +438,16 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             else
                 k_local<kLocalSThreads, kLocalSItems, false>
                     <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, st>>>(A, segs[LOCAL_S]);
+            prof.end();
+        }
+        if (m[LOCAL_M]) {
+            prof.begin(S5_K_LOCAL_M, h.elems[LOCAL_M]);
+            if (c.classifier)
+                k_local<kLocalMThreads, kLocalMItems, true>
+                    <<<m[LOCAL_M], kLocalMThreads, LocalMCfg::total, st>>>(A, segs[LOCAL_M]);
+            else
+                k_local<kLocalMThreads, kLocalMItems, false>
+                    <<<m[LOCAL_M], kLocalMThreads, LocalMCfg::total, st>>>(A, segs[LOCAL_M]);
             prof.end();
         }
         if (m[LOCAL]) {

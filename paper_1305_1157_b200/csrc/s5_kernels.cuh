@@ -26,11 +26,13 @@ struct Seg {
     uint32_t begin, size, depth, side;
 };
 
+constexpr int NCLS_MAX = 6;
+
 // Device control block: next-level list counters, error bits, statistics.
 struct Ctl {
-    uint32_t n_list[5];  // next-level wide, narrow, small, local, local_s segment counts
+    uint32_t n_list[NCLS_MAX];  // next-level segment counts per size class
     uint32_t err;        // bit0 handle range, bit1 list overflow, bit2 pool overflow
-    unsigned long long elems[5];  // strings in next-level lists, per class
+    unsigned long long elems[NCLS_MAX];  // strings in next-level lists, per class
     unsigned long long fetches;   // arena key gathers
     unsigned long long hints;     // boundary LCP hints appended to the hint list
     uint32_t wide_ctas;           // plan: CTAs of the current wide launch
@@ -39,7 +41,7 @@ struct Ctl {
 };
 
 enum : uint32_t { ERR_RANGE = 1, ERR_LIST = 2, ERR_POOL = 4 };
-enum : int { WIDE = 0, NARROW = 1, SMALL = 2, LOCAL = 3, LOCAL_S = 4, NCLS = 5 };
+enum : int { WIDE = 0, NARROW = 1, SMALL = 2, LOCAL = 3, LOCAL_S = 4, LOCAL_M = 5, NCLS = 6 };
 
 struct SortArgs {
     const uint8_t* arena;
@@ -52,7 +54,7 @@ struct SortArgs {
     Seg* next[NCLS];
     uint32_t cap[NCLS];
     Ctl* ctl;
-    uint32_t small_max, local_s_max, local_max, narrow_max;
+    uint32_t small_max, local_s_max, local_m_max, local_max, narrow_max;
     uint32_t dmax;         // log2(cfg.v + 1)
     uint32_t wide_dcap;    // wide steps use d <= wide_dcap (<= kWideDMax)
     uint32_t wide_target;  // wide steps aim at children of about this size
@@ -96,6 +98,7 @@ __host__ __device__ __forceinline__ uint32_t wide_ctas(uint32_t size) {
 __device__ __forceinline__ int size_class(const SortArgs& A, uint32_t size) {
     return size <= A.small_max     ? SMALL
          : size <= A.local_s_max   ? LOCAL_S
+         : size <= A.local_m_max   ? LOCAL_M
          : size <= A.local_max     ? LOCAL
          : size <= A.narrow_max    ? NARROW : WIDE;
 }
@@ -836,7 +839,7 @@ struct LocalSmem {
 };
 
 template <uint32_t THREADS, uint32_t ITEMS, bool EQUAL>
-__global__ void __launch_bounds__(THREADS, (THREADS >= 512 ? 2 : 8))
+__global__ void __launch_bounds__(THREADS, (THREADS >= 512 ? 2 : (THREADS >= 256 ? 4 : 8)))
 k_local(SortArgs A, const Seg* __restrict__ segs) {
     using L = LocalSmem<THREADS, ITEMS>;
     extern __shared__ __align__(16) uint8_t sm[];
