@@ -302,7 +302,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.local_s_max = std::min(c.local_max, LocalSCfg::maxn);
     A.local_m_max = std::min(c.local_max, LocalMCfg::maxn);
     A.wide_dcap = c.wide_dcap;
-    A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max / 2);
+    A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max * 3 / 8);
     A.narrow_max = c.narrow_max;
     A.dmax = c.dmax;
     A.alpha = c.alpha;

@@ -54,7 +54,7 @@ class SampleSortConfig:
     narrow_max: int = 16384
     local_max: int = 4096
     wide_v: int = 255
-    wide_target: int = 0
+    wide_target: int = 1536
     flags: int = 0
 
     def to_c(self) -> _lib.S5Config:
