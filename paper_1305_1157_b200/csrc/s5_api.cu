@@ -419,7 +419,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             k_wide_bscan<<<m[WIDE], 1024, 0, st>>>(A, P);
             prof.end();
             prof.begin(S5_K_WIDE_SCATTER, h.elems[WIDE]);
-            k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::total, st>>>(A, P);
+            k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::bytes(c.wide_dcap), st>>>(A, P);
             prof.end();
         }
         if (m[NARROW]) {

@@ -1324,22 +1324,25 @@ __global__ void __launch_bounds__(1024) k_wide_bscan(SortArgs A, WidePlan P) {
 // whole sectors) instead of one scattered 4 B + 8 B store per string.
 struct WideScatterSmem {
     static constexpr uint32_t kcap = 2u << kWideDMax;
-    static constexpr uint32_t words = 4 * kcap + 8;
-    static constexpr uint32_t total = words * 4 + kWideTile * (8 + 4 + 2) + 64 * 4;
+    static constexpr uint32_t total = (3 * kcap + 8) * 4 + kWideTile * (8 + 4 + 2) + 64 * 4;
+    // shared memory for a launch whose trees have depth <= dcap
+    __host__ __device__ static constexpr uint32_t bytes(uint32_t dcap) {
+        return (3 * (2u << dcap) + 8) * 4 + kWideTile * (8 + 4 + 2) + 64 * 4;
+    }
 };
 
 __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WidePlan P) {
     extern __shared__ __align__(16) uint8_t sm[];
-    using W = WideScatterSmem;
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;
     uint64_t* sk = reinterpret_cast<uint64_t*>(sm);
     uint32_t* so = reinterpret_cast<uint32_t*>(sk + kWideTile);
     uint16_t* sb = reinterpret_cast<uint16_t*>(so + kWideTile);
+    const uint32_t kc = 2u << A.wide_dcap;
     uint32_t* cur = reinterpret_cast<uint32_t*>(sb + kWideTile);
-    uint32_t* cnt = cur + W::kcap;
-    uint32_t* gb = cnt + W::kcap + 4;
-    uint32_t* warp_sums = gb + W::kcap + 4;
+    uint32_t* cnt = cur + kc;
+    uint32_t* gb = cnt + kc + 4;
+    uint32_t* warp_sums = gb + kc + 4;
     const uint32_t si = find_seg(P.cta_start, P.nsegs, G);
     const Seg s = P.segs[si];
     const WideGeom g = wide_geom(s, A);
