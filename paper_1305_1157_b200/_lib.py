@@ -32,7 +32,7 @@ class S5Config(C.Structure):
     _fields_ = [("v", C.c_uint32), ("alpha", C.c_uint32), ("classifier", C.c_uint32),
                 ("small_max", C.c_uint32), ("narrow_max", C.c_uint32), ("flags", C.c_uint32),
                 ("seed", C.c_uint64), ("local_max", C.c_uint32), ("wide_v", C.c_uint32),
-                ("wide_target", C.c_uint32), ("reserved", C.c_uint32)]
+                ("wide_target", C.c_uint32), ("local_target", C.c_uint32)]
 
 
 S5_MAX_LAUNCH_RECS = 512

@@ -45,7 +45,7 @@ int fail(int code, const char* fmt, ...) {
 
 struct Cfg {
     uint32_t v, alpha, classifier, small_max, local_max, narrow_max, flags, dmax, wide_dcap;
-    uint32_t wide_target;
+    uint32_t wide_target, local_target;
     uint64_t seed;
 };
 
@@ -61,7 +61,7 @@ int resolve(const s5_config* c, Cfg* o) {
     o->alpha = c && c->alpha ? c->alpha : 2;
     o->classifier = c ? c->classifier : 0;
     o->small_max = c && c->small_max ? c->small_max : 32;
-    o->narrow_max = c && c->narrow_max ? c->narrow_max : kNarrowMaxSize;
+    o->narrow_max = c && c->narrow_max ? c->narrow_max : 4096;  // narrow tier off by default
     o->local_max = c && c->local_max ? c->local_max : LocalCfg::maxn;
     uint32_t wv = c && c->wide_v ? c->wide_v : 255;
     uint32_t wd = 0;
@@ -70,6 +70,8 @@ int resolve(const s5_config* c, Cfg* o) {
         return fail(S5_E_INVALID, "wide_v must be 2**d - 1 with d <= %u, got %u", kWideDMax, wv);
     o->wide_dcap = wd;
     o->wide_target = c ? c->wide_target : 0;
+    o->local_target = c && c->local_target ? c->local_target : 8;
+    if (o->local_target > 32) return fail(S5_E_INVALID, "local_target must be <= 32");
     o->flags = c ? c->flags : 0;
     o->seed = c ? c->seed : 1;
     uint32_t d = 0;
@@ -302,6 +304,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.local_s_max = std::min(c.local_max, LocalSCfg::maxn);
     A.local_m_max = std::min(c.local_max, LocalMCfg::maxn);
     A.wide_dcap = c.wide_dcap;
+    A.local_target = c.local_target;
     A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max * 3 / 8);
     A.narrow_max = c.narrow_max;
     A.dmax = c.dmax;

@@ -58,6 +58,7 @@ struct SortArgs {
     uint32_t dmax;         // log2(cfg.v + 1)
     uint32_t wide_dcap;    // wide steps use d <= wide_dcap (<= kWideDMax)
     uint32_t wide_target;  // wide steps aim at children of about this size
+    uint32_t local_target; // one-CTA steps aim at inner buckets of about this size
     uint32_t alpha;
     uint32_t flags;        // s5_config flags (bit2: no common-prefix skip)
     uint64_t seed;
@@ -862,7 +863,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     Seg s = segs[blockIdx.x];
     __shared__ uint64_t red[2][32];
     const uint32_t dcap = A.dmax < L::dl ? A.dmax : L::dl;
-    uint32_t d = ceil_log2((s.size + 7) / 8);
+    uint32_t d = ceil_log2((s.size + A.local_target - 1) / A.local_target);
     d = d < 1 ? 1 : (d > dcap ? dcap : d);
     const uint32_t v = (1u << d) - 1, k = 2 * v + 1;
     uint32_t m = A.alpha * v;

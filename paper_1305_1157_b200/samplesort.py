@@ -51,10 +51,11 @@ class SampleSortConfig:
     interleave: int = 3
     seed: int = 1
     small_max: int = 32
-    narrow_max: int = 16384
+    narrow_max: int = 4096
     local_max: int = 4096
     wide_v: int = 255
     wide_target: int = 1536
+    local_target: int = 8
     flags: int = 0
 
     def to_c(self) -> _lib.S5Config:
@@ -63,7 +64,7 @@ class SampleSortConfig:
         return _lib.S5Config(self.v, self.alpha, 1 if self.classifier == "equal" else 0,
                              self.small_max, self.narrow_max, self.flags, self.seed,
                              self.local_max,
-                             self.wide_v, self.wide_target, 0)
+                             self.wide_v, self.wide_target, self.local_target)
 
 
 _ws_lock = threading.Lock()
