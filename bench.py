@@ -364,6 +364,8 @@ def run_ours(args):
         if i >= args.warmup:
             e2e_times.append(dt)
     e2e_s = sum(e2e_times) / len(e2e_times)
+    from paper_1305_1157_b200 import samplesort as _ss
+    e2e_phases = dict(_ss.LAST_HOST_MS)
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -398,7 +400,8 @@ def run_ours(args):
         "e2e": {"value": world * n / e2e_s, "unit": "strings/s",
                 "h2d_bytes_per_step": int(8 * n), "d2h_bytes_per_step": int(8 * n + 8 * (n - 1)),
                 "ms_per_step": 1e3 * e2e_s,
-                "note": "parallel_sample_sort(numpy handles, lcp_out=numpy): H2D + sort + D2H"},
+                "note": "parallel_sample_sort(numpy handles, lcp_out=numpy): H2D + sort + D2H",
+                "phases_ms": e2e_phases},
         "arena_upload_s": arena_upload_s,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk,

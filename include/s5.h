@@ -93,6 +93,7 @@ typedef struct {
     uint64_t kern_strings[16];           /* strings processed per kernel (S5_K_*)  */
     uint32_t n_launch_recs;              /* flags bit1: per-launch records        */
     uint32_t pad3_;
+    float host_h2d_ms, host_sort_ms, host_d2h_ms, pad4_;  /* s5_sort_host phases (wall) */
     s5_launch_rec launch_recs[S5_MAX_LAUNCH_RECS];
 } s5_stats;
 

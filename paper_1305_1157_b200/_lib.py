@@ -56,7 +56,9 @@ class S5Stats(C.Structure):
                 ("kern_ms", C.c_float * 16), ("kern_launches", C.c_uint32 * 16),
                 ("local_elems", C.c_uint64 * S5_MAX_LEVELS), ("local_steps", C.c_uint64),
                 ("kern_strings", C.c_uint64 * 16), ("n_launch_recs", C.c_uint32),
-                ("pad3_", C.c_uint32), ("launch_recs", S5LaunchRec * S5_MAX_LAUNCH_RECS)]
+                ("pad3_", C.c_uint32), ("host_h2d_ms", C.c_float), ("host_sort_ms", C.c_float),
+                ("host_d2h_ms", C.c_float), ("pad4_", C.c_float),
+                ("launch_recs", S5LaunchRec * S5_MAX_LAUNCH_RECS)]
 
     def as_dict(self) -> dict:
         L = min(self.levels, S5_MAX_LEVELS)
@@ -72,6 +74,8 @@ class S5Stats(C.Structure):
             "small_segments": int(self.small_segments), "key_fetches": int(self.key_fetches),
             "boundary_lcps": int(self.boundary_lcps), "ms_total": float(self.ms_total),
             "launches": int(self.launches),
+            "host_ms": {"h2d": float(self.host_h2d_ms), "sort": float(self.host_sort_ms),
+                        "d2h": float(self.host_d2h_ms)},
             "launch_recs": [(KERNELS[r.kernel] if r.kernel < len(KERNELS) else str(r.kernel),
                              int(r.level), int(r.strings), round(float(r.ms), 4))
                             for r in self.launch_recs[:min(self.n_launch_recs, S5_MAX_LAUNCH_RECS)]],

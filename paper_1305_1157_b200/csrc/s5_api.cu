@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstddef>
 #include <cstdarg>
 #include <cstdio>
@@ -579,6 +580,7 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
     void* dws = static_cast<char*>(H.dbuf) + 2 * align_up(n * 8);
 
     // H2D of the handles
+    auto t0 = std::chrono::steady_clock::now();
     const uint64_t bytes = n * 8;
     uint64_t i = 0;
     for (uint64_t off = 0; off < bytes; off += HostPath::kChunk, ++i) {
@@ -590,9 +592,13 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
                                 cudaMemcpyHostToDevice, st));
         S5_CUDA(cudaEventRecord(H.ev[b], st));
     }
+    S5_CUDA(cudaStreamSynchronize(st));
+    auto t1 = std::chrono::steady_clock::now();
     int rc = s5_sort(d_arena, arena_len, dh, n, depth, h_lcp ? dl : nullptr, cfg, dws, ws,
                      stream_, stats);
     if (rc) return rc;
+    S5_CUDA(cudaStreamSynchronize(st));
+    auto t2 = std::chrono::steady_clock::now();
 
     // D2H of handles then LCP, one DMA ahead of the copy-out
     struct Piece { const char* d; char* h; uint64_t len; };
@@ -624,6 +630,12 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
         par_memcpy(pieces[k].h, H.stage[b], pieces[k].len);
     }
     S5_CUDA(cudaStreamSynchronize(st));
+    auto t3 = std::chrono::steady_clock::now();
+    if (stats) {
+        stats->host_h2d_ms = std::chrono::duration<float, std::milli>(t1 - t0).count();
+        stats->host_sort_ms = std::chrono::duration<float, std::milli>(t2 - t1).count();
+        stats->host_d2h_ms = std::chrono::duration<float, std::milli>(t3 - t2).count();
+    }
     return 0;
 }
 

@@ -70,13 +70,13 @@ constexpr uint32_t kNarrowMaxSize = 16384;    // tags fit 14-bit ranks
 constexpr uint32_t kNarrowSampleCap = 8192;
 constexpr uint32_t kWideThreads = 512;
 constexpr uint32_t kWideDMax = 10;            // v <= 1023, k <= 2047
-constexpr uint32_t kWideTile = 2048;          // scatter tile staged in shared memory
+constexpr uint32_t kWideTile = 4096;          // scatter tile staged in shared memory
 constexpr uint32_t kWideSampleCap = 8192;
 constexpr uint32_t kMaxTreeD = 13;            // standalone tree / classify surfaces
 constexpr uint32_t kWideChunkMin = 16384;     // strings per CTA at least
 constexpr uint32_t kWideCtasMax = 1184;       // 8 waves of 148 SMs
 constexpr uint32_t kWideFrontier = 1u << 20;  // max C x k open bucket cursors
-constexpr int kWideItems = 8;                 // interleaved descents per thread
+constexpr int kWideItems = 4;                 // interleaved descents per thread
 
 __host__ __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) {
     uint32_t d = 0;
@@ -1332,7 +1332,7 @@ struct WideScatterSmem {
     }
 };
 
-__global__ void __launch_bounds__(kWideThreads, 3) k_wide_scatter(SortArgs A, WidePlan P) {
+__global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WidePlan P) {
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;

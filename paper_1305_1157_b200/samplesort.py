@@ -67,6 +67,9 @@ class SampleSortConfig:
                              self.wide_v, self.wide_target, self.local_target)
 
 
+#: wall-clock phases of the last host-buffer call (H2D, sort, D2H), ms
+LAST_HOST_MS: dict = {}
+
 _ws_lock = threading.Lock()
 _ws_cache: dict = {}
 
@@ -188,6 +191,9 @@ def _sort_host(arena, handles, depth, cfg, counters, lcp_out, dev):
                                      C.byref(st))
     _lib.check(rc, "s5_sort_host")
     _record(counters, st)
+    global LAST_HOST_MS
+    LAST_HOST_MS = {"h2d": float(st.host_h2d_ms), "sort": float(st.host_sort_ms),
+                    "d2h": float(st.host_d2h_ms)}
     if h is not handles:
         handles[:] = h
     if lcp_out is not None and lcp_buf is not lcp_out:
