@@ -173,6 +173,12 @@ def classify_tree_equal(keys, tree: SplitterTree, out=None):
     return _classify(keys, tree, 1, out)
 
 
+def classify_tree_lut(keys, tree: SplitterTree, out=None):
+    """Byte table over the splitters' first distinguishing byte + binary
+    search: the classifier of the multi-CTA count kernel (same buckets)."""
+    return _classify(keys, tree, 2, out)
+
+
 def bucket_layout(counts, tree: SplitterTree, parent_depth: int) -> BucketLayout:
     """Boundaries, depth gains and finished flags (classifier.py:284-304)."""
     v = tree.v

@@ -144,8 +144,10 @@ int set_smem(K kernel, int bytes) {
 }
 
 constexpr int kWideTreeSmem = 2 * kWideSampleCap * 8 + (1 << kWideDMax) * 12;
-constexpr int kWideSmem = (1 << kWideDMax) * 8 + ((2 << kWideDMax) + 2) * 4;
-inline int wide_smem(uint32_t dcap) { return (1 << dcap) * 8 + ((2 << dcap) + 2) * 4; }
+constexpr int kWideSmem = (1 << kWideDMax) * 8 + ((2 << kWideDMax) + 2) * 4 + (1 << kWideDMax) * 8 + 258 * 2 + 16;
+inline int wide_smem(uint32_t dcap) {
+    return (1 << dcap) * 8 + ((2 << dcap) + 2) * 4 + (1 << dcap) * 8 + 258 * 2 + 16;
+}
 
 int init_attributes() {
     static std::once_flag once;
@@ -677,17 +679,22 @@ int s5_classify(const uint64_t* d_keys, uint64_t n, const uint64_t* d_in_order, 
     while (d < 31 && ((1u << d) - 1) < v) ++d;
     if (v < 1 || ((1u << d) - 1) != v || d > kMaxTreeD)
         return fail(S5_E_INVALID, "need 2**d - 1 splitters (d <= %u), got %u", kMaxTreeD, v);
+    if (classifier > 2) return fail(S5_E_INVALID, "classifier must be 0, 1 or 2");
     if (!n) return 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    int smem = (1 << d) * 8;
+    int smem = (1 << d) * 8 * 2 + 258 * 2 + 16;
     if (smem > 48 * 1024) {
-        if (int rc = set_smem(k_classify<false>, smem)) return rc;
-        if (int rc = set_smem(k_classify<true>, smem)) return rc;
+        if (int rc = set_smem(k_classify<0>, smem)) return rc;
+        if (int rc = set_smem(k_classify<1>, smem)) return rc;
+        if (int rc = set_smem(k_classify<2>, smem)) return rc;
     }
-    if (classifier)
-        k_classify<true><<<grid_for(n, 256, 296), 256, smem, st>>>(d_keys, n, d_in_order, d, d_buckets);
+    const int g = grid_for(n, 256, 296);
+    if (classifier == 1)
+        k_classify<1><<<g, 256, smem, st>>>(d_keys, n, d_in_order, d, d_buckets);
+    else if (classifier == 2)
+        k_classify<2><<<g, 256, smem, st>>>(d_keys, n, d_in_order, d, d_buckets);
     else
-        k_classify<false><<<grid_for(n, 256, 296), 256, smem, st>>>(d_keys, n, d_in_order, d, d_buckets);
+        k_classify<0><<<g, 256, smem, st>>>(d_keys, n, d_in_order, d, d_buckets);
     S5_CUDA(cudaGetLastError());
     return 0;
 }

@@ -1238,6 +1238,8 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
     if (G >= A.ctl->wide_ctas) return;
     uint64_t* tree = reinterpret_cast<uint64_t*>(sm);
     uint32_t* hist = reinterpret_cast<uint32_t*>(sm + (1u << A.wide_dcap) * 8);
+    uint64_t* splitters = reinterpret_cast<uint64_t*>(hist + (2u << A.wide_dcap) + 2);
+    uint16_t* lut = reinterpret_cast<uint16_t*>(splitters + (1u << A.wide_dcap));
     const uint32_t si = find_seg(P.cta_start, P.nsegs, G);
     const Seg s = P.segs[si];
     const WideGeom g = wide_geom(s, A);
@@ -1251,6 +1253,30 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
     __syncthreads();
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
     uint16_t* __restrict__ bkt = P.bkt + s.begin;
+    if (!EQUAL) {  // byte-table classification (same buckets, fewer dependent loads)
+        const LutTree T = lut_build<kWideThreads>(tree, g.d, splitters, lut, nullptr);
+        for (uint32_t base = lo; base < hi; base += 4 * kWideThreads) {
+            uint64_t kk[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t i = base + j * kWideThreads + threadIdx.x;
+                kk[j] = i < hi ? __ldcs(key + i) : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t i = base + j * kWideThreads + threadIdx.x;
+                if (i < hi) {
+                    uint32_t b = classify_lut(kk[j], T);
+                    atomicAdd(&hist[b], 1u);
+                    bkt[i] = static_cast<uint16_t>(b);
+                }
+            }
+        }
+        __syncthreads();
+        uint32_t* row = P.hist_pool + P.hist_off[si] + static_cast<uint64_t>(c) * g.k;
+        for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) row[b] = hist[b];
+        return;
+    }
     constexpr int IW = kWideItems;
     for (uint32_t base = lo; base < hi; base += IW * kWideThreads) {
         uint64_t kk[IW];
@@ -1492,10 +1518,11 @@ __global__ void k_first_unsorted(const uint8_t* __restrict__ arena,
 
 // classify_tree_unrolled / _equal over a key batch: level order built in
 // shared memory from the in-order splitters (_fill_level_order).
-template <bool EQUAL>
-__global__ void k_classify(const uint64_t* __restrict__ keys, uint64_t n,
-                           const uint64_t* __restrict__ in_order, uint32_t d,
-                           uint16_t* __restrict__ out) {
+// MODE 0: branch-free descent, 1: equality descent, 2: byte table (k_wide_count)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_classify(const uint64_t* __restrict__ keys, uint64_t n,
+                                                  const uint64_t* __restrict__ in_order,
+                                                  uint32_t d, uint16_t* __restrict__ out) {
     extern __shared__ __align__(16) uint64_t tree[];
     const uint32_t v = (1u << d) - 1;
     for (uint32_t i = threadIdx.x + 1; i <= v; i += blockDim.x) {
@@ -1505,9 +1532,18 @@ __global__ void k_classify(const uint64_t* __restrict__ keys, uint64_t n,
     if (threadIdx.x == 0) tree[0] = 0;
     __syncthreads();
     uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    if (MODE == 2) {
+        uint64_t* s = tree + (1u << d);
+        uint16_t* lut = reinterpret_cast<uint16_t*>(s + (1u << d));
+        const LutTree T = lut_build<256>(tree, d, s, lut, nullptr);
+        for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+             i += stride)
+            out[i] = static_cast<uint16_t>(classify_lut(keys[i], T));
+        return;
+    }
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
          i += stride)
-        out[i] = static_cast<uint16_t>(classify<EQUAL>(keys[i], tree, d));
+        out[i] = static_cast<uint16_t>(classify<MODE == 1>(keys[i], tree, d));
 }
 
 // select_splitters + build_tree from a sorted sample (single CTA).

@@ -151,6 +151,7 @@ def test_classifier_and_tree_match_reference(classifier_cases):
         want = c["buckets"]
         assert np.array_equal(CL.classify_tree_unrolled(c["keys"], tree).astype(np.int64), want), name
         assert np.array_equal(CL.classify_tree_equal(c["keys"], tree).astype(np.int64), want), name
+        assert np.array_equal(CL.classify_tree_lut(c["keys"], tree).astype(np.int64), want), name
 
 
 def test_classifier_exhaustive_small_trees():
@@ -172,6 +173,7 @@ def test_classifier_exhaustive_small_trees():
                 tree = CL.build_tree(spl)
                 assert np.array_equal(CL.classify_tree_unrolled(keys, tree).astype(np.int64), want)
                 assert np.array_equal(CL.classify_tree_equal(keys, tree).astype(np.int64), want)
+                assert np.array_equal(CL.classify_tree_lut(keys, tree).astype(np.int64), want)
 
 
 @pytest.mark.parametrize("config,n", [(1, None), (2, 1 << 20), (3, 1 << 19), (4, 1 << 19),
