@@ -50,12 +50,12 @@ struct Cfg {
     uint64_t seed;
 };
 
-constexpr uint32_t kLocalThreads = 512, kLocalItems = 8;
-using LocalCfg = LocalSmem<kLocalThreads, kLocalItems>;
-constexpr uint32_t kLocalSThreads = 128, kLocalSItems = 8;
-using LocalSCfg = LocalSmem<kLocalSThreads, kLocalSItems>;
-constexpr uint32_t kLocalMThreads = 256, kLocalMItems = 8;
-using LocalMCfg = LocalSmem<kLocalMThreads, kLocalMItems>;
+constexpr uint32_t kLocalThreads = 512;   // segments of <= 4096 strings
+using LocalCfg = LocalSmem<kLocalThreads>;
+constexpr uint32_t kLocalSThreads = 128;  // <= 1024
+using LocalSCfg = LocalSmem<kLocalSThreads>;
+constexpr uint32_t kLocalMThreads = 256;  // <= 2048
+using LocalMCfg = LocalSmem<kLocalMThreads>;
 
 int resolve(const s5_config* c, Cfg* o) {
     o->v = c && c->v ? c->v : 8191;
@@ -160,12 +160,9 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_wide_count<true>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_scatter, WideScatterSmem::total);
         if (!rc) rc = set_smem(k_build_tree, 227 * 1024);
-        if (!rc) rc = set_smem(k_local<kLocalThreads, kLocalItems, false>, LocalCfg::total);
-        if (!rc) rc = set_smem(k_local<kLocalThreads, kLocalItems, true>, LocalCfg::total);
-        if (!rc) rc = set_smem(k_local<kLocalSThreads, kLocalSItems, false>, LocalSCfg::total);
-        if (!rc) rc = set_smem(k_local<kLocalSThreads, kLocalSItems, true>, LocalSCfg::total);
-        if (!rc) rc = set_smem(k_local<kLocalMThreads, kLocalMItems, false>, LocalMCfg::total);
-        if (!rc) rc = set_smem(k_local<kLocalMThreads, kLocalMItems, true>, LocalMCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalThreads>, LocalCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalSThreads>, LocalSCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalMThreads>, LocalMCfg::total);
     });
     return rc;
 }
@@ -438,32 +435,20 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         }
         if (m[LOCAL_S]) {
             prof.begin(S5_K_LOCAL_S, h.elems[LOCAL_S]);
-            if (c.classifier)
-                k_local<kLocalSThreads, kLocalSItems, true>
-                    <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, st>>>(A, segs[LOCAL_S]);
-            else
-                k_local<kLocalSThreads, kLocalSItems, false>
-                    <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, st>>>(A, segs[LOCAL_S]);
+            k_local<kLocalSThreads>
+                <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, st>>>(A, segs[LOCAL_S]);
             prof.end();
         }
         if (m[LOCAL_M]) {
             prof.begin(S5_K_LOCAL_M, h.elems[LOCAL_M]);
-            if (c.classifier)
-                k_local<kLocalMThreads, kLocalMItems, true>
-                    <<<m[LOCAL_M], kLocalMThreads, LocalMCfg::total, st>>>(A, segs[LOCAL_M]);
-            else
-                k_local<kLocalMThreads, kLocalMItems, false>
-                    <<<m[LOCAL_M], kLocalMThreads, LocalMCfg::total, st>>>(A, segs[LOCAL_M]);
+            k_local<kLocalMThreads>
+                <<<m[LOCAL_M], kLocalMThreads, LocalMCfg::total, st>>>(A, segs[LOCAL_M]);
             prof.end();
         }
         if (m[LOCAL]) {
             prof.begin(S5_K_LOCAL, h.elems[LOCAL]);
-            if (c.classifier)
-                k_local<kLocalThreads, kLocalItems, true>
-                    <<<m[LOCAL], kLocalThreads, LocalCfg::total, st>>>(A, segs[LOCAL]);
-            else
-                k_local<kLocalThreads, kLocalItems, false>
-                    <<<m[LOCAL], kLocalThreads, LocalCfg::total, st>>>(A, segs[LOCAL]);
+            k_local<kLocalThreads>
+                <<<m[LOCAL], kLocalThreads, LocalCfg::total, st>>>(A, segs[LOCAL]);
             prof.end();
         }
         if (m[SMALL]) {

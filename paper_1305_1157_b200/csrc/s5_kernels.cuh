@@ -193,69 +193,6 @@ __device__ __noinline__ void build_tree_levels(const uint64_t* sample, uint32_t 
     }
 }
 
-// The same splitters as build_tree_levels without a barrier per level: every
-// node's sample range follows from the root by its path (bits of i below the
-// top one: 0 = left, 1 = right), so each thread walks the path of its own
-// nodes, repeating the equal-sample skips by binary search (broadcast reads).
-template <uint32_t THREADS>
-__device__ __noinline__ void build_tree_paths(const uint64_t* sample, uint32_t m, uint32_t d,
-                                              uint64_t* tree) {
-    const uint32_t v = (1u << d) - 1;
-    if (threadIdx.x == 0) tree[0] = 0;
-#pragma unroll 1
-    for (uint32_t i = threadIdx.x + 1; i <= v; i += THREADS) {
-        const uint32_t l = 31 - __clz(i);
-        int32_t a = 0, b = static_cast<int32_t>(m) - 1;
-        uint32_t f = 0;
-#pragma unroll 1
-        for (int32_t sdx = static_cast<int32_t>(l) - 1; sdx >= 0; --sdx) {
-            if (a > b) break;  // empty range: the whole subtree takes the fallback
-            const int32_t mm = (a + b) >> 1;
-            const uint64_t x = sample[mm];
-            if (((i >> sdx) & 1u) == 0) {
-                int32_t lo = a, hi = mm;  // first index in [a, mm] with sample >= x
-                while (lo < hi) {
-                    int32_t mid = (lo + hi) >> 1;
-                    if (sample[mid] < x) lo = mid + 1; else hi = mid;
-                }
-                b = lo - 1;
-            } else {
-                int32_t lo = mm + 1, hi = b + 1;  // first index in (mm, b] with sample > x
-                while (lo < hi) {
-                    int32_t mid = (lo + hi) >> 1;
-                    if (sample[mid] <= x) lo = mid + 1; else hi = mid;
-                }
-                a = lo;
-            }
-            f = static_cast<uint32_t>(mm);
-        }
-        tree[i] = a > b ? sample[f] : sample[(a + b) >> 1];
-    }
-    __syncthreads();
-}
-
-// Ascending sort of s[0..m) by rank counting (each key's position = number
-// of smaller keys, ties by index; all threads read the same key at a time,
-// a shared-memory broadcast): O(m^2 / THREADS) work, two barriers.  For the
-// small samples of k_local (m <= maxn/2).
-template <uint32_t THREADS>
-__device__ __noinline__ void sort_sample_rank(uint64_t* s, uint64_t* tmp, uint32_t m) {
-#pragma unroll 1
-    for (uint32_t i = threadIdx.x; i < m; i += THREADS) {
-        const uint64_t x = s[i];
-        uint32_t r = 0;
-#pragma unroll 4
-        for (uint32_t j = 0; j < m; ++j) {
-            const uint64_t y = s[j];
-            r += (y < x) || (y == x && j < i);
-        }
-        tmp[r] = x;
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < m; i += THREADS) s[i] = tmp[i];
-    __syncthreads();
-}
-
 // Exclusive scan of h[0..k) in place, h[k] = total.  All threads call.
 template <uint32_t THREADS>
 __device__ __noinline__ void block_exclusive_scan(uint32_t* h, uint32_t k, uint32_t* warp_sums) {
@@ -603,35 +540,18 @@ __global__ void __launch_bounds__(256) k_small(SortArgs A, const Seg* __restrict
 }
 
 // ---------------------------------------------------------------------------
-// local tier: one CTA finishes a segment of <= THREADS*ITEMS strings.  The
-// strings stay in registers while the CTA samples, builds its splitter tree
-// and classifies them; the bucketed copy goes to shared memory, and every
-// bucket of <= small_max strings is finished right there by a rank sort on
-// the cached keys with refills (the base case) and written to its final slots
-// with its LCPs.  Only larger buckets leave as children.  Fuses a sequential
-// S^5 step (samplesort.py:213-238) with the base case that follows it
-// (basesort.py:123-173).
-
-// Ascending bitonic sort of 64 keys held two per lane (positions lane and
-// lane+32) of one warp, in registers.
-__device__ __forceinline__ void warp_sort64(uint64_t& a, uint64_t& b, uint32_t lane) {
-#pragma unroll
-    for (uint32_t K = 2; K <= 64; K <<= 1) {
-#pragma unroll
-        for (uint32_t J = K >> 1; J > 0; J >>= 1) {
-            if (J == 32) {
-                if (b < a) { uint64_t t = a; a = b; b = t; }
-            } else {
-                uint64_t oa = __shfl_xor_sync(0xffffffffu, a, J);
-                uint64_t ob = __shfl_xor_sync(0xffffffffu, b, J);
-                bool lower = (lane & J) == 0;
-                bool upa = (lane & K) == 0, upb = ((lane + 32) & K) == 0;
-                a = (lower == upa) ? (oa < a ? oa : a) : (oa > a ? oa : a);
-                b = (lower == upb) ? (ob < b ? ob : b) : (ob > b ? ob : b);
-            }
-        }
-    }
-}
+// local tier: one CTA finishes a segment of <= THREADS*8 strings.  Instead of
+// another sample/classify/distribute round, the CTA sorts the whole segment
+// by its cached keys with a register bitonic network: the key bytes after the
+// segment's common prefix and the string's slot (12 bits) are packed into one
+// u64, so every compare-exchange is a plain integer min/max.  Runs of equal
+// keys are the reference's equality buckets (classifier.py:297-303): identical
+// terminated strings finish, two-string runs take one direct walk, runs of
+// <= small_max strings one warp, longer runs leave as children at depth + 8.
+// Every LCP of the segment is produced here (adjacent keys of different runs
+// differ at the segment depth), so the local tier emits no k_lcp_fix hints.
+// Replaces the sequential S^5 step + base case (samplesort.py:213-238,
+// basesort.py:123-173) for segments that fit one CTA.
 
 // Stages J = jtop..1 of a bitonic merge with block size K on the 64 entries
 // at positions base + lane (a) and base + 32 + lane (b) of one warp, in
@@ -688,32 +608,86 @@ __device__ __noinline__ void sort_sample(uint64_t* s, uint32_t M) {
     }
 }
 
-// A tie of exactly two equal keys at sorted positions q, q+1 (its neighbours
-// inside the bucket hold other keys): finish it with a direct walk over both
-// strings instead of further CTA-wide refill rounds -- the common case for
-// duplicates (config 4 reads, 13 refills each).
-__device__ __forceinline__ bool lone_tie(const uint64_t* key1, const uint16_t* perm, uint32_t q,
-                                         uint32_t bs, uint32_t be, uint64_t k) {
-    return (q == bs || key1[perm[q - 1]] != k) && (q + 2 >= be || key1[perm[q + 2]] != k);
+// Shared-memory slot of sort position e: the low four bits are XORed with
+// bits 3..6, which makes both access patterns of block_sort8 -- eight
+// consecutive positions per thread, and consecutive positions per lane --
+// free of bank conflicts.
+__device__ __forceinline__ uint32_t swz(uint32_t e) { return e ^ ((e >> 3) & 15u); }
+
+// in-thread bitonic stage with partner distance JJ < 8
+template <uint32_t JJ>
+__device__ __forceinline__ void bitonic_thread_stage(uint64_t (&w)[8], uint32_t t, uint32_t K) {
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) {
+        if (j & JJ) continue;
+        const bool asc = (((t << 3) | j) & K) == 0;
+        const uint64_t a = w[j], b = w[j | JJ];
+        const bool x = (a > b) == asc;
+        w[j] = x ? b : a;
+        w[j | JJ] = x ? a : b;
+    }
 }
 
-// A tie group of g <= 32 equal unterminated keys at sorted positions
-// gs..gs+g-1 of an owned bucket, finished by one warp: the k_small loop on
-// (run, key) starting one word deeper; writes its pair LCPs and its order.
+// Ascending sort of THREADS*8 distinct u64 held eight per thread (thread t
+// holds positions 8t..8t+7): partner distances < 8 inside a thread, < 256
+// across lanes by shuffles, wider ones through shared memory `sb`.
+template <uint32_t THREADS>
+__device__ __forceinline__ void block_sort8(uint64_t (&w)[8], uint64_t* sb) {
+    constexpr uint32_t N = THREADS * 8;
+    const uint32_t t = threadIdx.x, lane = t & 31;
+#pragma unroll 1
+    for (uint32_t K = 2; K <= N; K <<= 1) {
+        uint32_t J = K >> 1;
+        if (J >= 256) {
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) sb[swz(t * 8 + j)] = w[j];
+            __syncthreads();
+#pragma unroll 1
+            for (; J >= 256; J >>= 1) {
+#pragma unroll 1
+                for (uint32_t i = t; i < N / 2; i += THREADS) {
+                    const uint32_t lo = ((i & ~(J - 1)) << 1) | (i & (J - 1));
+                    const uint32_t a = swz(lo), b = swz(lo + J);
+                    const uint64_t x = sb[a], y = sb[b];
+                    if ((x > y) == ((lo & K) == 0)) { sb[a] = y; sb[b] = x; }
+                }
+                __syncthreads();
+            }
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) w[j] = sb[swz(t * 8 + j)];
+        }
+        const bool asc = ((t << 3) & K) == 0;
+#pragma unroll 1
+        for (; J >= 8; J >>= 1) {
+            const uint32_t m = J >> 3;
+            const bool keep_min = ((lane & m) == 0) == asc;
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                const uint64_t o = __shfl_xor_sync(0xffffffffu, w[j], m);
+                if ((o < w[j]) == keep_min) w[j] = o;
+            }
+        }
+        if (J >= 4) bitonic_thread_stage<4>(w, t, K);
+        if (J >= 2) bitonic_thread_stage<2>(w, t, K);
+        bitonic_thread_stage<1>(w, t, K);
+    }
+}
+
+// A run of g <= 32 strings at sorted positions gs..gs+g-1 whose keys agree
+// below `depth`, finished by one warp: bitonic sort of (run, 16 string
+// bytes) with refills 16 bytes deeper while pairs stay unresolved (the mkqs
+// equal-partition refill, basesort.py:146-150, as warp rounds); writes the
+// pair LCPs, the order and the final handles.
 __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uint32_t gs,
-                                            const uint32_t* off1, uint16_t* perm,
-                                            const uint8_t* res, uint64_t depth, uint32_t lane,
+                                            uint32_t g, const uint32_t* off1, uint16_t* perm,
+                                            uint64_t depth, uint32_t lane,
                                             unsigned long long& fetches) {
-    uint32_t ge = gs;
-    while (res[ge] == 2) ++ge;
-    const uint32_t g = ge - gs + 1;
     const bool valid = lane < g;
     const bool pair_valid = lane + 1 < g;
     uint32_t e = valid ? perm[gs + lane] : 0u;
     uint32_t run = valid ? 0u : 0xFFFFFFFFu;
     uint64_t k0 = ~0ull, k1 = ~0ull;
     bool resolved = false, active = valid;
-    depth += 8;  // the group's keys are equal at depth: start one word deeper
     for (;; depth += 16) {  // 16 string bytes per round
         if (active) {
             load_key2(A.arena, static_cast<uint64_t>(off1[e]) + depth, k0, k1);
@@ -753,7 +727,10 @@ __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uin
         active = ((unres >> lane) & 1u) || prev_unres;
         if (valid) run = 31u - __clz(le);
     }
-    if (valid) perm[gs + lane] = static_cast<uint16_t>(e);
+    if (valid) {
+        perm[gs + lane] = static_cast<uint16_t>(e);
+        A.out[s.begin + gs + lane] = off1[e];
+    }
 }
 
 // strings.py:64-74 (_compare_from) + :56-61 (_lcp_pair) in one walk from a
@@ -781,20 +758,6 @@ __device__ __noinline__ int walk_compare(const uint8_t* __restrict__ arena, uint
     }
 }
 
-__device__ __forceinline__ void resolve_pair(const SortArgs& A, const Seg& s,
-                                             const uint64_t* key1, const uint32_t* off1,
-                                             uint16_t* perm, uint32_t q, uint64_t depth,
-                                             unsigned long long& fetches) {
-    const uint16_t pa = perm[q], pb = perm[q + 1];
-    uint64_t l;
-    int c = walk_compare(A.arena, off1[pa], off1[pb], depth, &l, fetches);
-    if (c > 0) {
-        perm[q] = pb;
-        perm[q + 1] = pa;
-    }
-    if (A.lcp) A.lcp[s.begin + q] = l;
-}
-
 // block-wide min and max of one u64 per thread (all threads call)
 template <uint32_t THREADS>
 __device__ __forceinline__ void block_minmax(uint64_t& mn, uint64_t& mx, uint64_t (*red)[32]) {
@@ -816,94 +779,83 @@ __device__ __forceinline__ void block_minmax(uint64_t& mn, uint64_t& mx, uint64_
     __syncthreads();
 }
 
-// bucket b of a k_local step left the CTA as a child segment
-__device__ __forceinline__ bool local_child(const SortArgs& A, const uint32_t* starts,
-                                            const uint64_t* tree, uint32_t d, uint32_t b) {
-    uint32_t cnt = starts[b + 1] - starts[b];
-    if (cnt <= A.small_max) return false;
-    return !((b & 1) && has_zero_byte(tree[node_of_rank(b >> 1, d)]));
+// run boundaries: bit p of the bitmap marks the first position of a run
+__device__ __forceinline__ uint32_t run_end(const uint32_t* bits, uint32_t p) {
+    uint32_t q = p + 1, wi = q >> 5;
+    uint32_t b = bits[wi] & (~0u << (q & 31));
+    while (!b) b = bits[++wi];
+    return wi * 32 + __ffs(b) - 1;
 }
 
-template <uint32_t THREADS, uint32_t ITEMS>
+__device__ __forceinline__ uint32_t run_begin(const uint32_t* bits, uint32_t p) {
+    uint32_t wi = p >> 5;
+    uint32_t b = bits[wi] & ((2u << (p & 31)) - 1u);
+    while (!b) b = bits[--wi];
+    return wi * 32 + 31 - __clz(b);
+}
+
+template <uint32_t THREADS>
 struct LocalSmem {
-    static constexpr uint32_t maxn = THREADS * ITEMS;
-    static constexpr uint32_t dl = 31 - __builtin_clz(maxn / 8);  // v+1 <= maxn/8
-    static constexpr uint32_t key_bytes = maxn * 8;                 // key1 | sample + tmp
-    static constexpr uint32_t off_bytes = maxn * 4;                 // off1 | tree scratch
-    static constexpr uint32_t u16_bytes = maxn * 2;                 // bpos, perm, perm2
-    static constexpr uint32_t u8_bytes = maxn;                      // own, res
-    static constexpr uint32_t tree_bytes = (1u << dl) * 8;
-    static constexpr uint32_t hist_bytes = ((2u << dl) + 4) * 4;
-    static constexpr uint32_t total = key_bytes + off_bytes + 3 * u16_bytes + 2 * u8_bytes +
-                                      tree_bytes + hist_bytes + 32 * 4;
-    static_assert((1u << dl) * 12 <= off_bytes, "tree scratch does not fit");
+    static constexpr uint32_t maxn = THREADS * 8;
+    static constexpr uint32_t total = maxn * 8      // sort buffer, later run lists
+                                    + maxn * 8      // key1: key by slot
+                                    + maxn * 4      // off1: offset by slot
+                                    + maxn * 2      // perm: sorted position -> slot
+                                    + (maxn / 32 + 1) * 4;  // run-start bitmap
 };
 
-template <uint32_t THREADS, uint32_t ITEMS, bool EQUAL>
+template <uint32_t THREADS>
 __global__ void __launch_bounds__(THREADS, (THREADS >= 512 ? 2 : (THREADS >= 256 ? 4 : 8)))
 k_local(SortArgs A, const Seg* __restrict__ segs) {
-    using L = LocalSmem<THREADS, ITEMS>;
+    using LS = LocalSmem<THREADS>;
+    constexpr uint32_t N = LS::maxn;
     extern __shared__ __align__(16) uint8_t sm[];
-    uint64_t* key1 = reinterpret_cast<uint64_t*>(sm);
-    uint64_t* sample = key1;
-    uint32_t* off1 = reinterpret_cast<uint32_t*>(sm + L::key_bytes);
-    int32_t* na = reinterpret_cast<int32_t*>(off1);
-    int32_t* nb = na + (1u << L::dl);
-    uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << L::dl));
-    uint16_t* bpos = reinterpret_cast<uint16_t*>(sm + L::key_bytes + L::off_bytes);
-    uint16_t* perm = bpos + L::maxn;
-    uint16_t* perm2 = perm + L::maxn;
-    uint8_t* own = reinterpret_cast<uint8_t*>(perm2 + L::maxn);
-    uint8_t* res = own + L::maxn;
-    uint64_t* tree = reinterpret_cast<uint64_t*>(res + L::maxn);
-    uint32_t* hist = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(tree) + L::tree_bytes);
-    uint32_t* warp_sums = hist + (L::hist_bytes / 4);
+    uint64_t* sb = reinterpret_cast<uint64_t*>(sm);
+    uint64_t* key1 = sb + N;
+    uint32_t* off1 = reinterpret_cast<uint32_t*>(key1 + N);
+    uint16_t* perm = reinterpret_cast<uint16_t*>(off1 + N);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(perm + N);
+    uint32_t* ties = reinterpret_cast<uint32_t*>(sb);   // run lists reuse the sort buffer
+    uint32_t* kids = ties + N;
     __shared__ EmitScratch es;
+    __shared__ uint64_t red[2][32];
+    __shared__ uint32_t nties, nkids;
 
     Seg s = segs[blockIdx.x];
-    __shared__ uint64_t red[2][32];
-    const uint32_t dcap = A.dmax < L::dl ? A.dmax : L::dl;
-    uint32_t d = ceil_log2((s.size + A.local_target - 1) / A.local_target);
-    d = d < 1 ? 1 : (d > dcap ? dcap : d);
-    const uint32_t v = (1u << d) - 1, k = 2 * v + 1;
-    uint32_t m = A.alpha * v;
-    if (m > L::maxn / 2) m = L::maxn / 2;
-    uint32_t M = 64;
-    while (M < m) M <<= 1;
+    const uint32_t t = threadIdx.x, lane = t & 31;
     const uint32_t* __restrict__ goff = A.off[s.side] + s.begin;
     const uint64_t* __restrict__ gkey = A.key[s.side] + s.begin;
 
-    // the segment in registers (coalesced), sample from global (L2)
-    uint64_t rk[ITEMS];
-    uint32_t ro[ITEMS];
+    // the segment in registers (coalesced)
+    uint64_t rk[8];
+    uint32_t ro[8];
 #pragma unroll
-    for (uint32_t j = 0; j < ITEMS; ++j) {
-        uint32_t i = threadIdx.x + j * THREADS;
+    for (uint32_t j = 0; j < 8; ++j) {
+        uint32_t i = t + j * THREADS;
         rk[j] = i < s.size ? gkey[i] : 0;
         ro[j] = i < s.size ? goff[i] : 0;
     }
-    // common-prefix skip: when the smallest and largest key share >= 4 bytes
-    // every string does, so the depth advances by that much in-CTA (the
-    // equality-bucket chain of long shared prefixes, classifier.py:297-303,
-    // without a level per 8 bytes); all-identical terminated keys finish here
+    // common prefix of the segment's keys; whole equal words advance the
+    // depth in-CTA (the equality-bucket chain of long shared prefixes,
+    // classifier.py:297-303, without a level per 8 bytes); all-identical
+    // terminated keys finish here
     unsigned long long fetches = 0;
-    const uint32_t seg_depth0 = s.depth;
+    uint32_t L;
     for (;;) {
         uint64_t mn = ~0ull, mx = 0;
 #pragma unroll
-        for (uint32_t j = 0; j < ITEMS; ++j) {
-            if (threadIdx.x + j * THREADS < s.size) {
+        for (uint32_t j = 0; j < 8; ++j) {
+            if (t + j * THREADS < s.size) {
                 mn = rk[j] < mn ? rk[j] : mn;
                 mx = rk[j] > mx ? rk[j] : mx;
             }
         }
         block_minmax<THREADS>(mn, mx, red);
-        uint32_t L;
         if (mn == mx) {
             if (has_zero_byte(mn)) {  // identical strings: any order, lcp = |s|
 #pragma unroll
-                for (uint32_t j = 0; j < ITEMS; ++j) {
-                    uint32_t i = threadIdx.x + j * THREADS;
+                for (uint32_t j = 0; j < 8; ++j) {
+                    uint32_t i = t + j * THREADS;
                     if (i < s.size) {
                         A.out[s.begin + i] = ro[j];
                         if (A.lcp && i + 1 < s.size) A.lcp[s.begin + i] = s.depth + zero_index(mn);
@@ -911,7 +863,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
                 }
                 for (uint32_t x = 16; x > 0; x >>= 1)
                     fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
-                if ((threadIdx.x & 31) == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
+                if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
                 return;
             }
             L = 8;
@@ -923,171 +875,126 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         if ((A.flags & 4) || L < ((A.flags & 8) ? 4u : 8u)) break;
         s.depth += L;
 #pragma unroll
-        for (uint32_t j = 0; j < ITEMS; ++j) {
-            if (threadIdx.x + j * THREADS < s.size) {
+        for (uint32_t j = 0; j < 8; ++j) {
+            if (t + j * THREADS < s.size) {
                 rk[j] = load_key(A.arena, static_cast<uint64_t>(ro[j]) + s.depth);
                 ++fetches;
             }
         }
     }
-    const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
-    for (uint32_t t = threadIdx.x; t < M; t += THREADS) {
-        uint64_t x = ~0ull;
-        if (t < m) {
-            uint32_t idx = sample_index(sseed, t, s.size);
-            x = s.depth == seg_depth0 ? gkey[idx]
-                                      : load_key(A.arena, static_cast<uint64_t>(goff[idx]) + s.depth);
-        }
-        sample[t] = x;
+    if (L > 7) L = 7;  // all keys equal (skip disabled): one run either way
+    // sort words: key bytes after the common prefix, slot in the low 12 bits.
+    // With L >= 2 the word holds the whole key (exact); with L < 2 the key's
+    // last 12 (L = 0) or 4 (L = 1) bits are dropped, so runs of equal words
+    // are only candidate ties, resolved from the segment depth
+    const bool exact = L >= 2;
+    uint64_t w[8];
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) {
+        uint32_t i = t + j * THREADS;
+        key1[i] = rk[j];
+        off1[i] = ro[j];
+        w[j] = i < s.size ? (((rk[j] << (8 * L)) & ~0xFFFull) | i) : ~0ull;
     }
-    __syncthreads();
-    sort_sample<THREADS>(sample, M);
-    build_tree_paths<THREADS>(sample, m, d, tree);
-    for (uint32_t b = threadIdx.x; b <= k; b += THREADS) hist[b] = 0;
+    block_sort8<THREADS>(w, sb);
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) sb[swz(t * 8 + j)] = w[j];
     __syncthreads();
 
-    // classify + rank (warp-aggregated shared-memory histogram)
-    const uint32_t lane = threadIdx.x & 31;
-    uint32_t rbr[ITEMS];  // bucket | rank-in-bucket << 11
-    classify_iw<EQUAL, ITEMS>(rk, tree, d, rbr);
-#pragma unroll
-    for (uint32_t j = 0; j < ITEMS; ++j) {
-        uint32_t i = threadIdx.x + j * THREADS;
-        bool act = i < s.size;
-        uint32_t b = act ? rbr[j] : 0x7FFu;
-        uint32_t peers = __match_any_sync(0xffffffffu, b);
-        uint32_t leader = __ffs(peers) - 1;
-        uint32_t r = 0;
-        if (act && lane == leader) r = atomicAdd(&hist[b], __popc(peers));
-        r = __shfl_sync(0xffffffffu, r, leader) + __popc(peers & lanemask_lt());
-        rbr[j] = b | (r << 11);
+    // runs of equal words: start bitmap (positions >= size all start runs)
+    if (t == 0) {
+        bits[N / 32] = 1u;
+        nties = 0;
+        nkids = 0;
     }
-    __syncthreads();
-    block_exclusive_scan<THREADS>(hist, k, warp_sums);
-    emit_block<THREADS, true>(A, s, hist, k, tree, d, &es);
-
-    // distribute: the bucketed copy goes to shared memory (registers -> smem),
-    // then one pass in position order sends finished buckets to their final
-    // slots and children to the other side (consecutive positions ->
-    // consecutive addresses), keeping small buckets for the base case
-#pragma unroll
-    for (uint32_t j = 0; j < ITEMS; ++j) {
-        uint32_t i = threadIdx.x + j * THREADS;
-        if (i >= s.size) continue;
-        uint32_t b = rbr[j] & 0x7FFu;
-        uint32_t p = hist[b] + (rbr[j] >> 11);
-        bpos[p] = static_cast<uint16_t>(b);
-        key1[p] = rk[j];
-        off1[p] = ro[j];
-    }
-    __syncthreads();
-    const uint32_t ns = s.side ^ 1u;
 #pragma unroll 1
-    for (uint32_t p = threadIdx.x; p < s.size; p += THREADS) {
-        const uint32_t b = bpos[p];
-        const uint32_t end = hist[b + 1], cnt = end - hist[b];
-        const uint64_t kk = key1[p];
-        const uint32_t o = off1[p];
-        const bool odd = b & 1;
-        const bool fin = cnt == 1 || (odd && has_zero_byte(kk));
-        const bool mine = !fin && cnt <= A.small_max;
-        own[p] = mine;
+    for (uint32_t p = t; p < N; p += THREADS) {
+        const uint64_t wp = sb[swz(p)];
+        const bool st = p == 0 || p >= s.size || (wp >> 12) != (sb[swz(p - 1)] >> 12);
+        const uint32_t b = __ballot_sync(0xffffffffu, st);
+        if (lane == 0) bits[p >> 5] = b;
+        if (p < s.size) perm[p] = static_cast<uint16_t>(wp & 0xFFFu);
+    }
+    __syncthreads();
+
+    // per position: finished strings go out, children to the other side,
+    // LCPs at run boundaries and inside identical runs; ties are listed
+    const uint32_t tmax = A.small_max;
+    const uint32_t ns = s.side ^ 1u;
+    const uint64_t depth = s.depth;
+#pragma unroll 1
+    for (uint32_t p = t; p < s.size; p += THREADS) {
+        const uint32_t slot = perm[p];
+        const uint64_t k = key1[slot];
+        const uint32_t o = off1[slot];
+        const uint32_t r0 = run_begin(bits, p), r1 = run_end(bits, p);
+        const uint32_t g = r1 - r0;
         const uint32_t dst = s.begin + p;
-        if (fin) {
+        if (A.lcp && p + 1 == r1 && r1 < s.size)
+            A.lcp[dst] = depth + diff_bytes(k, key1[perm[r1]]);
+        if (g == 1 || (exact && has_zero_byte(k))) {
             A.out[dst] = o;
-            if (odd && A.lcp && p + 1 < end) A.lcp[dst] = s.depth + zero_index(kk);
-            perm[p] = static_cast<uint16_t>(p);
-        } else if (!mine) {
+            if (A.lcp && p + 1 < r1) A.lcp[dst] = depth + zero_index(k);
+        } else if (g > 2 && g > tmax) {
             A.off[ns][dst] = o;
-            if (odd) {
-                A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + s.depth + 8);
+            if (exact) {
+                A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + depth + 8);
                 ++fetches;
             } else {
-                A.key[ns][dst] = kk;
+                A.key[ns][dst] = k;
             }
-        }
-    }
-    __syncthreads();
-
-    // base case: rank sort inside every owned bucket by cached key
-    for (uint32_t p = threadIdx.x; p < s.size; p += THREADS) {
-        if (!own[p]) continue;
-        const uint32_t b = bpos[p], bs = hist[b], be = hist[b + 1];
-        const uint64_t x = key1[p];
-        uint32_t r = 0;
-        for (uint32_t q = bs; q < be; ++q) {
-            uint64_t y = key1[q];
-            r += (y < x) || (y == x && q < p);
-        }
-        perm[bs + r] = static_cast<uint16_t>(p);
-    }
-    __syncthreads();
-    // resolve adjacent pairs at the segment depth:
-    //   keys differ            -> lcp = depth + equal leading bytes
-    //   keys equal, terminated -> identical strings, lcp = depth + |rest|
-    //   exactly two equal keys -> one direct string walk (resolve_pair)
-    //   >= 3 equal keys        -> a tie group, finished by one warp below
-    const uint64_t depth = s.depth;
-    __shared__ uint32_t ngroups;
-    if (threadIdx.x == 0) ngroups = 0;
-    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
-        if (!own[q]) continue;
-        const uint32_t b = bpos[q], bs = hist[b], be = hist[b + 1];
-        uint8_t rv = 1;
-        if (q + 1 < be) {
-            uint64_t ka = key1[perm[q]], kb = key1[perm[q + 1]];
-            if (ka != kb) {
-                if (A.lcp) A.lcp[s.begin + q] = depth + diff_bytes(ka, kb);
-            } else if (has_zero_byte(ka)) {
-                if (A.lcp) A.lcp[s.begin + q] = depth + zero_index(ka);
-            } else if (lone_tie(key1, perm, q, bs, be, ka)) {
-                resolve_pair(A, s, key1, off1, perm, q, depth + 8, fetches);
+            if (p == r0) kids[atomicAdd(&nkids, 1u)] = r0 | (g << 13);
+        } else if (p == r0) {
+            if (g == 2) {
+                const uint32_t sa = perm[p], sb2 = perm[p + 1];
+                uint64_t l;
+                const int c = walk_compare(A.arena, off1[sa], off1[sb2], exact ? depth + 8 : depth,
+                                           &l, fetches);
+                if (A.lcp) A.lcp[dst] = l;
+                A.out[dst] = off1[c > 0 ? sb2 : sa];
+                A.out[dst + 1] = off1[c > 0 ? sa : sb2];
             } else {
-                rv = 2;
+                ties[atomicAdd(&nties, 1u)] = r0 | (g << 13);
             }
         }
-        res[q] = rv;
     }
     __syncthreads();
-    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS) {
-        if (own[q] && res[q] == 2 && (q == hist[bpos[q]] || res[q - 1] != 2))
-            perm2[atomicAdd(&ngroups, 1u)] = static_cast<uint16_t>(q);
+    // runs of 3..small_max strings: one warp each
+    const uint32_t nt = nties, nk = nkids;
+    for (uint32_t q = t >> 5; q < nt; q += THREADS / 32) {
+        const uint32_t x = ties[q];
+        tie_group_warp(A, s, x & 0x1FFFu, x >> 13, off1, perm, exact ? depth + 8 : depth, lane,
+                       fetches);
     }
-    __syncthreads();
-    // one warp per tie group (<= small_max strings): bitonic sort of
-    // (run, key) with refills at depth+8, pair LCPs emitted when resolved
-    // (the mkqs equal-partition refill, basesort.py:146-150, without
-    // CTA-wide rounds)
-    for (uint32_t g = threadIdx.x >> 5; g < ngroups; g += THREADS / 32)
-        tie_group_warp(A, s, perm2[g], off1, perm, res, depth, lane, fetches);
-    __syncthreads();
-    for (uint32_t q = threadIdx.x; q < s.size; q += THREADS)
-        if (own[q]) A.out[s.begin + q] = off1[perm[q]];
-
-    // LCPs at bucket boundaries: exact when both neighbours were finished in
-    // this CTA (their keys at s.depth differ); otherwise a hint for k_lcp_fix
-    if (A.lcp) {
-        if (threadIdx.x == 0) es.hints = 0;
+    // children: one list reservation per size class per CTA
+    if (nk) {
+        if (t < NCLS) {
+            es.cnt[t] = 0;
+            es.elems[t] = 0;
+        }
         __syncthreads();
-        uint32_t my_hints = 0;
-        for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
-            uint32_t st = hist[b];
-            if (st == 0 || hist[b + 1] == st) continue;
-            if (local_child(A, hist, tree, d, b) || local_child(A, hist, tree, d, bpos[st - 1])) {
-                ++my_hints;
-            } else {
-                // keys at s.depth of the two neighbours are still in key1
-                // (tie handling never overwrites them) and differ
-                A.lcp[s.begin + st - 1] = s.depth + diff_bytes(key1[perm[st - 1]], key1[perm[st]]);
-            }
+        for (uint32_t q = t; q < nk; q += THREADS) {
+            const uint32_t g = kids[q] >> 13;
+            const int cls = size_class(A, g);
+            atomicAdd(&es.cnt[cls], 1u);
+            atomicAdd(&es.elems[cls], g);
         }
-        warp_add(&es.hints, my_hints);
-        reserve_hints(A, &es);
-        for (uint32_t b = threadIdx.x; b < k; b += THREADS) {
-            uint32_t st = hist[b];
-            if (st == 0 || hist[b + 1] == st) continue;
-            if (local_child(A, hist, tree, d, b) || local_child(A, hist, tree, d, bpos[st - 1]))
-                push_hint(A, &es, s.begin + st - 1, s.depth);
+        __syncthreads();
+        if (t < NCLS) {
+            const uint32_t c = es.cnt[t];
+            es.base[t] = c ? atomicAdd(&A.ctl->n_list[t], c) : 0;
+            if (c && es.base[t] + c > A.cap[t]) atomicOr(&A.ctl->err, ERR_LIST);
+            if (es.elems[t])
+                atomicAdd(&A.ctl->elems[t], static_cast<unsigned long long>(es.elems[t]));
+            es.cnt[t] = 0;
+        }
+        __syncthreads();
+        const uint32_t cdepth = static_cast<uint32_t>(exact ? depth + 8 : depth);
+        for (uint32_t q = t; q < nk; q += THREADS) {
+            const uint32_t r0 = kids[q] & 0x1FFFu, g = kids[q] >> 13;
+            const int cls = size_class(A, g);
+            const uint32_t at = es.base[cls] + atomicAdd(&es.cnt[cls], 1u);
+            if (at < A.cap[cls]) A.next[cls][at] = Seg{s.begin + r0, g, cdepth, ns};
         }
     }
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);

@@ -35,6 +35,8 @@ def sass_samples(rep, kregex, skip):
             return 0
     recs = []
     for r in rows[hdr + 1:]:
+        if r and r[0] == "Kernel Name":  # the page may repeat the table
+            break
         if len(r) <= si:
             continue
         recs.append((num(r[si]), {c: num(r[i]) if i < len(r) else 0 for i, c in cols},
