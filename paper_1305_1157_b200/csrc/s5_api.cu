@@ -52,6 +52,8 @@ struct Cfg {
 
 constexpr uint32_t kLocalThreads = 512;   // segments of <= 4096 strings
 using LocalCfg = LocalSmem<kLocalThreads>;
+constexpr uint32_t kLocalXSThreads = 64;  // <= 512
+using LocalXSCfg = LocalSmem<kLocalXSThreads>;
 constexpr uint32_t kLocalSThreads = 128;  // <= 1024
 using LocalSCfg = LocalSmem<kLocalSThreads>;
 constexpr uint32_t kLocalMThreads = 256;  // <= 2048
@@ -110,7 +112,8 @@ Layout make_layout(uint64_t n, const Cfg& c) {
         return p;
     };
     L.cap[SMALL] = static_cast<uint32_t>(n / 2 + 1);
-    L.cap[LOCAL_S] = static_cast<uint32_t>(n / (c.small_max + 1) + 1);
+    L.cap[LOCAL_XS] = static_cast<uint32_t>(n / (c.small_max + 1) + 1);
+    L.cap[LOCAL_S] = static_cast<uint32_t>(n / (std::min(c.local_max, LocalXSCfg::maxn) + 1) + 1);
     L.cap[LOCAL_M] = static_cast<uint32_t>(n / (std::min(c.local_max, LocalSCfg::maxn) + 1) + 1);
     L.cap[LOCAL] = static_cast<uint32_t>(n / (std::min(c.local_max, LocalMCfg::maxn) + 1) + 1);
     L.cap[NARROW] = static_cast<uint32_t>(n / (c.local_max + 1) + 1);
@@ -162,6 +165,7 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_build_tree, 227 * 1024);
         if (!rc) rc = set_smem(k_local<kLocalThreads>, LocalCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalSThreads>, LocalSCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalXSThreads>, LocalXSCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalMThreads>, LocalMCfg::total);
     });
     return rc;
@@ -301,6 +305,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
     A.small_max = c.small_max;
     A.local_max = c.local_max;
+    A.local_xs_max = std::min(c.local_max, LocalXSCfg::maxn);
     A.local_s_max = std::min(c.local_max, LocalSCfg::maxn);
     A.local_m_max = std::min(c.local_max, LocalMCfg::maxn);
     A.wide_dcap = c.wide_dcap;
@@ -381,8 +386,9 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             stats->wide_elems[level] = h.elems[WIDE];
             stats->narrow_elems[level] = h.elems[NARROW];
             stats->small_elems[level] = h.elems[SMALL];
-            stats->local_elems[level] = h.elems[LOCAL] + h.elems[LOCAL_S] + h.elems[LOCAL_M];
-            stats->local_steps += m[LOCAL] + m[LOCAL_S] + m[LOCAL_M];
+            stats->local_elems[level] =
+                h.elems[LOCAL] + h.elems[LOCAL_S] + h.elems[LOCAL_M] + h.elems[LOCAL_XS];
+            stats->local_steps += m[LOCAL] + m[LOCAL_S] + m[LOCAL_M] + m[LOCAL_XS];
             stats->n_per_pass[level] = live_elems;
             stats->wide_steps += m[WIDE];
             stats->narrow_steps += m[NARROW];
@@ -431,6 +437,12 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
                 k_narrow<true><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
             else
                 k_narrow<false><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
+            prof.end();
+        }
+        if (m[LOCAL_XS]) {
+            prof.begin(S5_K_LOCAL_XS, h.elems[LOCAL_XS]);
+            k_local<kLocalXSThreads>
+                <<<m[LOCAL_XS], kLocalXSThreads, LocalXSCfg::total, st>>>(A, segs[LOCAL_XS]);
             prof.end();
         }
         if (m[LOCAL_S]) {

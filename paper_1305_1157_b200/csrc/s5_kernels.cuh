@@ -26,7 +26,7 @@ struct Seg {
     uint32_t begin, size, depth, side;
 };
 
-constexpr int NCLS_MAX = 6;
+constexpr int NCLS_MAX = 8;
 
 // Device control block: next-level list counters, error bits, statistics.
 struct Ctl {
@@ -41,7 +41,8 @@ struct Ctl {
 };
 
 enum : uint32_t { ERR_RANGE = 1, ERR_LIST = 2, ERR_POOL = 4 };
-enum : int { WIDE = 0, NARROW = 1, SMALL = 2, LOCAL = 3, LOCAL_S = 4, LOCAL_M = 5, NCLS = 6 };
+enum : int { WIDE = 0, NARROW = 1, SMALL = 2, LOCAL = 3, LOCAL_S = 4, LOCAL_M = 5, LOCAL_XS = 6,
+              NCLS = 7 };
 
 struct SortArgs {
     const uint8_t* arena;
@@ -54,7 +55,7 @@ struct SortArgs {
     Seg* next[NCLS];
     uint32_t cap[NCLS];
     Ctl* ctl;
-    uint32_t small_max, local_s_max, local_m_max, local_max, narrow_max;
+    uint32_t small_max, local_xs_max, local_s_max, local_m_max, local_max, narrow_max;
     uint32_t dmax;         // log2(cfg.v + 1)
     uint32_t wide_dcap;    // wide steps use d <= wide_dcap (<= kWideDMax)
     uint32_t wide_target;  // wide steps aim at children of about this size
@@ -98,6 +99,7 @@ __host__ __device__ __forceinline__ uint32_t wide_ctas(uint32_t size) {
 
 __device__ __forceinline__ int size_class(const SortArgs& A, uint32_t size) {
     return size <= A.small_max     ? SMALL
+         : size <= A.local_xs_max  ? LOCAL_XS
          : size <= A.local_s_max   ? LOCAL_S
          : size <= A.local_m_max   ? LOCAL_M
          : size <= A.local_max     ? LOCAL
@@ -693,9 +695,14 @@ __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uin
             load_key2(A.arena, static_cast<uint64_t>(off1[e]) + depth, k0, k1);
             ++fetches;
         }
-        // bitonic sort of (run, k0, k1), payload e
+        // bitonic sort of (run, k0, k1), payload e -- skipped when every
+        // open run reads the same 16 bytes (identical strings so far)
+        const uint32_t lead = run & 31u;
+        const uint64_t l0 = __shfl_sync(0xffffffffu, k0, lead);
+        const uint64_t l1 = __shfl_sync(0xffffffffu, k1, lead);
+        const bool same = !active || (k0 == l0 && k1 == l1);
 #pragma unroll 1
-        for (uint32_t K = 2; K <= 32; K <<= 1) {
+        for (uint32_t K = __all_sync(0xffffffffu, same) ? 64u : 2u; K <= 32; K <<= 1) {
 #pragma unroll 1
             for (uint32_t J = K >> 1; J > 0; J >>= 1) {
                 uint32_t orun = __shfl_xor_sync(0xffffffffu, run, J);
@@ -801,11 +808,15 @@ struct LocalSmem {
                                     + maxn * 8      // key1: key by slot
                                     + maxn * 4      // off1: offset by slot
                                     + maxn * 2      // perm: sorted position -> slot
-                                    + (maxn / 32 + 1) * 4;  // run-start bitmap
+                                    + 2 * (maxn / 32 + 1) * 4;  // run-start bitmaps
 };
 
+// candidate runs of the truncated sort words up to this length are split by
+// the cached full keys in shared memory
+constexpr uint32_t kTruncFix = 64;
+
 template <uint32_t THREADS>
-__global__ void __launch_bounds__(THREADS, (THREADS >= 512 ? 2 : (THREADS >= 256 ? 4 : 8)))
+__global__ void __launch_bounds__(THREADS, (THREADS >= 512 ? 2 : THREADS >= 256 ? 4 : THREADS >= 128 ? 8 : 16))
 k_local(SortArgs A, const Seg* __restrict__ segs) {
     using LS = LocalSmem<THREADS>;
     constexpr uint32_t N = LS::maxn;
@@ -815,6 +826,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     uint32_t* off1 = reinterpret_cast<uint32_t*>(key1 + N);
     uint16_t* perm = reinterpret_cast<uint16_t*>(off1 + N);
     uint32_t* bits = reinterpret_cast<uint32_t*>(perm + N);
+    uint32_t* bits2 = bits + N / 32 + 1;
     uint32_t* ties = reinterpret_cast<uint32_t*>(sb);   // run lists reuse the sort buffer
     uint32_t* kids = ties + N;
     __shared__ EmitScratch es;
@@ -916,6 +928,48 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         if (p < s.size) perm[p] = static_cast<uint16_t>(wp & 0xFFFu);
     }
     __syncthreads();
+    const uint32_t* rb = bits;
+    if (!exact) {
+        // truncated words: candidate runs of <= kTruncFix strings are put in
+        // full-key order (rank by the cached keys) and split where the full
+        // keys differ, which makes them exact runs; longer candidate runs stay
+        // whole and leave as children at the same depth (their keys share
+        // >= 6 bytes, so the child's words are exact)
+        uint16_t* perm2 = reinterpret_cast<uint16_t*>(sb) + 3 * N;
+#pragma unroll 1
+        for (uint32_t p = t; p < s.size; p += THREADS) {
+            const uint32_t r0 = run_begin(bits, p), r1 = run_end(bits, p);
+            const uint32_t slot = perm[p];
+            uint32_t r = p - r0;
+            if (r1 - r0 >= 2 && r1 - r0 <= kTruncFix) {
+                const uint64_t k = key1[slot];
+                r = 0;
+#pragma unroll 1
+                for (uint32_t q = r0; q < r1; ++q) {
+                    const uint64_t y = key1[perm[q]];
+                    r += (y < k) || (y == k && q < p);
+                }
+            }
+            perm2[r0 + r] = static_cast<uint16_t>(slot);
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (uint32_t p = t; p < N; p += THREADS) {
+            bool st = true;
+            if (p < s.size) {
+                const uint32_t slot = perm2[p];
+                st = (bits[p >> 5] >> (p & 31)) & 1u;
+                if (!st && run_end(bits, p) - run_begin(bits, p) <= kTruncFix)
+                    st = key1[slot] != key1[perm2[p - 1]];
+                perm[p] = static_cast<uint16_t>(slot);
+            }
+            const uint32_t b = __ballot_sync(0xffffffffu, st);
+            if (lane == 0) bits2[p >> 5] = b;
+        }
+        if (t == 0) bits2[N / 32] = 1u;
+        __syncthreads();
+        rb = bits2;
+    }
 
     // per position: finished strings go out, children to the other side,
     // LCPs at run boundaries and inside identical runs; ties are listed
@@ -927,29 +981,29 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         const uint32_t slot = perm[p];
         const uint64_t k = key1[slot];
         const uint32_t o = off1[slot];
-        const uint32_t r0 = run_begin(bits, p), r1 = run_end(bits, p);
+        const uint32_t r0 = run_begin(rb, p), r1 = run_end(rb, p);
         const uint32_t g = r1 - r0;
+        const bool rexact = exact || g <= kTruncFix;  // keys of the run are equal
         const uint32_t dst = s.begin + p;
         if (A.lcp && p + 1 == r1 && r1 < s.size)
             A.lcp[dst] = depth + diff_bytes(k, key1[perm[r1]]);
-        if (g == 1 || (exact && has_zero_byte(k))) {
+        if (g == 1 || (rexact && has_zero_byte(k))) {
             A.out[dst] = o;
             if (A.lcp && p + 1 < r1) A.lcp[dst] = depth + zero_index(k);
         } else if (g > 2 && g > tmax) {
             A.off[ns][dst] = o;
-            if (exact) {
+            if (rexact) {
                 A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + depth + 8);
                 ++fetches;
             } else {
                 A.key[ns][dst] = k;
             }
-            if (p == r0) kids[atomicAdd(&nkids, 1u)] = r0 | (g << 13);
+            if (p == r0) kids[atomicAdd(&nkids, 1u)] = r0 | (g << 13) | (rexact ? 1u << 31 : 0u);
         } else if (p == r0) {
             if (g == 2) {
                 const uint32_t sa = perm[p], sb2 = perm[p + 1];
                 uint64_t l;
-                const int c = walk_compare(A.arena, off1[sa], off1[sb2], exact ? depth + 8 : depth,
-                                           &l, fetches);
+                const int c = walk_compare(A.arena, off1[sa], off1[sb2], depth + 8, &l, fetches);
                 if (A.lcp) A.lcp[dst] = l;
                 A.out[dst] = off1[c > 0 ? sb2 : sa];
                 A.out[dst + 1] = off1[c > 0 ? sa : sb2];
@@ -963,8 +1017,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     const uint32_t nt = nties, nk = nkids;
     for (uint32_t q = t >> 5; q < nt; q += THREADS / 32) {
         const uint32_t x = ties[q];
-        tie_group_warp(A, s, x & 0x1FFFu, x >> 13, off1, perm, exact ? depth + 8 : depth, lane,
-                       fetches);
+        tie_group_warp(A, s, x & 0x1FFFu, x >> 13, off1, perm, depth + 8, lane, fetches);
     }
     // children: one list reservation per size class per CTA
     if (nk) {
@@ -974,7 +1027,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         }
         __syncthreads();
         for (uint32_t q = t; q < nk; q += THREADS) {
-            const uint32_t g = kids[q] >> 13;
+            const uint32_t g = (kids[q] >> 13) & 0x3FFFu;
             const int cls = size_class(A, g);
             atomicAdd(&es.cnt[cls], 1u);
             atomicAdd(&es.elems[cls], g);
@@ -989,9 +1042,9 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
             es.cnt[t] = 0;
         }
         __syncthreads();
-        const uint32_t cdepth = static_cast<uint32_t>(exact ? depth + 8 : depth);
         for (uint32_t q = t; q < nk; q += THREADS) {
-            const uint32_t r0 = kids[q] & 0x1FFFu, g = kids[q] >> 13;
+            const uint32_t x = kids[q], r0 = x & 0x1FFFu, g = (x >> 13) & 0x3FFFu;
+            const uint32_t cdepth = static_cast<uint32_t>(depth) + ((x >> 31) ? 8u : 0u);
             const int cls = size_class(A, g);
             const uint32_t at = es.base[cls] + atomicAdd(&es.cnt[cls], 1u);
             if (at < A.cap[cls]) A.next[cls][at] = Seg{s.begin + r0, g, cdepth, ns};
