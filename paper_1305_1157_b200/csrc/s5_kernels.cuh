@@ -675,6 +675,80 @@ __device__ __forceinline__ void block_sort8(uint64_t (&w)[8], uint64_t* sb) {
     }
 }
 
+// Ascending sort of the 8 words of one thread (bitonic network, 24
+// compare-exchanges with compile-time directions).
+__device__ __forceinline__ void sort8_regs(uint64_t (&w)[8]) {
+#pragma unroll
+    for (uint32_t K = 2; K <= 8; K <<= 1) {
+#pragma unroll
+        for (uint32_t J = K >> 1; J > 0; J >>= 1) {
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                if (j & J) continue;
+                const bool asc = (j & K) == 0 || K == 8;
+                const uint64_t a = w[j], b = w[j | J];
+                const bool x = (a > b) == asc;
+                w[j] = x ? b : a;
+                w[j | J] = x ? a : b;
+            }
+        }
+    }
+}
+
+// Ascending merge sort of the first n_live positions (a multiple of 8; the
+// words beyond the live ones are ~0) held eight per thread (thread t holds
+// positions 8t..8t+7): each thread sorts its eight in registers, then
+// log2(n_live/8) rounds merge sorted runs pairwise through shared memory --
+// every thread finds where its eight outputs start by a merge-path binary
+// search and merges them serially.  O(n log n) work, no padding to a power
+// of two; positions >= n_live are never touched.
+template <uint32_t THREADS>
+__device__ __forceinline__ void block_merge_sort8(uint64_t (&w)[8], uint64_t* sb,
+                                                  uint32_t n_live) {
+    const uint32_t t = threadIdx.x;
+    const uint32_t my = 8 * t;
+    const bool live = my < n_live;
+    if (live) sort8_regs(w);
+#pragma unroll 1
+    for (uint32_t width = 8; width < n_live; width <<= 1) {
+        if (live) {
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) sb[swz(my + j)] = w[j];
+        }
+        __syncthreads();
+        if (live) {
+            const uint32_t start = my & ~(2 * width - 1);
+            const uint32_t a0 = start, a1 = min(start + width, n_live);
+            const uint32_t b1 = min(start + 2 * width, n_live);
+            const uint32_t la = a1 - a0, lb = b1 - a1;
+            const uint32_t diag = my - start;
+            uint32_t lo = diag > lb ? diag - lb : 0, hi = diag < la ? diag : la;
+#pragma unroll 1
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (sb[swz(a0 + mid)] <= sb[swz(a1 + diag - 1 - mid)]) lo = mid + 1;
+                else hi = mid;
+            }
+            uint32_t ia = a0 + lo, ib = a1 + diag - lo;
+            uint64_t va = ia < a1 ? sb[swz(ia)] : ~0ull;
+            uint64_t vb = ib < b1 ? sb[swz(ib)] : ~0ull;
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                const bool take_a = ib >= b1 || (ia < a1 && va <= vb);
+                w[j] = take_a ? va : vb;
+                if (take_a) {
+                    ++ia;
+                    va = ia < a1 ? sb[swz(ia)] : ~0ull;
+                } else {
+                    ++ib;
+                    vb = ib < b1 ? sb[swz(ib)] : ~0ull;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // A run of g <= 32 strings at sorted positions gs..gs+g-1 whose keys agree
 // below `depth`, finished by one warp: bitonic sort of (run, 16 string
 // bytes) with refills 16 bytes deeper while pairs stay unresolved (the mkqs
@@ -901,14 +975,30 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     // are only candidate ties, resolved from the segment depth
     const bool exact = L >= 2;
     uint64_t w[8];
+    if (A.flags & 16) {  // power-of-two bitonic network over the whole CTA
 #pragma unroll
-    for (uint32_t j = 0; j < 8; ++j) {
-        uint32_t i = t + j * THREADS;
-        key1[i] = rk[j];
-        off1[i] = ro[j];
-        w[j] = i < s.size ? (((rk[j] << (8 * L)) & ~0xFFFull) | i) : ~0ull;
+        for (uint32_t j = 0; j < 8; ++j) {
+            uint32_t i = t + j * THREADS;
+            key1[swz(i)] = rk[j];
+            off1[i] = ro[j];
+            w[j] = i < s.size ? (((rk[j] << (8 * L)) & ~0xFFFull) | i) : ~0ull;
+        }
+        block_sort8<THREADS>(w, sb);
+    } else {  // merge sort of the live positions (slot i at position i)
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            uint32_t i = t + j * THREADS;
+            key1[swz(i)] = rk[j];
+            off1[i] = ro[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            const uint32_t i = 8 * t + j;
+            w[j] = i < s.size ? (((key1[swz(i)] << (8 * L)) & ~0xFFFull) | i) : ~0ull;
+        }
+        block_merge_sort8<THREADS>(w, sb, (s.size + 7) & ~7u);
     }
-    block_sort8<THREADS>(w, sb);
 #pragma unroll
     for (uint32_t j = 0; j < 8; ++j) sb[swz(t * 8 + j)] = w[j];
     __syncthreads();
@@ -942,11 +1032,11 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
             const uint32_t slot = perm[p];
             uint32_t r = p - r0;
             if (r1 - r0 >= 2 && r1 - r0 <= kTruncFix) {
-                const uint64_t k = key1[slot];
+                const uint64_t k = key1[swz(slot)];
                 r = 0;
 #pragma unroll 1
                 for (uint32_t q = r0; q < r1; ++q) {
-                    const uint64_t y = key1[perm[q]];
+                    const uint64_t y = key1[swz(perm[q])];
                     r += (y < k) || (y == k && q < p);
                 }
             }
@@ -960,7 +1050,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
                 const uint32_t slot = perm2[p];
                 st = (bits[p >> 5] >> (p & 31)) & 1u;
                 if (!st && run_end(bits, p) - run_begin(bits, p) <= kTruncFix)
-                    st = key1[slot] != key1[perm2[p - 1]];
+                    st = key1[swz(slot)] != key1[swz(perm2[p - 1])];
                 perm[p] = static_cast<uint16_t>(slot);
             }
             const uint32_t b = __ballot_sync(0xffffffffu, st);
@@ -979,14 +1069,14 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
 #pragma unroll 1
     for (uint32_t p = t; p < s.size; p += THREADS) {
         const uint32_t slot = perm[p];
-        const uint64_t k = key1[slot];
+        const uint64_t k = key1[swz(slot)];
         const uint32_t o = off1[slot];
         const uint32_t r0 = run_begin(rb, p), r1 = run_end(rb, p);
         const uint32_t g = r1 - r0;
         const bool rexact = exact || g <= kTruncFix;  // keys of the run are equal
         const uint32_t dst = s.begin + p;
         if (A.lcp && p + 1 == r1 && r1 < s.size)
-            A.lcp[dst] = depth + diff_bytes(k, key1[perm[r1]]);
+            A.lcp[dst] = depth + diff_bytes(k, key1[swz(perm[r1])]);
         if (g == 1 || (rexact && has_zero_byte(k))) {
             A.out[dst] = o;
             if (A.lcp && p + 1 < r1) A.lcp[dst] = depth + zero_index(k);
