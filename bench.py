@@ -398,9 +398,12 @@ def run_ours(args):
         "kernels_strings_per_step": {k: int(v["strings"]) for k, v in sorted(kern.items())},
         "launch_recs": prof_stats[-1].get("launch_recs", []) if args.launch_recs else None,
         "e2e": {"value": world * n / e2e_s, "unit": "strings/s",
-                "h2d_bytes_per_step": int(8 * n), "d2h_bytes_per_step": int(8 * n + 8 * (n - 1)),
+                "h2d_bytes_per_step": int(e2e_phases.get("h2d_bytes", 8 * n)),
+                "d2h_bytes_per_step": int(e2e_phases.get("d2h_bytes", 16 * n - 8)),
                 "ms_per_step": 1e3 * e2e_s,
-                "note": "parallel_sample_sort(numpy handles, lcp_out=numpy): H2D + sort + D2H",
+                "note": "parallel_sample_sort(numpy int64 handles, lcp_out=numpy int64): "
+                        "handles cross PCIe as u32 both ways, LCPs in the narrowest width "
+                        "holding their maximum; H2D + sort + D2H + host widening",
                 "phases_ms": e2e_phases},
         "arena_upload_s": arena_upload_s,
         "gpu_launches": launches_per_step * args.steps,

@@ -95,6 +95,7 @@ typedef struct {
     uint32_t pad3_;
     float host_h2d_ms, host_sort_ms, host_d2h_ms, pad4_;  /* s5_sort_host phases (wall) */
     s5_launch_rec launch_recs[S5_MAX_LAUNCH_RECS];
+    uint64_t host_h2d_bytes, host_d2h_bytes;  /* s5_sort_host: bytes over PCIe       */
 } s5_stats;
 
 enum {

@@ -58,7 +58,8 @@ class S5Stats(C.Structure):
                 ("kern_strings", C.c_uint64 * 16), ("n_launch_recs", C.c_uint32),
                 ("pad3_", C.c_uint32), ("host_h2d_ms", C.c_float), ("host_sort_ms", C.c_float),
                 ("host_d2h_ms", C.c_float), ("pad4_", C.c_float),
-                ("launch_recs", S5LaunchRec * S5_MAX_LAUNCH_RECS)]
+                ("launch_recs", S5LaunchRec * S5_MAX_LAUNCH_RECS),
+                ("host_h2d_bytes", C.c_uint64), ("host_d2h_bytes", C.c_uint64)]
 
     def as_dict(self) -> dict:
         L = min(self.levels, S5_MAX_LEVELS)

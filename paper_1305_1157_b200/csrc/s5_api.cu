@@ -13,6 +13,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -241,6 +244,121 @@ struct Prof {
     }
     size_t recs_total = 0;
 };
+
+}  // namespace
+
+namespace {
+
+// Persistent host worker pool for the staging copies (thread start-up per
+// chunk would cost more than the copies themselves).
+class Pool {
+    std::vector<std::thread> th_;
+    std::mutex mu_;
+    std::condition_variable go_, done_;
+    std::function<void(unsigned)> job_;
+    uint64_t gen_ = 0;
+    unsigned left_ = 0;
+    bool stop_ = false;
+    unsigned T_ = 1;
+
+    Pool() {
+        T_ = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        for (unsigned i = 1; i < T_; ++i) th_.emplace_back([this, i] { loop(i); });
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+        }
+        go_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void loop(unsigned i) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::function<void(unsigned)> f;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                go_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                f = job_;
+            }
+            f(i);
+            std::lock_guard<std::mutex> g(mu_);
+            if (--left_ == 0) done_.notify_one();
+        }
+    }
+
+public:
+    static Pool& get() {
+        static Pool p;
+        return p;
+    }
+    // f(begin, end) over T contiguous parts of [0, n)
+    void par_for(uint64_t n, const std::function<void(uint64_t, uint64_t)>& f) {
+        const unsigned T = n < (1u << 16) ? 1u : T_;
+        if (T == 1) {
+            f(0, n);
+            return;
+        }
+        auto part = [&, T](unsigned i) { f(n * i / T, n * (i + 1) / T); };
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            job_ = part;
+            left_ = T_ - 1;
+            ++gen_;
+        }
+        go_.notify_all();
+        part(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return left_ == 0; });
+    }
+};
+
+void par_memcpy(void* dst, const void* src, uint64_t bytes) {
+    Pool::get().par_for(bytes, [&](uint64_t a, uint64_t b) {
+        memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+    });
+}
+
+__global__ void k_widen32(const uint32_t* __restrict__ a, int64_t* __restrict__ b, uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        b[i] = a[i];
+}
+
+template <typename T>
+__global__ void k_narrow(const int64_t* __restrict__ a, T* __restrict__ b, uint64_t n) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        b[i] = static_cast<T>(a[i]);
+}
+
+__global__ void k_max64(const int64_t* __restrict__ a, uint64_t n, unsigned long long* out) {
+    unsigned long long m = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        m = max(m, static_cast<unsigned long long>(a[i]));
+    for (int x = 16; x > 0; x >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, x));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+struct HostPath {
+    std::mutex mu;
+    void* dbuf = nullptr;
+    uint64_t dbytes = 0;
+    void* stage[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    unsigned long long* dmax = nullptr;
+    unsigned long long* hmax = nullptr;
+    static constexpr uint64_t kChunk = 32ull << 20;  // bytes per staging buffer
+};
+
+HostPath& host_path() {
+    static HostPath hp;
+    return hp;
+}
 
 }  // namespace
 
@@ -511,42 +629,12 @@ int s5_sort_audit(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_handles
 // Host-buffer entry: handles and LCP move through two pinned staging chunks
 // so the host memcpy of chunk i overlaps the DMA of chunk i-1 (H2D) and the
 // DMA of chunk i+1 overlaps the copy-out of chunk i (D2H).
-namespace {
 
-void par_memcpy(void* dst, const void* src, uint64_t bytes) {
-    const uint64_t kMin = 8ull << 20;
-    unsigned t = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    uint64_t parts = std::min<uint64_t>(t, (bytes + kMin - 1) / kMin);
-    if (parts <= 1) {
-        memcpy(dst, src, bytes);
-        return;
-    }
-    std::vector<std::thread> th;
-    uint64_t per = (bytes + parts - 1) / parts;
-    for (uint64_t p = 0; p < parts; ++p) {
-        uint64_t a = p * per, b = std::min(bytes, a + per);
-        if (a >= b) break;
-        th.emplace_back([=] { memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a); });
-    }
-    for (auto& x : th) x.join();
-}
-
-struct HostPath {
-    std::mutex mu;
-    void* dbuf = nullptr;
-    uint64_t dbytes = 0;
-    void* stage[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    static constexpr uint64_t kChunk = 64ull << 20;
-};
-
-HostPath& host_path() {
-    static HostPath hp;
-    return hp;
-}
-
-}  // namespace
-
+// Host-buffer entry.  Offsets are 32-bit (arena < 4 GiB), so the handles
+// cross PCIe as u32 (narrowed on the host while they are staged, with the
+// range check the device would do) and come back as u32; the LCP array
+// comes back in the narrowest of 1/2/4/8 bytes that holds its maximum.
+// Host workers narrow/widen chunk i while the DMA of chunk i+-1 runs.
 int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles, uint64_t n,
                  uint64_t depth, int64_t* h_lcp, const s5_config* cfg, void* stream_,
                  s5_stats* stats) {
@@ -558,8 +646,11 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
     }
     Cfg c;
     if (int rc = resolve(cfg, &c)) return rc;
+    if (arena_len > 0xFFFFFFFFull)
+        return fail(S5_E_RANGE, "arena of %llu bytes: offsets are 32-bit (< 4 GiB)",
+                    static_cast<unsigned long long>(arena_len));
     uint64_t ws = make_layout(n, c).total;
-    uint64_t need = align_up(n * 8) + align_up(n * 8) + ws;
+    uint64_t need = 2 * align_up(n * 8) + 2 * align_up(n * 4) + ws;
     if (need > H.dbytes) {
         if (H.dbuf) cudaFree(H.dbuf);
         H.dbuf = nullptr;
@@ -572,61 +663,102 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
             S5_CUDA(cudaHostAlloc(&H.stage[i], HostPath::kChunk, cudaHostAllocDefault));
             S5_CUDA(cudaEventCreateWithFlags(&H.ev[i], cudaEventDisableTiming));
         }
+        S5_CUDA(cudaMalloc(&H.dmax, sizeof(unsigned long long)));
+        S5_CUDA(cudaHostAlloc(&H.hmax, sizeof(unsigned long long), cudaHostAllocDefault));
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream_);
-    int64_t* dh = static_cast<int64_t*>(H.dbuf);
-    int64_t* dl = reinterpret_cast<int64_t*>(static_cast<char*>(H.dbuf) + align_up(n * 8));
-    void* dws = static_cast<char*>(H.dbuf) + 2 * align_up(n * 8);
+    char* base = static_cast<char*>(H.dbuf);
+    int64_t* dh = reinterpret_cast<int64_t*>(base);
+    int64_t* dl = reinterpret_cast<int64_t*>(base + align_up(n * 8));
+    uint32_t* d32 = reinterpret_cast<uint32_t*>(base + 2 * align_up(n * 8));
+    void* dn = base + 2 * align_up(n * 8) + align_up(n * 4);
+    void* dws = base + 2 * align_up(n * 8) + 2 * align_up(n * 4);
+    Pool& pool = Pool::get();
 
-    // H2D of the handles
+    // H2D: narrow + range-check into pinned staging, DMA, widen on the device
     auto t0 = std::chrono::steady_clock::now();
-    const uint64_t bytes = n * 8;
-    uint64_t i = 0;
-    for (uint64_t off = 0; off < bytes; off += HostPath::kChunk, ++i) {
-        uint64_t len = std::min(HostPath::kChunk, bytes - off);
-        int b = static_cast<int>(i & 1);
-        if (i >= 2) S5_CUDA(cudaEventSynchronize(H.ev[b]));
-        par_memcpy(H.stage[b], reinterpret_cast<const char*>(h_handles) + off, len);
-        S5_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dh) + off, H.stage[b], len,
-                                cudaMemcpyHostToDevice, st));
+    const uint64_t per = HostPath::kChunk / 4;
+    std::atomic<bool> bad{false};
+    uint64_t ci = 0;
+    for (uint64_t off = 0; off < n; off += per, ++ci) {
+        const uint64_t len = std::min(per, n - off);
+        const int b = static_cast<int>(ci & 1);
+        if (ci >= 2) S5_CUDA(cudaEventSynchronize(H.ev[b]));
+        uint32_t* s32 = static_cast<uint32_t*>(H.stage[b]);
+        const int64_t* src = h_handles + off;
+        pool.par_for(len, [&](uint64_t a, uint64_t e) {
+            uint64_t any = 0;
+            for (uint64_t i = a; i < e; ++i) {
+                const uint64_t x = static_cast<uint64_t>(src[i]);
+                any |= x >= arena_len;
+                s32[i] = static_cast<uint32_t>(x);
+            }
+            if (any) bad.store(true, std::memory_order_relaxed);
+        });
+        S5_CUDA(cudaMemcpyAsync(d32 + off, s32, len * 4, cudaMemcpyHostToDevice, st));
         S5_CUDA(cudaEventRecord(H.ev[b], st));
     }
+    k_widen32<<<grid_for(n, 256), 256, 0, st>>>(d32, dh, n);
     S5_CUDA(cudaStreamSynchronize(st));
+    if (bad.load()) return fail(S5_E_RANGE, "handle outside the arena");
     auto t1 = std::chrono::steady_clock::now();
     int rc = s5_sort(d_arena, arena_len, dh, n, depth, h_lcp ? dl : nullptr, cfg, dws, ws,
                      stream_, stats);
     if (rc) return rc;
+
+    // D2H: narrow on the device, DMA, widen into the caller's arrays
+    k_narrow<uint32_t><<<grid_for(n, 256), 256, 0, st>>>(dh, d32, n);
+    uint32_t w = 8;
+    if (h_lcp) {
+        S5_CUDA(cudaMemsetAsync(H.dmax, 0, sizeof(unsigned long long), st));
+        k_max64<<<grid_for(n - 1, 256), 256, 0, st>>>(dl, n - 1, H.dmax);
+        S5_CUDA(cudaMemcpyAsync(H.hmax, H.dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        S5_CUDA(cudaStreamSynchronize(st));
+        const unsigned long long mx = *H.hmax;
+        w = mx <= 0xFFull ? 1 : mx <= 0xFFFFull ? 2 : mx <= 0xFFFFFFFFull ? 4 : 8;
+        const int g = grid_for(n - 1, 256);
+        if (w == 1) k_narrow<uint8_t><<<g, 256, 0, st>>>(dl, static_cast<uint8_t*>(dn), n - 1);
+        if (w == 2) k_narrow<uint16_t><<<g, 256, 0, st>>>(dl, static_cast<uint16_t*>(dn), n - 1);
+        if (w == 4) k_narrow<uint32_t><<<g, 256, 0, st>>>(dl, static_cast<uint32_t*>(dn), n - 1);
+    }
+    S5_CUDA(cudaGetLastError());
     S5_CUDA(cudaStreamSynchronize(st));
     auto t2 = std::chrono::steady_clock::now();
 
-    // D2H of handles then LCP, one DMA ahead of the copy-out
-    struct Piece { const char* d; char* h; uint64_t len; };
+    struct Piece { const char* d; int64_t* h; uint64_t count; uint32_t w; };
     std::vector<Piece> pieces;
-    for (uint64_t off = 0; off < bytes; off += HostPath::kChunk)
-        pieces.push_back({reinterpret_cast<const char*>(dh) + off,
-                          reinterpret_cast<char*>(h_handles) + off,
-                          std::min(HostPath::kChunk, bytes - off)});
+    for (uint64_t off = 0; off < n; off += per)
+        pieces.push_back({reinterpret_cast<const char*>(d32 + off), h_handles + off,
+                          std::min(per, n - off), 4});
     if (h_lcp) {
-        const uint64_t lb = (n - 1) * 8;
-        for (uint64_t off = 0; off < lb; off += HostPath::kChunk)
-            pieces.push_back({reinterpret_cast<const char*>(dl) + off,
-                              reinterpret_cast<char*>(h_lcp) + off,
-                              std::min(HostPath::kChunk, lb - off)});
+        const char* src = w == 8 ? reinterpret_cast<const char*>(dl) : static_cast<const char*>(dn);
+        const uint64_t pl = HostPath::kChunk / w;
+        for (uint64_t off = 0; off < n - 1; off += pl)
+            pieces.push_back({src + off * w, h_lcp + off, std::min(pl, n - 1 - off), w});
     }
     auto issue = [&](uint64_t k) -> int {
         int b = static_cast<int>(k & 1);
-        S5_CUDA(cudaMemcpyAsync(H.stage[b], pieces[k].d, pieces[k].len, cudaMemcpyDeviceToHost, st));
+        S5_CUDA(cudaMemcpyAsync(H.stage[b], pieces[k].d, pieces[k].count * pieces[k].w,
+                                cudaMemcpyDeviceToHost, st));
         S5_CUDA(cudaEventRecord(H.ev[b], st));
         return 0;
     };
-    if (!pieces.empty())
-        if (int e = issue(0)) return e;
+    if (int e = issue(0)) return e;
     for (uint64_t k = 0; k < pieces.size(); ++k) {
         if (k + 1 < pieces.size())
             if (int e = issue(k + 1)) return e;
-        int b = static_cast<int>(k & 1);
+        const int b = static_cast<int>(k & 1);
         S5_CUDA(cudaEventSynchronize(H.ev[b]));
-        par_memcpy(pieces[k].h, H.stage[b], pieces[k].len);
+        const Piece P = pieces[k];
+        const void* sp = H.stage[b];
+        pool.par_for(P.count, [&](uint64_t a, uint64_t e) {
+            switch (P.w) {
+                case 1: { auto q = static_cast<const uint8_t*>(sp); for (uint64_t i = a; i < e; ++i) P.h[i] = q[i]; break; }
+                case 2: { auto q = static_cast<const uint16_t*>(sp); for (uint64_t i = a; i < e; ++i) P.h[i] = q[i]; break; }
+                case 4: { auto q = static_cast<const uint32_t*>(sp); for (uint64_t i = a; i < e; ++i) P.h[i] = q[i]; break; }
+                default: memcpy(P.h + a, static_cast<const int64_t*>(sp) + a, (e - a) * 8);
+            }
+        });
     }
     S5_CUDA(cudaStreamSynchronize(st));
     auto t3 = std::chrono::steady_clock::now();
@@ -634,6 +766,8 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
         stats->host_h2d_ms = std::chrono::duration<float, std::milli>(t1 - t0).count();
         stats->host_sort_ms = std::chrono::duration<float, std::milli>(t2 - t1).count();
         stats->host_d2h_ms = std::chrono::duration<float, std::milli>(t3 - t2).count();
+        stats->host_h2d_bytes = n * 4;
+        stats->host_d2h_bytes = n * 4 + (h_lcp ? (n - 1) * w : 0);
     }
     return 0;
 }

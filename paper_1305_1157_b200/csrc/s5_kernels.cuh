@@ -695,18 +695,36 @@ __device__ __forceinline__ void sort8_regs(uint64_t (&w)[8]) {
     }
 }
 
+// the eight words of thread t at positions 8t..8t+7 of a shared array, as
+// four 16-byte accesses
+__device__ __forceinline__ void store8(uint64_t* sb, uint32_t my, const uint64_t (&w)[8]) {
+    ulonglong2* q = reinterpret_cast<ulonglong2*>(sb + my);
+#pragma unroll
+    for (uint32_t j = 0; j < 4; ++j) q[j] = make_ulonglong2(w[2 * j], w[2 * j + 1]);
+}
+
+__device__ __forceinline__ void load8(const uint64_t* sb, uint32_t my, uint64_t (&w)[8]) {
+    const ulonglong2* q = reinterpret_cast<const ulonglong2*>(sb + my);
+#pragma unroll
+    for (uint32_t j = 0; j < 4; ++j) {
+        const ulonglong2 x = q[j];
+        w[2 * j] = x.x;
+        w[2 * j + 1] = x.y;
+    }
+}
+
 // Ascending merge sort of the first n_live positions (a multiple of 8; the
 // words beyond the live ones are ~0) held eight per thread (thread t holds
 // positions 8t..8t+7): each thread sorts its eight in registers, then
 // log2(n_live/8) rounds merge sorted runs pairwise through shared memory --
 // every thread finds where its eight outputs start by a merge-path binary
-// search and merges them serially.  O(n log n) work, no padding to a power
-// of two; positions >= n_live are never touched.
+// search and merges them serially (one shared load per output, no
+// divergence).  O(n log n) work, no padding to a power of two; positions
+// >= n_live are never touched.
 template <uint32_t THREADS>
 __device__ __forceinline__ void block_merge_sort8(uint64_t (&w)[8], uint64_t* sb,
                                                   uint32_t n_live) {
-    const uint32_t t = threadIdx.x;
-    const uint32_t my = 8 * t;
+    const uint32_t my = 8 * threadIdx.x;
     const bool live = my < n_live;
     if (live) sort8_regs(w);
 #pragma unroll 1
@@ -717,11 +735,9 @@ __device__ __forceinline__ void block_merge_sort8(uint64_t (&w)[8], uint64_t* sb
         }
         __syncthreads();
         if (live) {
-            const uint32_t start = my & ~(2 * width - 1);
-            const uint32_t a0 = start, a1 = min(start + width, n_live);
-            const uint32_t b1 = min(start + 2 * width, n_live);
-            const uint32_t la = a1 - a0, lb = b1 - a1;
-            const uint32_t diag = my - start;
+            const uint32_t a0 = my & ~(2 * width - 1);
+            const uint32_t a1 = min(a0 + width, n_live), b1 = min(a0 + 2 * width, n_live);
+            const uint32_t diag = my - a0, la = a1 - a0, lb = b1 - a1;
             uint32_t lo = diag > lb ? diag - lb : 0, hi = diag < la ? diag : la;
 #pragma unroll 1
             while (lo < hi) {
@@ -734,15 +750,14 @@ __device__ __forceinline__ void block_merge_sort8(uint64_t (&w)[8], uint64_t* sb
             uint64_t vb = ib < b1 ? sb[swz(ib)] : ~0ull;
 #pragma unroll
             for (uint32_t j = 0; j < 8; ++j) {
-                const bool take_a = ib >= b1 || (ia < a1 && va <= vb);
-                w[j] = take_a ? va : vb;
-                if (take_a) {
-                    ++ia;
-                    va = ia < a1 ? sb[swz(ia)] : ~0ull;
-                } else {
-                    ++ib;
-                    vb = ib < b1 ? sb[swz(ib)] : ~0ull;
-                }
+                const bool pa = va <= vb;  // an exhausted side holds ~0 (live words are smaller)
+                w[j] = pa ? va : vb;
+                ia += pa;
+                ib += !pa;
+                const uint32_t nx = pa ? ia : ib;
+                const uint64_t nv = (pa ? ia < a1 : ib < b1) ? sb[swz(nx)] : ~0ull;
+                va = pa ? nv : va;
+                vb = pa ? vb : nv;
             }
         }
         __syncthreads();
@@ -975,32 +990,30 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     // are only candidate ties, resolved from the segment depth
     const bool exact = L >= 2;
     uint64_t w[8];
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) {
+        uint32_t i = t + j * THREADS;
+        key1[i] = rk[j];
+        off1[i] = ro[j];
+    }
     if (A.flags & 16) {  // power-of-two bitonic network over the whole CTA
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j) {
             uint32_t i = t + j * THREADS;
-            key1[swz(i)] = rk[j];
-            off1[i] = ro[j];
             w[j] = i < s.size ? (((rk[j] << (8 * L)) & ~0xFFFull) | i) : ~0ull;
         }
         block_sort8<THREADS>(w, sb);
     } else {  // merge sort of the live positions (slot i at position i)
-#pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) {
-            uint32_t i = t + j * THREADS;
-            key1[swz(i)] = rk[j];
-            off1[i] = ro[j];
-        }
         __syncthreads();
+        load8(key1, 8 * t, w);
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j) {
             const uint32_t i = 8 * t + j;
-            w[j] = i < s.size ? (((key1[swz(i)] << (8 * L)) & ~0xFFFull) | i) : ~0ull;
+            w[j] = i < s.size ? (((w[j] << (8 * L)) & ~0xFFFull) | i) : ~0ull;
         }
         block_merge_sort8<THREADS>(w, sb, (s.size + 7) & ~7u);
     }
-#pragma unroll
-    for (uint32_t j = 0; j < 8; ++j) sb[swz(t * 8 + j)] = w[j];
+    store8(sb, 8 * t, w);
     __syncthreads();
 
     // runs of equal words: start bitmap (positions >= size all start runs)
@@ -1011,8 +1024,8 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     }
 #pragma unroll 1
     for (uint32_t p = t; p < N; p += THREADS) {
-        const uint64_t wp = sb[swz(p)];
-        const bool st = p == 0 || p >= s.size || (wp >> 12) != (sb[swz(p - 1)] >> 12);
+        const uint64_t wp = sb[p];
+        const bool st = p == 0 || p >= s.size || (wp >> 12) != (sb[p - 1] >> 12);
         const uint32_t b = __ballot_sync(0xffffffffu, st);
         if (lane == 0) bits[p >> 5] = b;
         if (p < s.size) perm[p] = static_cast<uint16_t>(wp & 0xFFFu);
@@ -1032,11 +1045,11 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
             const uint32_t slot = perm[p];
             uint32_t r = p - r0;
             if (r1 - r0 >= 2 && r1 - r0 <= kTruncFix) {
-                const uint64_t k = key1[swz(slot)];
+                const uint64_t k = key1[(slot)];
                 r = 0;
 #pragma unroll 1
                 for (uint32_t q = r0; q < r1; ++q) {
-                    const uint64_t y = key1[swz(perm[q])];
+                    const uint64_t y = key1[(perm[q])];
                     r += (y < k) || (y == k && q < p);
                 }
             }
@@ -1050,7 +1063,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
                 const uint32_t slot = perm2[p];
                 st = (bits[p >> 5] >> (p & 31)) & 1u;
                 if (!st && run_end(bits, p) - run_begin(bits, p) <= kTruncFix)
-                    st = key1[swz(slot)] != key1[swz(perm2[p - 1])];
+                    st = key1[(slot)] != key1[(perm2[p - 1])];
                 perm[p] = static_cast<uint16_t>(slot);
             }
             const uint32_t b = __ballot_sync(0xffffffffu, st);
@@ -1069,14 +1082,14 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
 #pragma unroll 1
     for (uint32_t p = t; p < s.size; p += THREADS) {
         const uint32_t slot = perm[p];
-        const uint64_t k = key1[swz(slot)];
+        const uint64_t k = key1[(slot)];
         const uint32_t o = off1[slot];
         const uint32_t r0 = run_begin(rb, p), r1 = run_end(rb, p);
         const uint32_t g = r1 - r0;
         const bool rexact = exact || g <= kTruncFix;  // keys of the run are equal
         const uint32_t dst = s.begin + p;
         if (A.lcp && p + 1 == r1 && r1 < s.size)
-            A.lcp[dst] = depth + diff_bytes(k, key1[swz(perm[r1])]);
+            A.lcp[dst] = depth + diff_bytes(k, key1[(perm[r1])]);
         if (g == 1 || (rexact && has_zero_byte(k))) {
             A.out[dst] = o;
             if (A.lcp && p + 1 < r1) A.lcp[dst] = depth + zero_index(k);

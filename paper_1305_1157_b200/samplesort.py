@@ -193,7 +193,8 @@ def _sort_host(arena, handles, depth, cfg, counters, lcp_out, dev):
     _record(counters, st)
     global LAST_HOST_MS
     LAST_HOST_MS = {"h2d": float(st.host_h2d_ms), "sort": float(st.host_sort_ms),
-                    "d2h": float(st.host_d2h_ms)}
+                    "d2h": float(st.host_d2h_ms), "h2d_bytes": int(st.host_h2d_bytes),
+                    "d2h_bytes": int(st.host_d2h_bytes)}
     if h is not handles:
         handles[:] = h
     if lcp_out is not None and lcp_buf is not lcp_out:

@@ -112,6 +112,27 @@ def test_tiny_inputs():
         assert got == sorted(strs), n
 
 
+def test_host_path_lcp_widths_and_range():
+    # the host path returns LCPs in the narrowest width that holds them:
+    # LCPs above 255 and 65535 take the 2- and 4-byte transfers
+    from paper_1305_1157_b200 import arena_from_strings
+    for L in (300, 70000):
+        strs = [b"x" * L + bytes([97 + i % 3, 98 + (i * 7) % 5]) for i in range(40)] + [b"a", b"b"]
+        arena, h = arena_from_strings(strs)
+        h2, lcp = sort_with_lcp(arena, h.copy())
+        raw = arena.data.tobytes()
+        assert [raw[x:raw.index(0, x)] for x in h2] == sorted(strs)
+        assert np.array_equal(lcp, O.adjacent_lcps(arena, h2))
+        assert lcp.max() >= L
+    # handles outside the arena are rejected before any sorting
+    arena, h = arena_from_strings([b"ab", b"cd", b"ef", b"gh"])
+    for badv in (arena.data.size + 10, -1, 1 << 33):
+        bad = h.copy()
+        bad[2] = badv
+        with pytest.raises((IndexError, ValueError)):
+            sort_with_lcp(arena, bad)
+
+
 def test_pack_keys_matches_reference():
     from conftest import GOLDEN
     z = np.load(os.path.join(GOLDEN, "pack_keys.npz"))
