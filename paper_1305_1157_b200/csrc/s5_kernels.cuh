@@ -1454,13 +1454,13 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
     const uint32_t lane = threadIdx.x & 31;
     unsigned long long fetches = 0;
     constexpr uint32_t IT = kWideTile / kWideThreads;
-    for (uint32_t base = lo; base < hi; base += kWideTile) {
-        for (uint32_t b = threadIdx.x; b <= g.k; b += kWideThreads) cnt[b] = 0;
-        __syncthreads();
-        uint64_t kk[IT];
-        uint32_t oo[IT], br[IT];  // bucket | rank-in-tile << 16
+    uint64_t kk[IT];
+    uint32_t oo[IT], br[IT];  // bucket | rank-in-tile << 16
+    // tile loads are issued one tile ahead: the loads of tile t+1 are in
+    // flight while tile t is written out
+    auto load_tile = [&](uint32_t base) {
 #pragma unroll
-        for (uint32_t j = 0; j < IT; ++j) {  // all loads in flight first
+        for (uint32_t j = 0; j < IT; ++j) {
             uint32_t i = base + j * kWideThreads + threadIdx.x;
             if (i < hi) {
                 kk[j] = __ldcs(key + i);
@@ -1468,6 +1468,11 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
                 br[j] = __ldcs(bkt + i);
             }
         }
+    };
+    if (lo < hi) load_tile(lo);
+    for (uint32_t base = lo; base < hi; base += kWideTile) {
+        for (uint32_t b = threadIdx.x; b <= g.k; b += kWideThreads) cnt[b] = 0;
+        __syncthreads();
 #pragma unroll
         for (uint32_t j = 0; j < IT; ++j) {
             uint32_t i = base + j * kWideThreads + threadIdx.x;
@@ -1492,6 +1497,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
                 sb[p] = static_cast<uint16_t>(b);
             }
         }
+        if (base + kWideTile < hi) load_tile(base + kWideTile);
         __syncthreads();
         const uint32_t m = min(kWideTile, hi - base);
         for (uint32_t t = threadIdx.x; t < m; t += kWideThreads) {
