@@ -12,6 +12,7 @@
 #include <cstddef>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <condition_variable>
@@ -428,6 +429,8 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.local_m_max = std::min(c.local_max, LocalMCfg::maxn);
     A.wide_dcap = c.wide_dcap;
     A.local_target = c.local_target;
+    A.wide_chunk = kWideChunkMin;
+    if (const char* e = getenv("S5_WIDE_CHUNK")) A.wide_chunk = std::max(1024, atoi(e));  // tuning
     A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max * 3 / 8);
     A.narrow_max = c.narrow_max;
     A.dmax = c.dmax;
@@ -530,7 +533,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             prof.end();
             // upper bound on CTAs; surplus CTAs exit on ctl->wide_ctas
             uint32_t ub = static_cast<uint32_t>(std::min<uint64_t>(
-                uint64_t(m[WIDE]) * kWideCtasMax, n / kWideChunkMin + m[WIDE]));
+                uint64_t(m[WIDE]) * kWideCtasMax, n / A.wide_chunk + m[WIDE]));
             const int wsm = wide_smem(c.wide_dcap);
             prof.begin(S5_K_WIDE_COUNT, h.elems[WIDE]);
             if (c.classifier)
@@ -538,9 +541,12 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             else
                 k_wide_count<false><<<ub, kWideThreads, wsm, st>>>(A, P);
             prof.end();
-            dim3 cg(m[WIDE], ((2u << std::min(c.dmax, c.wide_dcap)) + 1023) / 1024);
+            dim3 cg(m[WIDE], ((2u << std::min(c.dmax, c.wide_dcap)) + 31) / 32);
             prof.begin(S5_K_WIDE_COLSCAN);
-            k_wide_colscan<<<cg, 1024, 0, st>>>(A, P);
+            if (m[WIDE] <= 32)  // few, large segments: many rows per column
+                k_wide_colscan<32><<<cg, 1024, 0, st>>>(A, P);
+            else
+                k_wide_colscan<8><<<cg, 256, 0, st>>>(A, P);
             prof.end();
             prof.begin(S5_K_WIDE_BSCAN);
             k_wide_bscan<<<m[WIDE], 1024, 0, st>>>(A, P);

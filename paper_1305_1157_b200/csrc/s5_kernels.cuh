@@ -59,7 +59,8 @@ struct SortArgs {
     uint32_t dmax;         // log2(cfg.v + 1)
     uint32_t wide_dcap;    // wide steps use d <= wide_dcap (<= kWideDMax)
     uint32_t wide_target;  // wide steps aim at children of about this size
-    uint32_t local_target; // one-CTA steps aim at inner buckets of about this size
+    uint32_t local_target; // unused (the local tier sorts whole segments)
+    uint32_t wide_chunk;   // strings per wide CTA at least (kWideChunkMin)
     uint32_t alpha;
     uint32_t flags;        // s5_config flags (bit2: no common-prefix skip)
     uint64_t seed;
@@ -90,11 +91,6 @@ __host__ __device__ __forceinline__ uint32_t choose_d(uint32_t size, uint32_t dm
     uint32_t d = ceil_log2((size + 15) / 16);
     if (d < 1) d = 1;
     return d < dmax ? d : dmax;
-}
-
-__host__ __device__ __forceinline__ uint32_t wide_ctas(uint32_t size) {
-    uint32_t c = (size + kWideChunkMin - 1) / kWideChunkMin;
-    return c < 1 ? 1 : (c > kWideCtasMax ? kWideCtasMax : c);
 }
 
 __device__ __forceinline__ int size_class(const SortArgs& A, uint32_t size) {
@@ -1188,7 +1184,7 @@ __device__ __forceinline__ WideGeom wide_geom(const Seg& s, const SortArgs& A) {
     g.d = d < 1 ? 1 : (d > dcap ? dcap : d);
     g.v = (1u << g.d) - 1;
     g.k = 2 * g.v + 1;
-    uint32_t c = (s.size + kWideChunkMin - 1) / kWideChunkMin;
+    uint32_t c = (s.size + A.wide_chunk - 1) / A.wide_chunk;
     uint32_t cmax = kWideFrontier / g.k;
     cmax = cmax < 1 ? 1 : (cmax > kWideCtasMax ? kWideCtasMax : cmax);
     g.C = c < 1 ? 1 : (c > cmax ? cmax : c);
@@ -1318,12 +1314,19 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
     uint16_t* __restrict__ bkt = P.bkt + s.begin;
     if (!EQUAL) {  // byte-table classification (same buckets, fewer dependent loads)
         const LutTree T = lut_build<kWideThreads>(tree, g.d, splitters, lut, nullptr);
+        uint64_t nx[4];  // keys of the next round, loaded one round ahead
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t i = lo + j * kWideThreads + threadIdx.x;
+            nx[j] = i < hi ? __ldcs(key + i) : 0;
+        }
         for (uint32_t base = lo; base < hi; base += 4 * kWideThreads) {
             uint64_t kk[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                uint32_t i = base + j * kWideThreads + threadIdx.x;
-                kk[j] = i < hi ? __ldcs(key + i) : 0;
+                kk[j] = nx[j];
+                uint32_t i = base + (4 + j) * kWideThreads + threadIdx.x;
+                nx[j] = i < hi ? __ldcs(key + i) : 0;
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -1366,32 +1369,41 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
 
 // Column prefix over the C rows of every bucket (the worker-major cursor scan
 // of samplesort.py:402-410); totals land in the bucket-start area.
-__global__ void __launch_bounds__(1024) k_wide_colscan(SortArgs A, WidePlan P) {
+// One CTA per (segment, 32 buckets): lane = bucket, the NW warps split the C
+// rows; per-warp column sums, a prefix over the warps in shared memory, then
+// every warp rewrites its rows as running exclusive prefixes (row reads and
+// writes are 128-byte coalesced).
+template <uint32_t NW>
+__global__ void __launch_bounds__(NW * 32) k_wide_colscan(SortArgs A, WidePlan P) {
+    __shared__ uint32_t part[NW][33];
     if (A.ctl->wide_ctas == 0) return;
     const uint32_t si = blockIdx.x;
     const Seg s = P.segs[si];
     const WideGeom g = wide_geom(s, A);
-    const uint32_t b = blockIdx.y * blockDim.x + threadIdx.x;
-    if (b >= g.k) return;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t b = blockIdx.y * 32 + lane;
+    if (blockIdx.y * 32 >= g.k) return;
     uint32_t* rows = P.hist_pool + P.hist_off[si];
+    const uint32_t R = (g.C + NW - 1) / NW;
+    const uint32_t r0 = min(g.C, w * R), r1 = min(g.C, r0 + R);
+    uint32_t sum = 0;
+    if (b < g.k) {
+#pragma unroll 4
+        for (uint32_t c = r0; c < r1; ++c) sum += rows[static_cast<uint64_t>(c) * g.k + b];
+    }
+    part[w][lane] = sum;
+    __syncthreads();
     uint32_t run = 0;
-    uint32_t c = 0;
-    for (; c + 8 <= g.C; c += 8) {
-        uint32_t x[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) x[q] = rows[static_cast<uint64_t>(c + q) * g.k + b];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            rows[static_cast<uint64_t>(c + q) * g.k + b] = run;
-            run += x[q];
+    for (uint32_t q = 0; q < w; ++q) run += part[q][lane];
+    if (b < g.k) {
+        for (uint32_t c = r0; c < r1; ++c) {
+            const uint64_t at = static_cast<uint64_t>(c) * g.k + b;
+            const uint32_t x = rows[at];
+            rows[at] = run;
+            run += x;
         }
+        if (w == NW - 1) rows[static_cast<uint64_t>(g.C) * g.k + b] = run;
     }
-    for (; c < g.C; ++c) {
-        uint32_t x = rows[static_cast<uint64_t>(c) * g.k + b];
-        rows[static_cast<uint64_t>(c) * g.k + b] = run;
-        run += x;
-    }
-    rows[static_cast<uint64_t>(g.C) * g.k + b] = run;
 }
 
 // Bucket starts (stage 3) and the per-bucket epilogue (children, LCP hints).
