@@ -131,7 +131,7 @@ Layout make_layout(uint64_t n, const Cfg& c) {
     L.hist_off = take(uint64_t(L.cap[WIDE]) * 8);
     // wide segments have > narrow_max strings; v+1 <= size/8, and at most
     // ceil(size/64K) <= 296 rows of k <= size/4 counters (see choose_d)
-    L.tree_cap = n / 8 + uint64_t(L.cap[WIDE]) * 2 + 16;
+    L.tree_cap = n / 4 + uint64_t(L.cap[WIDE]) * (2 + kLutWords) + 16;
     L.hist_cap = n + n / 2 + 3 * uint64_t(L.cap[WIDE]) + 65536;
     L.tree_pool = take(L.tree_cap * 8);
     L.hist_pool = take(L.hist_cap * 4);
@@ -150,7 +150,18 @@ int set_smem(K kernel, int bytes) {
     return 0;
 }
 
-constexpr int kWideTreeSmem = 2 * kWideSampleCap * 8 + (1 << kWideDMax) * 12;
+constexpr int kWideTreeSmem = kWideSampleCap * 8 + (1 << kWideDMax) * 12;
+// k_wide_tree: sample of <= alpha * v keys (power of two >= 64) + node ranges
+inline uint32_t wide_sample_words(const Cfg& c) {
+    const uint32_t dw = std::min(c.dmax, c.wide_dcap);
+    const uint32_t m = std::min<uint32_t>(kWideSampleCap, c.alpha * ((1u << dw) - 1));
+    uint32_t M = 64;
+    while (M < m) M <<= 1;
+    return M;
+}
+inline int wide_tree_smem(const Cfg& c) {
+    return wide_sample_words(c) * 8 + (1 << std::min(c.dmax, c.wide_dcap)) * 12;
+}
 constexpr int kWideSmem = (1 << kWideDMax) * 8 + ((2 << kWideDMax) + 2) * 4 + (1 << kWideDMax) * 8 + 258 * 2 + 16;
 inline int wide_smem(uint32_t dcap) {
     return (1 << dcap) * 8 + ((2 << dcap) + 2) * 4 + (1 << dcap) * 8 + 258 * 2 + 16;
@@ -430,6 +441,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.wide_dcap = c.wide_dcap;
     A.local_target = c.local_target;
     A.wide_chunk = kWideChunkMin;
+    A.wide_sample = wide_sample_words(c);
     if (const char* e = getenv("S5_WIDE_CHUNK")) A.wide_chunk = std::max(1024, atoi(e));  // tuning
     A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max * 3 / 8);
     A.narrow_max = c.narrow_max;
@@ -529,7 +541,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             k_wide_plan<<<1, 1024, 0, st>>>(A, P);
             prof.end();
             prof.begin(S5_K_WIDE_TREE);
-            k_wide_tree<<<m[WIDE], kWideThreads, kWideTreeSmem, st>>>(A, P);
+            k_wide_tree<<<m[WIDE], kWideThreads, wide_tree_smem(c), st>>>(A, P);
             prof.end();
             // upper bound on CTAs; surplus CTAs exit on ctl->wide_ctas
             uint32_t ub = static_cast<uint32_t>(std::min<uint64_t>(
@@ -549,7 +561,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
                 k_wide_colscan<8><<<cg, 256, 0, st>>>(A, P);
             prof.end();
             prof.begin(S5_K_WIDE_BSCAN);
-            k_wide_bscan<<<m[WIDE], 1024, 0, st>>>(A, P);
+            k_wide_bscan<<<m[WIDE], 256, 0, st>>>(A, P);
             prof.end();
             prof.begin(S5_K_WIDE_SCATTER, h.elems[WIDE]);
             k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::bytes(c.wide_dcap), st>>>(A, P);

@@ -61,6 +61,7 @@ struct SortArgs {
     uint32_t wide_target;  // wide steps aim at children of about this size
     uint32_t local_target; // unused (the local tier sorts whole segments)
     uint32_t wide_chunk;   // strings per wide CTA at least (kWideChunkMin)
+    uint32_t wide_sample;  // power-of-two bound of a wide step's sample (k_wide_tree smem)
     uint32_t alpha;
     uint32_t flags;        // s5_config flags (bit2: no common-prefix skip)
     uint64_t seed;
@@ -79,6 +80,9 @@ constexpr uint32_t kWideChunkMin = 16384;     // strings per CTA at least
 constexpr uint32_t kWideCtasMax = 1184;       // 8 waves of 148 SMs
 constexpr uint32_t kWideFrontier = 1u << 20;  // max C x k open bucket cursors
 constexpr int kWideItems = 4;                 // interleaved descents per thread
+// per wide segment after the level-order tree: in-order splitters, the byte
+// table (258 u16) and (pf, pb) -- built once in k_wide_tree
+constexpr uint32_t kLutWords = 65 + 2;
 
 __host__ __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) {
     uint32_t d = 0;
@@ -1204,7 +1208,7 @@ __global__ void __launch_bounds__(1024) k_wide_plan(SortArgs A, WidePlan P) {
         if (i < P.nsegs) {
             WideGeom g = wide_geom(P.segs[i], A);
             x[0] = g.C;
-            x[1] = g.v + 1;
+            x[1] = 2 * g.v + 1 + kLutWords;
             x[2] = static_cast<unsigned long long>(g.C) * g.k + g.k + 1;
         }
         unsigned long long incl[3];
@@ -1255,13 +1259,14 @@ __global__ void __launch_bounds__(1024) k_wide_plan(SortArgs A, WidePlan P) {
 }
 
 // Sample + splitter tree per wide segment (one CTA each).
-__global__ void __launch_bounds__(kWideThreads, 1) k_wide_tree(SortArgs A, WidePlan P) {
+__global__ void __launch_bounds__(kWideThreads) k_wide_tree(SortArgs A, WidePlan P) {
     extern __shared__ __align__(16) uint8_t sm[];
     if (A.ctl->wide_ctas == 0) return;
+    const uint32_t dw = A.dmax < A.wide_dcap ? A.dmax : A.wide_dcap;
     uint64_t* sample = reinterpret_cast<uint64_t*>(sm);
-    int32_t* na = reinterpret_cast<int32_t*>(sm + 2 * kWideSampleCap * 8);
-    int32_t* nb = na + (1u << kWideDMax);
-    uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << kWideDMax));
+    int32_t* na = reinterpret_cast<int32_t*>(sm + A.wide_sample * 8);
+    int32_t* nb = na + (1u << dw);
+    uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << dw));
     const Seg s = P.segs[blockIdx.x];
     const WideGeom g = wide_geom(s, A);
     uint32_t m = A.alpha * g.v;
@@ -1274,7 +1279,16 @@ __global__ void __launch_bounds__(kWideThreads, 1) k_wide_tree(SortArgs A, WideP
         sample[t] = t < m ? key[sample_index(sseed, t, s.size)] : ~0ull;
     __syncthreads();
     sort_sample<kWideThreads>(sample, M);
-    build_tree_levels<kWideThreads>(sample, m, g.d, P.tree_pool + P.tree_off[blockIdx.x], na, nb, nf);
+    uint64_t* tree = P.tree_pool + P.tree_off[blockIdx.x];
+    build_tree_levels<kWideThreads>(sample, m, g.d, tree, na, nb, nf);
+    // byte table for k_wide_count, once per segment
+    uint64_t* spl = tree + g.v + 1;
+    const LutTree T = lut_build<kWideThreads>(tree, g.d, spl, reinterpret_cast<uint16_t*>(spl + g.v),
+                                              nullptr);
+    if (threadIdx.x == 0) {
+        spl[g.v + 65] = T.pf;
+        spl[g.v + 66] = T.pb;
+    }
 }
 
 __device__ __forceinline__ uint32_t find_seg(const uint32_t* cta_start, uint32_t nsegs,
@@ -1298,7 +1312,6 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
     uint64_t* tree = reinterpret_cast<uint64_t*>(sm);
     uint32_t* hist = reinterpret_cast<uint32_t*>(sm + (1u << A.wide_dcap) * 8);
     uint64_t* splitters = reinterpret_cast<uint64_t*>(hist + (2u << A.wide_dcap) + 2);
-    uint16_t* lut = reinterpret_cast<uint16_t*>(splitters + (1u << A.wide_dcap));
     const uint32_t si = find_seg(P.cta_start, P.nsegs, G);
     const Seg s = P.segs[si];
     const WideGeom g = wide_geom(s, A);
@@ -1307,13 +1320,24 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
     const uint32_t lo = c * chunk;
     const uint32_t hi = min(s.size, lo + chunk);
     const uint64_t* tsrc = P.tree_pool + P.tree_off[si];
-    for (uint32_t i = threadIdx.x; i <= g.v; i += kWideThreads) tree[i] = tsrc[i];
+    if (EQUAL) {
+        for (uint32_t i = threadIdx.x; i <= g.v; i += kWideThreads) tree[i] = tsrc[i];
+    } else {  // splitters in order + byte table, prepared by k_wide_tree
+        const uint64_t* src = tsrc + g.v + 1;
+        uint64_t* dst = splitters;  // splitters then lut, contiguous as in the pool
+        for (uint32_t i = threadIdx.x; i < g.v + 65; i += kWideThreads) dst[i] = src[i];
+    }
     for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) hist[b] = 0;
     __syncthreads();
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
     uint16_t* __restrict__ bkt = P.bkt + s.begin;
     if (!EQUAL) {  // byte-table classification (same buckets, fewer dependent loads)
-        const LutTree T = lut_build<kWideThreads>(tree, g.d, splitters, lut, nullptr);
+        LutTree T;
+        T.s = splitters;
+        T.lut = reinterpret_cast<const uint16_t*>(splitters + g.v);
+        T.v = g.v;
+        T.pf = tsrc[2 * g.v + 1 + 65];
+        T.pb = static_cast<uint32_t>(tsrc[2 * g.v + 1 + 66]);
         uint64_t nx[4];  // keys of the next round, loaded one round ahead
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -1407,17 +1431,17 @@ __global__ void __launch_bounds__(NW * 32) k_wide_colscan(SortArgs A, WidePlan P
 }
 
 // Bucket starts (stage 3) and the per-bucket epilogue (children, LCP hints).
-__global__ void __launch_bounds__(1024) k_wide_bscan(SortArgs A, WidePlan P) {
+__global__ void __launch_bounds__(256) k_wide_bscan(SortArgs A, WidePlan P) {
     __shared__ uint32_t warp_sums[32];
     if (A.ctl->wide_ctas == 0) return;
     const uint32_t si = blockIdx.x;
     const Seg s = P.segs[si];
     const WideGeom g = wide_geom(s, A);
     uint32_t* starts = P.hist_pool + P.hist_off[si] + static_cast<uint64_t>(g.C) * g.k;
-    block_exclusive_scan<1024>(starts, g.k, warp_sums);
+    block_exclusive_scan<256>(starts, g.k, warp_sums);
     const uint64_t* tree = P.tree_pool + P.tree_off[si];
     __shared__ EmitScratch es;
-    emit_block<1024>(A, s, starts, g.k, tree, g.d, &es);
+    emit_block<256>(A, s, starts, g.k, tree, g.d, &es);
 }
 
 // Out-of-place distribution with per-CTA cursors (stage 4, samplesort.py:412-417).
