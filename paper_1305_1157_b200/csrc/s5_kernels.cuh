@@ -779,6 +779,8 @@ __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uin
     uint32_t run = valid ? 0u : 0xFFFFFFFFu;
     uint64_t k0 = ~0ull, k1 = ~0ull;
     bool resolved = false, active = valid;
+    // network width: the group's lanes [0, P) (the rest hold no string)
+    const uint32_t P = g <= 2 ? 2u : 1u << (32 - __clz(g - 1));
     for (;; depth += 16) {  // 16 string bytes per round
         if (active) {
             load_key2(A.arena, static_cast<uint64_t>(off1[e]) + depth, k0, k1);
@@ -791,7 +793,7 @@ __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uin
         const uint64_t l1 = __shfl_sync(0xffffffffu, k1, lead);
         const bool same = !active || (k0 == l0 && k1 == l1);
 #pragma unroll 1
-        for (uint32_t K = __all_sync(0xffffffffu, same) ? 64u : 2u; K <= 32; K <<= 1) {
+        for (uint32_t K = __all_sync(0xffffffffu, same) ? 64u : 2u; K <= P; K <<= 1) {
 #pragma unroll 1
             for (uint32_t J = K >> 1; J > 0; J >>= 1) {
                 uint32_t orun = __shfl_xor_sync(0xffffffffu, run, J);
