@@ -443,7 +443,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.wide_chunk = kWideChunkMin;
     A.wide_sample = wide_sample_words(c);
     if (const char* e = getenv("S5_WIDE_CHUNK")) A.wide_chunk = std::max(1024, atoi(e));  // tuning
-    A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max * 3 / 8);
+    A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max * 3 / 16);
     A.narrow_max = c.narrow_max;
     A.dmax = c.dmax;
     A.alpha = c.alpha;

@@ -54,7 +54,7 @@ class SampleSortConfig:
     narrow_max: int = 4096
     local_max: int = 4096
     wide_v: int = 255
-    wide_target: int = 1536
+    wide_target: int = 768
     local_target: int = 8
     flags: int = 0
 
