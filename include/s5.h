@@ -151,6 +151,16 @@ int s5_adjacent_lcp(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d
 int s5_first_unsorted(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_handles,
                       uint64_t n, int64_t *d_result, void *stream);
 
+/* Multi-GPU partition step (the reference's only parallel
+ * split is the pS^5 worker split, samplesort.py:369-434): the destination
+ * rank of each of n local strings is the number of the nsplit splitter
+ * strings below it in (string, handle) order; d_out receives the handles
+ * grouped by destination (order inside a group unspecified) and
+ * h_counts[nsplit+1] the group sizes (host memory).  nsplit < 1024. */
+int s5_partition(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_handles,
+                 uint64_t n, const int64_t *d_splitters, uint32_t nsplit, int64_t *d_out,
+                 uint64_t *h_counts, void *stream);
+
 /* classify_tree_unrolled / classify_tree_equal (classifier.py:259-278):
  * buckets of n keys against v = 2^d-1 sorted splitters (in-order).
  * classifier: 0 branch-free descent, 1 equality descent, 2 byte table + binary

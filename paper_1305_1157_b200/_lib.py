@@ -115,6 +115,7 @@ SIGNATURES = {
     "s5_pack_keys": (C.c_int, [_vp, _u64, _vp, _u64, _u64, _vp, _vp]),
     "s5_adjacent_lcp": (C.c_int, [_vp, _u64, _vp, _u64, _vp, _vp]),
     "s5_first_unsorted": (C.c_int, [_vp, _u64, _vp, _u64, _vp, _vp]),
+    "s5_partition": (C.c_int, [_vp, _u64, _vp, _u64, _vp, C.c_uint32, _vp, _vp, _vp]),
     "s5_classify": (C.c_int, [_vp, _u64, _vp, _u32, _u32, _vp, _vp]),
     "s5_build_tree": (C.c_int, [_vp, _u32, _u32, _vp, _vp, _vp]),
     "s5_host_markov_text": (C.c_int, [_vp, _vp, _u64, _u32, _vp]),

@@ -822,6 +822,57 @@ int s5_first_unsorted(const uint8_t* d_arena, uint64_t arena_len, const int64_t*
     return 0;
 }
 
+int s5_partition(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_handles, uint64_t n,
+                 const int64_t* d_splitters, uint32_t nsplit, int64_t* d_out, uint64_t* h_counts,
+                 void* stream) {
+    static std::mutex mu;
+    static void* scratch = nullptr;
+    static uint64_t scratch_bytes = 0;
+    static unsigned long long* h_tot = nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    (void)arena_len;
+    const uint32_t G = nsplit + 1;
+    if (G > kPartMaxRanks) return fail(S5_E_INVALID, "at most %u ranks", kPartMaxRanks);
+    if (n >= (1ull << 31)) return fail(S5_E_RANGE, "n must be < 2^31");
+    if (!h_counts) return fail(S5_E_INVALID, "null counts");
+    if (n == 0) {
+        for (uint32_t d = 0; d < G; ++d) h_counts[d] = 0;
+        return 0;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (nsplit == 0) {  // one rank: everything stays
+        S5_CUDA(cudaMemcpyAsync(d_out, d_handles, n * 8, cudaMemcpyDeviceToDevice, st));
+        S5_CUDA(cudaStreamSynchronize(st));
+        h_counts[0] = n;
+        return 0;
+    }
+    const uint32_t C = static_cast<uint32_t>(std::min<uint64_t>(1184, std::max<uint64_t>(1, n / 2048)));
+    const uint32_t chunk = static_cast<uint32_t>((n + C - 1) / C);
+    const uint64_t need = align_up(n * 2) + align_up(uint64_t(C) * G * 4) + align_up(G * 8ull);
+    if (need > scratch_bytes) {
+        if (scratch) cudaFree(scratch);
+        scratch = nullptr;
+        scratch_bytes = 0;
+        S5_CUDA(cudaMalloc(&scratch, need));
+        scratch_bytes = need;
+    }
+    if (!h_tot) S5_CUDA(cudaHostAlloc(&h_tot, kPartMaxRanks * 8, cudaHostAllocDefault));
+    char* p = static_cast<char*>(scratch);
+    uint16_t* dest = reinterpret_cast<uint16_t*>(p);
+    uint32_t* rows = reinterpret_cast<uint32_t*>(p + align_up(n * 2));
+    auto* tot = reinterpret_cast<unsigned long long*>(p + align_up(n * 2) + align_up(uint64_t(C) * G * 4));
+    k_part_count<<<C, kPartThreads, 0, st>>>(d_arena, d_handles, static_cast<uint32_t>(n),
+                                             d_splitters, nsplit, chunk, dest, rows);
+    k_part_scan<<<1, 1024, 0, st>>>(rows, C, G, tot);
+    k_part_scatter<<<C, kPartThreads, 0, st>>>(d_handles, static_cast<uint32_t>(n), chunk, G, dest,
+                                               rows, tot, d_out);
+    S5_CUDA(cudaGetLastError());
+    S5_CUDA(cudaMemcpyAsync(h_tot, tot, G * 8ull, cudaMemcpyDeviceToHost, st));
+    S5_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t d = 0; d < G; ++d) h_counts[d] = h_tot[d];
+    return 0;
+}
+
 int s5_classify(const uint64_t* d_keys, uint64_t n, const uint64_t* d_in_order, uint32_t v,
                 uint32_t classifier, uint16_t* d_buckets, void* stream) {
     uint32_t d = 0;

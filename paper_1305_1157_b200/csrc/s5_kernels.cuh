@@ -1670,4 +1670,103 @@ __global__ void __launch_bounds__(1024) k_build_tree(const uint64_t* __restrict_
     for (uint32_t c = threadIdx.x; c < v; c += 1024) in_order[c] = level_order[node_of_rank(c, d)];
 }
 
+
+// ---------------------------------------------------------------------------
+// multi-GPU partition (distributed.py step 3): destination rank
+// of every local string = number of the G-1 splitter strings below it in
+// (string, handle) order; then a stable-free grouping of the handles by
+// destination (contiguous send ranges for the all-to-all).
+
+constexpr uint32_t kPartThreads = 256;
+constexpr uint32_t kPartMaxRanks = 1024;
+
+// (string, handle) three-way compare of splitter a with string b whose
+// 8-byte keys at depth 0 are equal
+__device__ __forceinline__ int part_tail(const uint8_t* __restrict__ arena, int64_t a, int64_t b,
+                                         uint64_t key, unsigned long long& fetches) {
+    int c = 0;
+    if (!has_zero_byte(key))
+        c = walk_compare(arena, static_cast<uint64_t>(a), static_cast<uint64_t>(b), 8, nullptr,
+                         fetches);
+    return c ? c : (a < b ? -1 : (a > b ? 1 : 0));
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_count(
+        const uint8_t* __restrict__ arena, const int64_t* __restrict__ h, uint32_t n,
+        const int64_t* __restrict__ spl, uint32_t ns, uint32_t chunk, uint16_t* __restrict__ dest,
+        uint32_t* __restrict__ rows) {
+    __shared__ uint64_t skey[kPartMaxRanks];
+    __shared__ uint32_t hist[kPartMaxRanks];
+    const uint32_t G = ns + 1;
+    for (uint32_t i = threadIdx.x; i < ns; i += kPartThreads)
+        skey[i] = load_key(arena, static_cast<uint64_t>(spl[i]));
+    for (uint32_t d = threadIdx.x; d < G; d += kPartThreads) hist[d] = 0;
+    __syncthreads();
+    const uint32_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    unsigned long long fetches = 0;
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += kPartThreads) {
+        const int64_t x = h[i];
+        const uint64_t k = load_key(arena, static_cast<uint64_t>(x));
+        uint32_t a = 0, b = ns;  // first splitter not below the string
+#pragma unroll 1
+        while (a < b) {
+            const uint32_t mid = (a + b) >> 1;
+            const uint64_t sk = skey[mid];
+            const int c = sk < k ? -1 : (sk > k ? 1 : part_tail(arena, spl[mid], x, k, fetches));
+            if (c < 0) a = mid + 1; else b = mid;
+        }
+        dest[i] = static_cast<uint16_t>(a);
+        atomicAdd(&hist[a], 1u);
+    }
+    __syncthreads();
+    for (uint32_t d = threadIdx.x; d < G; d += kPartThreads)
+        rows[static_cast<uint64_t>(blockIdx.x) * G + d] = hist[d];
+}
+
+// rows[c][d] -> exclusive prefix over c per destination d; starts[d] =
+// exclusive prefix of the destination totals, starts[G] = n.  One warp per
+// destination, lanes split the rows.
+__global__ void __launch_bounds__(1024) k_part_scan(uint32_t* __restrict__ rows, uint32_t C,
+                                                    uint32_t G, unsigned long long* __restrict__ tot) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t R = (C + 31) / 32;
+    for (uint32_t d = threadIdx.x >> 5; d < G; d += 32) {
+        const uint32_t r0 = min(C, lane * R), r1 = min(C, r0 + R);
+        uint32_t sum = 0;
+        for (uint32_t c = r0; c < r1; ++c) sum += rows[static_cast<uint64_t>(c) * G + d];
+        uint32_t incl = sum;
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t run = incl - sum;
+        for (uint32_t c = r0; c < r1; ++c) {
+            const uint64_t at = static_cast<uint64_t>(c) * G + d;
+            const uint32_t x = rows[at];
+            rows[at] = run;
+            run += x;
+        }
+        if (lane == 31) tot[d] = incl;
+    }
+}
+
+__global__ void __launch_bounds__(kPartThreads) k_part_scatter(
+        const int64_t* __restrict__ h, uint32_t n, uint32_t chunk, uint32_t G,
+        const uint16_t* __restrict__ dest, const uint32_t* __restrict__ rows,
+        const unsigned long long* __restrict__ tot, int64_t* __restrict__ out) {
+    __shared__ uint32_t cur[kPartMaxRanks];
+    // destination starts: exclusive prefix of the totals (G is small)
+    for (uint32_t d = threadIdx.x; d < G; d += kPartThreads) {
+        unsigned long long st = 0;
+        for (uint32_t q = 0; q < d; ++q) st += tot[q];
+        cur[d] = static_cast<uint32_t>(st) + rows[static_cast<uint64_t>(blockIdx.x) * G + d];
+    }
+    __syncthreads();
+    const uint32_t lo = blockIdx.x * chunk, hi = min(n, lo + chunk);
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += kPartThreads) {
+        const uint32_t d = dest[i];
+        out[atomicAdd(&cur[d], 1u)] = h[i];
+    }
+}
+
 }  // namespace s5

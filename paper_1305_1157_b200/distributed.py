@@ -12,8 +12,10 @@ contiguous slices of the global sorted order:
    ranks (their order is free: the reference is not stable), and picks the
    same G-1 splitters;
 3. every local string is classified to a destination rank by binary search
-   over the splitters with full-string comparison (8-byte keys at
-   increasing depth, only undecided pairs reload);
+   over the splitters with full-string comparison and the handles are
+   grouped by destination -- one library call (``s5_partition``: a counting
+   kernel with the splitters' keys in shared memory, a column scan, a
+   scatter);
 4. ``all_to_all_single`` of the per-destination counts, then of the
    handles (NCCL over NVLink on GPUs; gloo in the CPU tests);
 5. each rank sorts its received strings with the single-GPU sorter and
@@ -51,6 +53,34 @@ class GpuBackend:
     def lengths(self, handles):
         from .strings import string_lengths
         return string_lengths(self.arena, handles)
+
+    def partition(self, handles, splitters):
+        """Handles grouped by destination rank (s5_partition) and the group
+        sizes."""
+        import ctypes as C
+
+        import torch
+        from . import _lib
+        n, ns = handles.numel(), splitters.numel()
+        out = torch.empty_like(handles)
+        counts = (C.c_uint64 * (ns + 1))()
+        rc = _lib.lib().s5_partition(self.arena.device(self.device).data_ptr(),
+                                     self.arena.data.size, handles.data_ptr(), n,
+                                     splitters.contiguous().data_ptr(), ns, out.data_ptr(), counts,
+                                     _lib.current_stream_ptr())
+        _lib.check(rc, "s5_partition")
+        return out, [int(x) for x in counts]
+
+    def lcp_pair(self, pair):
+        """LCP of two strings (one-element tensor)."""
+        import torch
+        from . import _lib
+        out = torch.empty(1, dtype=torch.int64, device=pair.device)
+        rc = _lib.lib().s5_adjacent_lcp(self.arena.device(self.device).data_ptr(),
+                                        self.arena.data.size, pair.contiguous().data_ptr(), 2,
+                                        out.data_ptr(), _lib.current_stream_ptr())
+        _lib.check(rc, "s5_adjacent_lcp")
+        return out
 
     def sort(self, handles):
         """Sort a device int64 tensor in place; returns (handles, lcp)."""
@@ -142,25 +172,12 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
     # 2. identical splitters on every rank: sort by (string, handle)
     splitters = _pick_splitters(be, allsamp, G)
 
-    # 3. destination of every local string
-    dest = torch.zeros(n_local, dtype=torch.int64, device=dev)
-    if n_local and splitters.numel():
-        lo = torch.zeros(n_local, dtype=torch.int64, device=dev)
-        hi = torch.full((n_local,), splitters.numel(), dtype=torch.int64, device=dev)
-        while True:
-            active = lo < hi
-            if not bool(active.any()):
-                break
-            idx = torch.nonzero(active).flatten()
-            mid = (lo[idx] + hi[idx]) // 2
-            c = compare_strings(be, splitters[mid], h[idx])   # splitter < string ?
-            right = c < 0
-            lo[idx[right]] = mid[right] + 1
-            hi[idx[~right]] = mid[~right]
-        dest = lo
-    order = torch.argsort(dest, stable=True)
-    send = h[order]
-    send_counts = torch.bincount(dest, minlength=G).to(torch.int64)
+    # 3. destination of every local string, handles grouped by destination
+    if G == 1 or splitters.numel() == 0:  # one rank, or no strings on any rank
+        send, counts = h, [0] * (G - 1) + [n_local]
+    else:
+        send, counts = be.partition(h, splitters)
+    send_counts = torch.tensor(counts, dtype=torch.int64, device=dev)
 
     # 4. exchange counts, then handles
     recv_counts = torch.empty_like(send_counts)
@@ -187,26 +204,9 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
             break
     if recv.numel() and nxt is not None:
         pair = torch.cat([recv[-1:], nxt])
-        bl = _lcp_pair(be, pair)
-        lcp = torch.cat([lcp, bl])
+        lcp = torch.cat([lcp, be.lcp_pair(pair)])
     offset = sum(counts[:rank])
     return ShardResult(recv, lcp, offset, counts)
-
-
-def _lcp_pair(be, pair):
-    import torch
-    depth = 0
-    while True:
-        k = be.pack_keys(pair, depth)
-        if int(k[0].item()) != int(k[1].item()):
-            x = (int(k[0].item()) ^ int(k[1].item())) & ((1 << 64) - 1)
-            return torch.tensor([depth + (64 - x.bit_length()) // 8], dtype=torch.int64,
-                                device=pair.device)
-        w = int(k[0].item()) & ((1 << 64) - 1)
-        b = w.to_bytes(8, "big")
-        if 0 in b:
-            return torch.tensor([depth + b.index(0)], dtype=torch.int64, device=pair.device)
-        depth += 8
 
 
 def _pick_splitters(be, samples, G: int):

@@ -28,6 +28,25 @@ class OracleBackend:
     def lengths(self, handles):
         return torch.from_numpy(O.string_lengths(self.arena, handles.numpy()))
 
+    def partition(self, h, splitters):
+        # binary search over the splitters with full-string comparison
+        n, G = h.numel(), splitters.numel() + 1
+        lo = torch.zeros(n, dtype=torch.int64)
+        hi = torch.full((n,), G - 1, dtype=torch.int64)
+        while True:
+            idx = torch.nonzero(lo < hi).flatten()
+            if not idx.numel():
+                break
+            mid = (lo[idx] + hi[idx]) // 2
+            right = compare_strings(self, splitters[mid], h[idx]) < 0  # splitter < string
+            lo[idx[right]] = mid[right] + 1
+            hi[idx[~right]] = mid[~right]
+        order = torch.argsort(lo, stable=True)
+        return h[order], torch.bincount(lo, minlength=G).tolist()
+
+    def lcp_pair(self, pair):
+        return torch.from_numpy(O.adjacent_lcps(self.arena, pair.numpy()))
+
     def sort(self, handles):
         h = handles.numpy().copy()
         O.parallel_sample_sort(self.arena, h, 1)

@@ -133,6 +133,35 @@ def test_host_path_lcp_widths_and_range():
             sort_with_lcp(arena, bad)
 
 
+def test_partition_kernel_groups_by_full_string_rank():
+    # multi-GPU step 3 (s5_partition): destination = number of splitters below
+    # the string in (string, handle) order; identical strings straddle a splitter
+    import bisect
+    import torch
+    from paper_1305_1157_b200 import arena_from_strings
+    from paper_1305_1157_b200.distributed import GpuBackend
+    rng = np.random.default_rng(5)
+    strs = [bytes(rng.integers(97, 100, rng.integers(0, 20)).tolist()) for _ in range(20000)]
+    strs += [b"abcabcabcabcabcabc" * 3] * 50 + [b""] * 7
+    arena, h = arena_from_strings(strs)
+    raw = arena.data.tobytes()
+    text = {int(x): raw[x:raw.index(0, x)] for x in h}
+    ident = [int(x) for x in h if text[int(x)] == b"abcabcabcabcabcabc" * 3]
+    sample = sorted({int(x) for x in rng.choice(h, 40, replace=False)} | set(ident[20:23]),
+                    key=lambda x: (text[x], x))
+    be = GpuBackend(arena)
+    out, counts = be.partition(torch.from_numpy(h.copy()).cuda(),
+                               torch.tensor(sample, dtype=torch.int64, device="cuda"))
+    out = out.cpu().numpy()
+    keys = [(text[x], x) for x in sample]
+    dest = np.array([bisect.bisect_left(keys, (text[int(x)], int(x))) for x in h])
+    assert counts == np.bincount(dest, minlength=len(sample) + 1).tolist()
+    at = 0
+    for g, c in enumerate(counts):
+        assert sorted(out[at:at + c].tolist()) == sorted(h[dest == g].tolist()), g
+        at += c
+
+
 def test_pack_keys_matches_reference():
     from conftest import GOLDEN
     z = np.load(os.path.join(GOLDEN, "pack_keys.npz"))
