@@ -192,6 +192,7 @@ def run_distributed(args):
     clocks.start()
     times = []
     res = None
+    be.launches = 0
     for _ in range(args.steps):
         d = shard.clone()
         l2_flush.zero_()
@@ -205,6 +206,7 @@ def run_distributed(args):
         torch.cuda.synchronize()
         times.append(ev0.elapsed_time(ev1))
     clk = clocks.stop()
+    launches = be.launches
     t = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_per_step = float(t.item()) / args.steps
@@ -237,7 +239,7 @@ def run_distributed(args):
                     "h2d_bytes_per_step": int(8 * n), "d2h_bytes_per_step": int(16 * n - 8),
                     "note": "host shards in, host slices + LCP out, all ranks"},
             "sorted_ok": bool(ok.item()), "slice_sizes": res.counts, "clocks": clk,
-            "gpu_launches": None,
+            "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

@@ -43,6 +43,7 @@ class GpuBackend:
         self.arena = arena
         self.cfg = cfg
         self.device = torch.device("cuda", torch.cuda.current_device())
+        self.launches = 0  # library kernels launched (sorts, partition, LCP)
         arena.device(self.device)
 
     def pack_keys(self, handles, depth: int):
@@ -69,6 +70,7 @@ class GpuBackend:
                                      splitters.contiguous().data_ptr(), ns, out.data_ptr(), counts,
                                      _lib.current_stream_ptr())
         _lib.check(rc, "s5_partition")
+        self.launches += 3
         return out, [int(x) for x in counts]
 
     def lcp_pair(self, pair):
@@ -80,16 +82,20 @@ class GpuBackend:
                                         self.arena.data.size, pair.contiguous().data_ptr(), 2,
                                         out.data_ptr(), _lib.current_stream_ptr())
         _lib.check(rc, "s5_adjacent_lcp")
+        self.launches += 1
         return out
 
     def sort(self, handles):
         """Sort a device int64 tensor in place; returns (handles, lcp)."""
         import torch
+        from . import _lib
         from .samplesort import gpu_sort
         n = handles.numel()
         lcp = torch.empty(max(n - 1, 0), dtype=torch.int64, device=handles.device)
         if n > 1:
-            gpu_sort(self.arena, handles, 0, self.cfg, lcp)
+            st = _lib.S5Stats()
+            gpu_sort(self.arena, handles, 0, self.cfg, lcp, stats=st)
+            self.launches += int(st.launches)
         return handles, lcp
 
 
