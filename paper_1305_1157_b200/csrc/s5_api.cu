@@ -14,6 +14,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <immintrin.h>
+
 #include <atomic>
 #include <condition_variable>
 #include <functional>
@@ -327,6 +329,80 @@ public:
         done_.wait(lk, [&] { return left_ == 0; });
     }
 };
+
+// Host staging kernels.  The output streams are written once and not read
+// again by this thread, so AVX2 non-temporal stores skip the read-for-
+// ownership of every destination line (half the host memory traffic).
+bool has_avx2() {
+    static const bool v = (__builtin_cpu_init(), __builtin_cpu_supports("avx2"));
+    return v;
+}
+
+// int64 handles -> u32 offsets with the range check; true if any is outside [0, lim)
+__attribute__((target("avx2"))) bool narrow_u32_avx2(const int64_t* src, uint32_t* dst, uint64_t n,
+                                                     uint64_t lim) {
+    uint64_t i = 0, bad = 0;
+    for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 31); ++i) {
+        bad |= static_cast<uint64_t>(src[i]) >= lim;
+        dst[i] = static_cast<uint32_t>(src[i]);
+    }
+    const __m256i zero = _mm256_setzero_si256();
+    const __m256i top = _mm256_set1_epi64x(static_cast<long long>(lim) - 1);
+    const __m256i lows = _mm256_setr_epi32(0, 2, 4, 6, 1, 3, 5, 7);
+    __m256i badv = zero;
+    for (; i + 8 <= n; i += 8) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 4));
+        badv = _mm256_or_si256(badv, _mm256_or_si256(_mm256_cmpgt_epi64(zero, a), _mm256_cmpgt_epi64(a, top)));
+        badv = _mm256_or_si256(badv, _mm256_or_si256(_mm256_cmpgt_epi64(zero, b), _mm256_cmpgt_epi64(b, top)));
+        const __m128i la = _mm256_castsi256_si128(_mm256_permutevar8x32_epi32(a, lows));
+        const __m128i lb = _mm256_castsi256_si128(_mm256_permutevar8x32_epi32(b, lows));
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), _mm256_set_m128i(lb, la));
+    }
+    for (; i < n; ++i) {
+        bad |= static_cast<uint64_t>(src[i]) >= lim;
+        dst[i] = static_cast<uint32_t>(src[i]);
+    }
+    _mm_sfence();
+    return bad || !_mm256_testz_si256(badv, badv);
+}
+
+template <typename T>
+__attribute__((target("avx2"))) void widen_avx2(const T* src, int64_t* dst, uint64_t n) {
+    uint64_t i = 0;
+    for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 31); ++i) dst[i] = src[i];
+    for (; i + 4 <= n; i += 4) {
+        __m256i v;
+        if (sizeof(T) == 4) {
+            v = _mm256_cvtepu32_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i)));
+        } else if (sizeof(T) == 2) {
+            v = _mm256_cvtepu16_epi64(_mm_loadl_epi64(reinterpret_cast<const __m128i*>(src + i)));
+        } else {
+            uint32_t x;
+            memcpy(&x, src + i, 4);
+            v = _mm256_cvtepu8_epi64(_mm_cvtsi32_si128(static_cast<int>(x)));
+        }
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), v);
+    }
+    for (; i < n; ++i) dst[i] = src[i];
+    _mm_sfence();
+}
+
+bool narrow_u32(const int64_t* src, uint32_t* dst, uint64_t n, uint64_t lim) {
+    if (has_avx2()) return narrow_u32_avx2(src, dst, n, lim);
+    uint64_t bad = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        bad |= static_cast<uint64_t>(src[i]) >= lim;
+        dst[i] = static_cast<uint32_t>(src[i]);
+    }
+    return bad;
+}
+
+template <typename T>
+void widen(const T* src, int64_t* dst, uint64_t n) {
+    if (has_avx2()) return widen_avx2<T>(src, dst, n);
+    for (uint64_t i = 0; i < n; ++i) dst[i] = src[i];
+}
 
 void par_memcpy(void* dst, const void* src, uint64_t bytes) {
     Pool::get().par_for(bytes, [&](uint64_t a, uint64_t b) {
@@ -705,13 +781,7 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
         uint32_t* s32 = static_cast<uint32_t*>(H.stage[b]);
         const int64_t* src = h_handles + off;
         pool.par_for(len, [&](uint64_t a, uint64_t e) {
-            uint64_t any = 0;
-            for (uint64_t i = a; i < e; ++i) {
-                const uint64_t x = static_cast<uint64_t>(src[i]);
-                any |= x >= arena_len;
-                s32[i] = static_cast<uint32_t>(x);
-            }
-            if (any) bad.store(true, std::memory_order_relaxed);
+            if (narrow_u32(src + a, s32 + a, e - a, arena_len)) bad.store(true, std::memory_order_relaxed);
         });
         S5_CUDA(cudaMemcpyAsync(d32 + off, s32, len * 4, cudaMemcpyHostToDevice, st));
         S5_CUDA(cudaEventRecord(H.ev[b], st));
@@ -771,9 +841,9 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
         const void* sp = H.stage[b];
         pool.par_for(P.count, [&](uint64_t a, uint64_t e) {
             switch (P.w) {
-                case 1: { auto q = static_cast<const uint8_t*>(sp); for (uint64_t i = a; i < e; ++i) P.h[i] = q[i]; break; }
-                case 2: { auto q = static_cast<const uint16_t*>(sp); for (uint64_t i = a; i < e; ++i) P.h[i] = q[i]; break; }
-                case 4: { auto q = static_cast<const uint32_t*>(sp); for (uint64_t i = a; i < e; ++i) P.h[i] = q[i]; break; }
+                case 1: widen(static_cast<const uint8_t*>(sp) + a, P.h + a, e - a); break;
+                case 2: widen(static_cast<const uint16_t*>(sp) + a, P.h + a, e - a); break;
+                case 4: widen(static_cast<const uint32_t*>(sp) + a, P.h + a, e - a); break;
                 default: memcpy(P.h + a, static_cast<const int64_t*>(sp) + a, (e - a) * 8);
             }
         });
