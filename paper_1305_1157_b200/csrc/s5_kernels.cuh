@@ -713,6 +713,49 @@ __device__ __forceinline__ void load8(const uint64_t* sb, uint32_t my, uint64_t 
     }
 }
 
+// Sorts the 256 words of one warp (8 per lane, lane l holds positions
+// 8l..8l+7, each lane's eight already ascending): bitonic merges of runs of
+// 8, 16, .., 128 in registers -- the first stage of each merge compares
+// position p with the block's mirror position (partner lane l ^ (g-1),
+// element 7-j), so both runs stay ascending; then half-cleaners by shuffle
+// and inside the thread.  No shared memory, no barriers.
+__device__ __forceinline__ void warp_merge256(uint64_t (&w)[8], uint32_t lane) {
+#pragma unroll 1
+    for (uint32_t g = 2; g <= 32; g <<= 1) {  // lanes per merged run
+        {
+            uint64_t o[8];
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) o[j] = __shfl_xor_sync(0xffffffffu, w[7 - j], g - 1);
+            const bool lo_half = (lane & (g >> 1)) == 0;
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                const bool lt = o[j] < w[j];
+                w[j] = (lt == lo_half) ? o[j] : w[j];
+            }
+        }
+#pragma unroll 1
+        for (uint32_t m = g >> 2; m > 0; m >>= 1) {
+            const bool keep_min = (lane & m) == 0;
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                const uint64_t o = __shfl_xor_sync(0xffffffffu, w[j], m);
+                if ((o < w[j]) == keep_min) w[j] = o;
+            }
+        }
+#pragma unroll
+        for (uint32_t J = 4; J > 0; J >>= 1) {
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                if (j & J) continue;
+                const uint64_t a = w[j], b = w[j | J];
+                const bool x = a > b;
+                w[j] = x ? b : a;
+                w[j | J] = x ? a : b;
+            }
+        }
+    }
+}
+
 // Ascending merge sort of the first n_live positions (a multiple of 8; the
 // words beyond the live ones are ~0) held eight per thread (thread t holds
 // positions 8t..8t+7): each thread sorts its eight in registers, then
@@ -726,9 +769,12 @@ __device__ __forceinline__ void block_merge_sort8(uint64_t (&w)[8], uint64_t* sb
                                                   uint32_t n_live) {
     const uint32_t my = 8 * threadIdx.x;
     const bool live = my < n_live;
-    if (live) sort8_regs(w);
+    if (8 * (threadIdx.x & ~31u) < n_live) {  // warp holds live words: runs of 256 in registers
+        sort8_regs(w);
+        warp_merge256(w, threadIdx.x & 31);
+    }
 #pragma unroll 1
-    for (uint32_t width = 8; width < n_live; width <<= 1) {
+    for (uint32_t width = 256; width < n_live; width <<= 1) {
         if (live) {
 #pragma unroll
             for (uint32_t j = 0; j < 8; ++j) sb[swz(my + j)] = w[j];
