@@ -163,7 +163,7 @@ int s5_partition(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_ha
 
 /* classify_tree_unrolled / classify_tree_equal (classifier.py:259-278):
  * buckets of n keys against v = 2^d-1 sorted splitters (in-order).
- * classifier: 0 branch-free descent, 1 equality descent, 2 byte table + binary
+ * classifier: 0 branch-free descent, 1 equality descent, 2 12-bit table + binary
  * search (the multi-CTA count kernel's classifier); identical buckets. */
 int s5_classify(const uint64_t *d_keys, uint64_t n, const uint64_t *d_in_order, uint32_t v,
                 uint32_t classifier, uint16_t *d_buckets, void *stream);

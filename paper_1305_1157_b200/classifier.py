@@ -174,7 +174,7 @@ def classify_tree_equal(keys, tree: SplitterTree, out=None):
 
 
 def classify_tree_lut(keys, tree: SplitterTree, out=None):
-    """Byte table over the splitters' first distinguishing byte + binary
+    """Table over the 12 key bits after the splitters' common prefix + binary
     search: the classifier of the multi-CTA count kernel (same buckets)."""
     return _classify(keys, tree, 2, out)
 

@@ -164,9 +164,9 @@ inline uint32_t wide_sample_words(const Cfg& c) {
 inline int wide_tree_smem(const Cfg& c) {
     return wide_sample_words(c) * 8 + (1 << std::min(c.dmax, c.wide_dcap)) * 12;
 }
-constexpr int kWideSmem = (1 << kWideDMax) * 8 + ((2 << kWideDMax) + 2) * 4 + (1 << kWideDMax) * 8 + 258 * 2 + 16;
+constexpr int kWideSmem = (1 << kWideDMax) * 8 + ((2 << kWideDMax) + 2) * 4 + (1 << kWideDMax) * 8 + (kLutCells + 1) * 2 + 16;
 inline int wide_smem(uint32_t dcap) {
-    return (1 << dcap) * 8 + ((2 << dcap) + 2) * 4 + (1 << dcap) * 8 + 258 * 2 + 16;
+    return (1 << dcap) * 8 + ((2 << dcap) + 2) * 4 + (1 << dcap) * 8 + (kLutCells + 1) * 2 + 16;
 }
 
 int init_attributes() {
@@ -952,7 +952,7 @@ int s5_classify(const uint64_t* d_keys, uint64_t n, const uint64_t* d_in_order, 
     if (classifier > 2) return fail(S5_E_INVALID, "classifier must be 0, 1 or 2");
     if (!n) return 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    int smem = (1 << d) * 8 * 2 + 258 * 2 + 16;
+    int smem = (1 << d) * 8 * 2 + (kLutCells + 1) * 2 + 16;
     if (smem > 48 * 1024) {
         if (int rc = set_smem(k_classify<0>, smem)) return rc;
         if (int rc = set_smem(k_classify<1>, smem)) return rc;

@@ -152,25 +152,33 @@ __device__ __forceinline__ void classify_iw(const uint64_t (&k)[IW], const uint6
     }
 }
 
-// Byte-table classification: the same bucket as classify_oracle
+// Table classification: the same bucket as classify_oracle
 // (classifier.py:187-200) in ~3 shared loads instead of d dependent ones.
-// The in-order splitters s[0..v) share `pb` leading bytes (value `pf`);
-// lut[x] = first splitter whose byte pb is >= x, so a key's splitter count
-// lies in [lut[x], lut[x+1]) for its byte x, finished by a binary search.
+// The in-order splitters s[0..v) share their first `lb` bits (value `pf`);
+// the next kLutBits bits of a key index lut, lut[x] = first splitter whose
+// bits there are >= x, so the key's splitter count lies in [lut[x],
+// lut[x+1]), finished by a (usually empty) binary search.
+constexpr uint32_t kLutBits = 12;
+constexpr uint32_t kLutCells = 1u << kLutBits;  // lut has kLutCells + 1 entries
+
 struct LutTree {
     const uint64_t* s;
     const uint16_t* lut;
-    uint32_t v, pb;
+    uint32_t v, lb;
     uint64_t pf;
 };
 
+__device__ __forceinline__ uint32_t lut_cell(uint64_t k, uint32_t lb) {
+    return static_cast<uint32_t>((k << lb) >> (64 - kLutBits));
+}
+
 __device__ __forceinline__ uint32_t classify_lut(uint64_t k, const LutTree& T) {
-    if (T.pb == 8) return k < T.pf ? 0u : (k > T.pf ? 2 * T.v : 1u);
-    if (T.pb) {
-        uint64_t kp = k >> (64 - 8 * T.pb);
+    if (T.lb == 64) return k < T.pf ? 0u : (k > T.pf ? 2 * T.v : 1u);
+    if (T.lb) {
+        uint64_t kp = k >> (64 - T.lb);
         if (kp != T.pf) return kp < T.pf ? 0u : 2 * T.v;
     }
-    const uint32_t x = static_cast<uint32_t>((k << (8 * T.pb)) >> 56);
+    const uint32_t x = lut_cell(k, T.lb);
     uint32_t lo = T.lut[x], hi = T.lut[x + 1];
 #pragma unroll 1
     while (lo < hi) {
@@ -180,34 +188,33 @@ __device__ __forceinline__ uint32_t classify_lut(uint64_t k, const LutTree& T) {
     return 2 * lo + ((lo < T.v && T.s[lo] == k) ? 1u : 0u);
 }
 
-// Builds s (in order, from the level-order tree t[1..v]) and lut[0..256];
+// Builds s (in order, from the level-order tree t[1..v]) and lut[0..kLutCells];
 // all threads call; ends with a barrier.  Returns the table descriptor.
 template <uint32_t THREADS>
 __device__ __forceinline__ LutTree lut_build(const uint64_t* t, uint32_t d, uint64_t* s,
-                                             uint16_t* lut, uint32_t* shared_pb) {
+                                             uint16_t* lut) {
     const uint32_t v = (1u << d) - 1;
     for (uint32_t c = threadIdx.x; c < v; c += THREADS) s[c] = t[node_of_rank(c, d)];
     __syncthreads();
     const uint64_t a = s[0], b = s[v - 1];
-    const uint32_t pb = a == b ? 8u : diff_bytes(a, b);
-    if (pb < 8) {
-        for (uint32_t x = threadIdx.x; x <= 256; x += THREADS) {
+    const uint32_t lb = a == b ? 64u : static_cast<uint32_t>(__clzll(static_cast<long long>(a ^ b)));
+    if (lb < 64) {
+        for (uint32_t x = threadIdx.x; x <= kLutCells; x += THREADS) {
             uint32_t lo = 0, hi = v;
             while (lo < hi) {
                 uint32_t mid = (lo + hi) >> 1;
-                if (((s[mid] << (8 * pb)) >> 56) < x) lo = mid + 1; else hi = mid;
+                if (lut_cell(s[mid], lb) < x) lo = mid + 1; else hi = mid;
             }
             lut[x] = static_cast<uint16_t>(lo);
         }
     }
     __syncthreads();
-    (void)shared_pb;
     LutTree T;
     T.s = s;
     T.lut = lut;
     T.v = v;
-    T.pb = pb;
-    T.pf = pb == 8 ? a : (pb ? a >> (64 - 8 * pb) : 0);
+    T.lb = lb;
+    T.pf = lb == 64 ? a : (lb ? a >> (64 - lb) : 0);
     return T;
 }
 

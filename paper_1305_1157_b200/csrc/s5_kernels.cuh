@@ -80,9 +80,11 @@ constexpr uint32_t kWideChunkMin = 16384;     // strings per CTA at least
 constexpr uint32_t kWideCtasMax = 1184;       // 8 waves of 148 SMs
 constexpr uint32_t kWideFrontier = 1u << 20;  // max C x k open bucket cursors
 constexpr int kWideItems = 4;                 // interleaved descents per thread
-// per wide segment after the level-order tree: in-order splitters, the byte
-// table (258 u16) and (pf, pb) -- built once in k_wide_tree
-constexpr uint32_t kLutWords = 65 + 2;
+// per wide segment after the level-order tree: in-order splitters, the
+// classification table (kLutCells + 1 u16) and (pf, lb) -- built once in
+// k_wide_tree
+constexpr uint32_t kLutTabWords = (kLutCells + 1 + 3) / 4;
+constexpr uint32_t kLutWords = kLutTabWords + 2;
 
 __host__ __device__ __forceinline__ uint32_t ceil_log2(uint32_t x) {
     uint32_t d = 0;
@@ -1329,13 +1331,12 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_tree(SortArgs A, WidePlan
     sort_sample<kWideThreads>(sample, M);
     uint64_t* tree = P.tree_pool + P.tree_off[blockIdx.x];
     build_tree_levels<kWideThreads>(sample, m, g.d, tree, na, nb, nf);
-    // byte table for k_wide_count, once per segment
+    // classification table for k_wide_count, once per segment
     uint64_t* spl = tree + g.v + 1;
-    const LutTree T = lut_build<kWideThreads>(tree, g.d, spl, reinterpret_cast<uint16_t*>(spl + g.v),
-                                              nullptr);
+    const LutTree T = lut_build<kWideThreads>(tree, g.d, spl, reinterpret_cast<uint16_t*>(spl + g.v));
     if (threadIdx.x == 0) {
-        spl[g.v + 65] = T.pf;
-        spl[g.v + 66] = T.pb;
+        spl[g.v + kLutTabWords] = T.pf;
+        spl[g.v + kLutTabWords + 1] = T.lb;
     }
 }
 
@@ -1370,22 +1371,22 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
     const uint64_t* tsrc = P.tree_pool + P.tree_off[si];
     if (EQUAL) {
         for (uint32_t i = threadIdx.x; i <= g.v; i += kWideThreads) tree[i] = tsrc[i];
-    } else {  // splitters in order + byte table, prepared by k_wide_tree
+    } else {  // splitters in order + classification table, prepared by k_wide_tree
         const uint64_t* src = tsrc + g.v + 1;
         uint64_t* dst = splitters;  // splitters then lut, contiguous as in the pool
-        for (uint32_t i = threadIdx.x; i < g.v + 65; i += kWideThreads) dst[i] = src[i];
+        for (uint32_t i = threadIdx.x; i < g.v + kLutTabWords; i += kWideThreads) dst[i] = src[i];
     }
     for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) hist[b] = 0;
     __syncthreads();
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
     uint16_t* __restrict__ bkt = P.bkt + s.begin;
-    if (!EQUAL) {  // byte-table classification (same buckets, fewer dependent loads)
+    if (!EQUAL) {  // table classification (same buckets, fewer dependent loads)
         LutTree T;
         T.s = splitters;
         T.lut = reinterpret_cast<const uint16_t*>(splitters + g.v);
         T.v = g.v;
-        T.pf = tsrc[2 * g.v + 1 + 65];
-        T.pb = static_cast<uint32_t>(tsrc[2 * g.v + 1 + 66]);
+        T.pf = tsrc[2 * g.v + 1 + kLutTabWords];
+        T.lb = static_cast<uint32_t>(tsrc[2 * g.v + 1 + kLutTabWords + 1]);
         uint64_t nx[4];  // keys of the next round, loaded one round ahead
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -1671,7 +1672,7 @@ __global__ void k_first_unsorted(const uint8_t* __restrict__ arena,
 
 // classify_tree_unrolled / _equal over a key batch: level order built in
 // shared memory from the in-order splitters (_fill_level_order).
-// MODE 0: branch-free descent, 1: equality descent, 2: byte table (k_wide_count)
+// MODE 0: branch-free descent, 1: equality descent, 2: table (k_wide_count)
 template <int MODE>
 __global__ void __launch_bounds__(256) k_classify(const uint64_t* __restrict__ keys, uint64_t n,
                                                   const uint64_t* __restrict__ in_order,
@@ -1688,7 +1689,7 @@ __global__ void __launch_bounds__(256) k_classify(const uint64_t* __restrict__ k
     if (MODE == 2) {
         uint64_t* s = tree + (1u << d);
         uint16_t* lut = reinterpret_cast<uint16_t*>(s + (1u << d));
-        const LutTree T = lut_build<256>(tree, d, s, lut, nullptr);
+        const LutTree T = lut_build<256>(tree, d, s, lut);
         for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
              i += stride)
             out[i] = static_cast<uint16_t>(classify_lut(keys[i], T));
