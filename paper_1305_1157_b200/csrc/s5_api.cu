@@ -19,6 +19,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -209,6 +210,35 @@ int grid_for(uint64_t n, int threads, int max_blocks = 148 * 16) {
 
 // Launch bookkeeping; with cfg flags bit1, CUDA events around every launch
 // give per-kernel device time on the launching stream.
+// Side streams of a device: the size classes of one level work on disjoint
+// segments, so the one-CTA classes run concurrently with each other and
+// with the level's wide step (fork/join by events; the per-kernel profiling
+// mode keeps everything on the caller's stream).
+struct Side {
+    static constexpr int kLanes = 5;
+    cudaStream_t s[kLanes] = {};
+    cudaEvent_t fork = nullptr, join[kLanes] = {};
+    bool ok = false;
+};
+
+Side* side_streams() {
+    static std::mutex mu;
+    static std::map<int, Side> per_device;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    Side& sd = per_device[dev];
+    if (!sd.ok) {
+        bool good = cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; good && i < Side::kLanes; ++i)
+            good = cudaStreamCreateWithFlags(&sd.s[i], cudaStreamNonBlocking) == cudaSuccess &&
+                   cudaEventCreateWithFlags(&sd.join[i], cudaEventDisableTiming) == cudaSuccess;
+        if (!good) return nullptr;
+        sd.ok = true;
+    }
+    return &sd;
+}
+
 struct Prof {
     bool on = false;
     cudaStream_t st = nullptr;
@@ -609,6 +639,15 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         cur ^= 1;
         for (int q = 0; q < NCLS; ++q) A.next[q] = reinterpret_cast<Seg*>(ws + L.lists[cur][q]);
         S5_CUDA(cudaMemsetAsync(A.ctl, 0, offsetof(Ctl, fetches), st));
+        Side* sd = prof.on ? nullptr : side_streams();
+        bool lane_used[Side::kLanes] = {};
+        if (sd) S5_CUDA(cudaEventRecord(sd->fork, st));
+        auto lane = [&](int i) -> cudaStream_t {
+            if (!sd) return st;
+            if (!lane_used[i]) cudaStreamWaitEvent(sd->s[i], sd->fork, 0);
+            lane_used[i] = true;
+            return sd->s[i];
+        };
 
         if (m[WIDE]) {
             P.segs = segs[WIDE];
@@ -654,32 +693,37 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         if (m[LOCAL_XS]) {
             prof.begin(S5_K_LOCAL_XS, h.elems[LOCAL_XS]);
             k_local<kLocalXSThreads>
-                <<<m[LOCAL_XS], kLocalXSThreads, LocalXSCfg::total, st>>>(A, segs[LOCAL_XS]);
+                <<<m[LOCAL_XS], kLocalXSThreads, LocalXSCfg::total, lane(0)>>>(A, segs[LOCAL_XS]);
             prof.end();
         }
         if (m[LOCAL_S]) {
             prof.begin(S5_K_LOCAL_S, h.elems[LOCAL_S]);
             k_local<kLocalSThreads>
-                <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, st>>>(A, segs[LOCAL_S]);
+                <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, lane(1)>>>(A, segs[LOCAL_S]);
             prof.end();
         }
         if (m[LOCAL_M]) {
             prof.begin(S5_K_LOCAL_M, h.elems[LOCAL_M]);
             k_local<kLocalMThreads>
-                <<<m[LOCAL_M], kLocalMThreads, LocalMCfg::total, st>>>(A, segs[LOCAL_M]);
+                <<<m[LOCAL_M], kLocalMThreads, LocalMCfg::total, lane(2)>>>(A, segs[LOCAL_M]);
             prof.end();
         }
         if (m[LOCAL]) {
             prof.begin(S5_K_LOCAL, h.elems[LOCAL]);
             k_local<kLocalThreads>
-                <<<m[LOCAL], kLocalThreads, LocalCfg::total, st>>>(A, segs[LOCAL]);
+                <<<m[LOCAL], kLocalThreads, LocalCfg::total, lane(3)>>>(A, segs[LOCAL]);
             prof.end();
         }
         if (m[SMALL]) {
             uint32_t blocks = (m[SMALL] + 7) / 8;
             prof.begin(S5_K_SMALL, h.elems[SMALL]);
-            k_small<<<blocks, 256, 0, st>>>(A, segs[SMALL], m[SMALL]);
+            k_small<<<blocks, 256, 0, lane(4)>>>(A, segs[SMALL], m[SMALL]);
             prof.end();
+        }
+        for (int i = 0; sd && i < Side::kLanes; ++i) {
+            if (!lane_used[i]) continue;
+            S5_CUDA(cudaEventRecord(sd->join[i], sd->s[i]));
+            S5_CUDA(cudaStreamWaitEvent(st, sd->join[i], 0));
         }
         S5_CUDA(cudaGetLastError());
     }
