@@ -101,7 +101,7 @@ typedef struct {
 enum {
     S5_K_GATHER = 0, S5_K_WIDE_PLAN, S5_K_WIDE_TREE, S5_K_WIDE_COUNT, S5_K_WIDE_COLSCAN,
     S5_K_WIDE_BSCAN, S5_K_WIDE_SCATTER, S5_K_NARROW, S5_K_SMALL, S5_K_LCP_FIX, S5_K_INIT,
-    S5_K_LOCAL, S5_K_LOCAL_S, S5_K_LOCAL_M, S5_K_LOCAL_XS, S5_K_COUNT
+    S5_K_LOCAL, S5_K_LOCAL_S, S5_K_LOCAL_M, S5_K_LOCAL_XS, S5_K_LOCAL_W, S5_K_COUNT
 };
 
 /* Bytes of device workspace s5_sort needs for n strings. */

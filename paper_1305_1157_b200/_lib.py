@@ -89,7 +89,7 @@ class S5Stats(C.Structure):
 
 KERNELS = ["k_gather", "k_wide_plan", "k_wide_tree", "k_wide_count", "k_wide_colscan",
            "k_wide_bscan", "k_wide_scatter", "k_narrow", "k_small", "k_lcp_fix", "k_init_root",
-           "k_local", "k_local_s", "k_local_m", "k_local_xs"]
+           "k_local", "k_local_s", "k_local_m", "k_local_xs", "k_local_w"]
 
 _vp = C.c_void_p
 _u64 = C.c_uint64

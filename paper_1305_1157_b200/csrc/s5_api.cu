@@ -119,7 +119,8 @@ Layout make_layout(uint64_t n, const Cfg& c) {
         return p;
     };
     L.cap[SMALL] = static_cast<uint32_t>(n / 2 + 1);
-    L.cap[LOCAL_XS] = static_cast<uint32_t>(n / (c.small_max + 1) + 1);
+    L.cap[LOCAL_W] = static_cast<uint32_t>(n / (c.small_max + 1) + 1);
+    L.cap[LOCAL_XS] = static_cast<uint32_t>(n / (std::min(c.local_max, kWarpLocalMax) + 1) + 1);
     L.cap[LOCAL_S] = static_cast<uint32_t>(n / (std::min(c.local_max, LocalXSCfg::maxn) + 1) + 1);
     L.cap[LOCAL_M] = static_cast<uint32_t>(n / (std::min(c.local_max, LocalSCfg::maxn) + 1) + 1);
     L.cap[LOCAL] = static_cast<uint32_t>(n / (std::min(c.local_max, LocalMCfg::maxn) + 1) + 1);
@@ -215,7 +216,7 @@ int grid_for(uint64_t n, int threads, int max_blocks = 148 * 16) {
 // with the level's wide step (fork/join by events; the per-kernel profiling
 // mode keeps everything on the caller's stream).
 struct Side {
-    static constexpr int kLanes = 5;
+    static constexpr int kLanes = 6;
     cudaStream_t s[kLanes] = {};
     cudaEvent_t fork = nullptr, join[kLanes] = {};
     bool ok = false;
@@ -541,6 +542,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.ctl = reinterpret_cast<Ctl*>(ws + L.ctl);
     A.small_max = c.small_max;
     A.local_max = c.local_max;
+    A.local_w_max = std::min(c.local_max, kWarpLocalMax);
     A.local_xs_max = std::min(c.local_max, LocalXSCfg::maxn);
     A.local_s_max = std::min(c.local_max, LocalSCfg::maxn);
     A.local_m_max = std::min(c.local_max, LocalMCfg::maxn);
@@ -625,9 +627,9 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             stats->wide_elems[level] = h.elems[WIDE];
             stats->narrow_elems[level] = h.elems[NARROW];
             stats->small_elems[level] = h.elems[SMALL];
-            stats->local_elems[level] =
-                h.elems[LOCAL] + h.elems[LOCAL_S] + h.elems[LOCAL_M] + h.elems[LOCAL_XS];
-            stats->local_steps += m[LOCAL] + m[LOCAL_S] + m[LOCAL_M] + m[LOCAL_XS];
+            stats->local_elems[level] = h.elems[LOCAL] + h.elems[LOCAL_S] + h.elems[LOCAL_M] +
+                                        h.elems[LOCAL_XS] + h.elems[LOCAL_W];
+            stats->local_steps += m[LOCAL] + m[LOCAL_S] + m[LOCAL_M] + m[LOCAL_XS] + m[LOCAL_W];
             stats->n_per_pass[level] = live_elems;
             stats->wide_steps += m[WIDE];
             stats->narrow_steps += m[NARROW];
@@ -688,6 +690,12 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
                 k_narrow<true><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
             else
                 k_narrow<false><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
+            prof.end();
+        }
+        if (m[LOCAL_W]) {
+            prof.begin(S5_K_LOCAL_W, h.elems[LOCAL_W]);
+            k_local_w<<<(m[LOCAL_W] + kWarpLocalWarps - 1) / kWarpLocalWarps, kWarpLocalWarps * 32, 0,
+                        lane(5)>>>(A, segs[LOCAL_W], m[LOCAL_W]);
             prof.end();
         }
         if (m[LOCAL_XS]) {

@@ -42,7 +42,7 @@ struct Ctl {
 
 enum : uint32_t { ERR_RANGE = 1, ERR_LIST = 2, ERR_POOL = 4 };
 enum : int { WIDE = 0, NARROW = 1, SMALL = 2, LOCAL = 3, LOCAL_S = 4, LOCAL_M = 5, LOCAL_XS = 6,
-              NCLS = 7 };
+              LOCAL_W = 7, NCLS = 8 };
 
 struct SortArgs {
     const uint8_t* arena;
@@ -55,7 +55,7 @@ struct SortArgs {
     Seg* next[NCLS];
     uint32_t cap[NCLS];
     Ctl* ctl;
-    uint32_t small_max, local_xs_max, local_s_max, local_m_max, local_max, narrow_max;
+    uint32_t small_max, local_w_max, local_xs_max, local_s_max, local_m_max, local_max, narrow_max;
     uint32_t dmax;         // log2(cfg.v + 1)
     uint32_t wide_dcap;    // wide steps use d <= wide_dcap (<= kWideDMax)
     uint32_t wide_target;  // wide steps aim at children of about this size
@@ -101,6 +101,7 @@ __host__ __device__ __forceinline__ uint32_t choose_d(uint32_t size, uint32_t dm
 
 __device__ __forceinline__ int size_class(const SortArgs& A, uint32_t size) {
     return size <= A.small_max     ? SMALL
+         : size <= A.local_w_max   ? LOCAL_W
          : size <= A.local_xs_max  ? LOCAL_XS
          : size <= A.local_s_max   ? LOCAL_S
          : size <= A.local_m_max   ? LOCAL_M
@@ -1201,6 +1202,208 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
             const int cls = size_class(A, g);
             const uint32_t at = es.base[cls] + atomicAdd(&es.cnt[cls], 1u);
             if (at < A.cap[cls]) A.next[cls][at] = Seg{s.begin + r0, g, cdepth, ns};
+        }
+    }
+    for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
+    if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
+}
+
+// Warp tier: one warp finishes a segment of <= 256 strings (8 per lane) with
+// the local tier's algorithm at warp scope -- the sort words are merged in
+// registers (sort8_regs + warp_merge256), so there are no shared-memory sort
+// rounds and no block barriers; 8 segments per CTA.
+constexpr uint32_t kWarpLocalMax = 256;
+constexpr uint32_t kWarpLocalWarps = 8;
+
+struct WarpLocalSmem {
+    uint64_t key1[kWarpLocalMax];
+    uint32_t off1[kWarpLocalMax];
+    uint16_t perm[kWarpLocalMax];
+    uint16_t perm2[kWarpLocalMax];
+    uint32_t bits[kWarpLocalMax / 32 + 1];
+    uint32_t bits2[kWarpLocalMax / 32 + 1];
+    uint32_t ties[kWarpLocalMax / 3 + 1];
+    uint32_t nties;
+};
+
+__global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, const Seg* __restrict__ segs,
+                                                                  uint32_t nsegs) {
+    __shared__ WarpLocalSmem wsm[kWarpLocalWarps];
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t si = blockIdx.x * kWarpLocalWarps + wid;
+    if (si >= nsegs) return;  // warp scope only: no block barriers below
+    WarpLocalSmem& W = wsm[wid];
+    Seg s = segs[si];
+    const uint32_t* __restrict__ goff = A.off[s.side] + s.begin;
+    const uint64_t* __restrict__ gkey = A.key[s.side] + s.begin;
+    uint64_t rk[8];
+    uint32_t ro[8];
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) {
+        const uint32_t i = lane + 32 * j;
+        rk[j] = i < s.size ? gkey[i] : 0;
+        ro[j] = i < s.size ? goff[i] : 0;
+    }
+    unsigned long long fetches = 0;
+    uint32_t L;
+    for (;;) {  // common-prefix skip, as in k_local
+        uint64_t mn = ~0ull, mx = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            if (lane + 32 * j < s.size) {
+                mn = rk[j] < mn ? rk[j] : mn;
+                mx = rk[j] > mx ? rk[j] : mx;
+            }
+        }
+        for (uint32_t x = 16; x > 0; x >>= 1) {
+            const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, x);
+            const uint64_t b = __shfl_xor_sync(0xffffffffu, mx, x);
+            mn = a < mn ? a : mn;
+            mx = b > mx ? b : mx;
+        }
+        if (mn == mx) {
+            if (has_zero_byte(mn)) {  // identical strings
+#pragma unroll
+                for (uint32_t j = 0; j < 8; ++j) {
+                    const uint32_t i = lane + 32 * j;
+                    if (i < s.size) {
+                        A.out[s.begin + i] = ro[j];
+                        if (A.lcp && i + 1 < s.size) A.lcp[s.begin + i] = s.depth + zero_index(mn);
+                    }
+                }
+                L = 9;  // done
+                break;
+            }
+            L = 8;
+        } else {
+            L = diff_bytes(mn, mx);
+        }
+        if ((A.flags & 4) || L < ((A.flags & 8) ? 4u : 8u)) break;
+        s.depth += L;
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            if (lane + 32 * j < s.size) {
+                rk[j] = load_key(A.arena, static_cast<uint64_t>(ro[j]) + s.depth);
+                ++fetches;
+            }
+        }
+    }
+    if (L <= 8) {
+        if (L > 7) L = 7;
+        const bool exact = L >= 2;
+        uint64_t w[8];
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            const uint32_t i = lane + 32 * j;
+            W.key1[i] = rk[j];
+            W.off1[i] = ro[j];
+            w[j] = i < s.size ? (((rk[j] << (8 * L)) & ~0xFFFull) | i) : ~0ull;
+        }
+        sort8_regs(w);
+        warp_merge256(w, lane);
+        // run starts of the sorted words (lane l holds positions 8l..8l+7)
+        const uint64_t prev = __shfl_up_sync(0xffffffffu, w[7], 1);
+        uint32_t fl = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < 8; ++j) {
+            const uint32_t p = 8 * lane + j;
+            const uint64_t pw = j ? w[j - 1] : prev;
+            const bool st = p == 0 || p >= s.size || (w[j] >> 12) != (pw >> 12);
+            fl |= (st ? 1u : 0u) << j;
+            if (p < s.size) W.perm[p] = static_cast<uint16_t>(w[j] & 0xFFFu);
+        }
+        uint32_t word = fl << (8 * (lane & 3));
+        word |= __shfl_xor_sync(0xffffffffu, word, 1);
+        word |= __shfl_xor_sync(0xffffffffu, word, 2);
+        if ((lane & 3) == 0) W.bits[lane >> 2] = word;
+        if (lane == 0) {
+            W.bits[kWarpLocalMax / 32] = 1u;
+            W.nties = 0;
+        }
+        __syncwarp();
+        const uint32_t* rb = W.bits;
+        if (!exact) {  // candidate runs of truncated words: rank by the full keys
+#pragma unroll 1
+            for (uint32_t p = lane; p < s.size; p += 32) {
+                const uint32_t r0 = run_begin(W.bits, p), r1 = run_end(W.bits, p);
+                const uint32_t slot = W.perm[p];
+                uint32_t r = p - r0;
+                if (r1 - r0 >= 2 && r1 - r0 <= kTruncFix) {
+                    const uint64_t k = W.key1[slot];
+                    r = 0;
+#pragma unroll 1
+                    for (uint32_t q = r0; q < r1; ++q) {
+                        const uint64_t y = W.key1[W.perm[q]];
+                        r += (y < k) || (y == k && q < p);
+                    }
+                }
+                W.perm2[r0 + r] = static_cast<uint16_t>(slot);
+            }
+            __syncwarp();
+#pragma unroll 1
+            for (uint32_t p = lane; p < kWarpLocalMax; p += 32) {
+                bool st = true;
+                if (p < s.size) {
+                    const uint32_t slot = W.perm2[p];
+                    st = (W.bits[p >> 5] >> (p & 31)) & 1u;
+                    if (!st && run_end(W.bits, p) - run_begin(W.bits, p) <= kTruncFix)
+                        st = W.key1[slot] != W.key1[W.perm2[p - 1]];
+                }
+                const uint32_t b = __ballot_sync(0xffffffffu, st);
+                if (lane == 0) W.bits2[p >> 5] = b;
+            }
+            __syncwarp();
+            for (uint32_t p = lane; p < s.size; p += 32) W.perm[p] = W.perm2[p];
+            if (lane == 0) W.bits2[kWarpLocalMax / 32] = 1u;
+            __syncwarp();
+            rb = W.bits2;
+        }
+        // per position, as in k_local; children are emitted one by one
+        const uint32_t tmax = A.small_max;
+        const uint32_t ns = s.side ^ 1u;
+        const uint64_t depth = s.depth;
+#pragma unroll 1
+        for (uint32_t p = lane; p < s.size; p += 32) {
+            const uint32_t slot = W.perm[p];
+            const uint64_t k = W.key1[slot];
+            const uint32_t o = W.off1[slot];
+            const uint32_t r0 = run_begin(rb, p), r1 = run_end(rb, p);
+            const uint32_t g = r1 - r0;
+            const bool rexact = exact || g <= kTruncFix;
+            const uint32_t dst = s.begin + p;
+            if (A.lcp && p + 1 == r1 && r1 < s.size)
+                A.lcp[dst] = depth + diff_bytes(k, W.key1[W.perm[r1]]);
+            if (g == 1 || (rexact && has_zero_byte(k))) {
+                A.out[dst] = o;
+                if (A.lcp && p + 1 < r1) A.lcp[dst] = depth + zero_index(k);
+            } else if (g > 2 && g > tmax) {
+                A.off[ns][dst] = o;
+                if (rexact) {
+                    A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + depth + 8);
+                    ++fetches;
+                } else {
+                    A.key[ns][dst] = k;
+                }
+                if (p == r0)
+                    emit_child(A, s.begin + r0, g, static_cast<uint32_t>(depth) + (rexact ? 8u : 0u), ns);
+            } else if (p == r0) {
+                if (g == 2) {
+                    const uint32_t sa = W.perm[p], sb2 = W.perm[p + 1];
+                    uint64_t l;
+                    const int c = walk_compare(A.arena, W.off1[sa], W.off1[sb2], depth + 8, &l, fetches);
+                    if (A.lcp) A.lcp[dst] = l;
+                    A.out[dst] = W.off1[c > 0 ? sb2 : sa];
+                    A.out[dst + 1] = W.off1[c > 0 ? sa : sb2];
+                } else {
+                    W.ties[atomicAdd(&W.nties, 1u)] = r0 | (g << 13);
+                }
+            }
+        }
+        __syncwarp();
+        const uint32_t nt = W.nties;
+        for (uint32_t q = 0; q < nt; ++q) {
+            const uint32_t x = W.ties[q];
+            tie_group_warp(A, s, x & 0x1FFFu, x >> 13, W.off1, W.perm, depth + 8, lane, fetches);
         }
     }
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
