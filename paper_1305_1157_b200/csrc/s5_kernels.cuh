@@ -969,9 +969,10 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     uint32_t* bits2 = bits + N / 32 + 1;
     uint32_t* ties = reinterpret_cast<uint32_t*>(sb);   // run lists reuse the sort buffer
     uint32_t* kids = ties + N;
+    uint16_t* pairs = reinterpret_cast<uint16_t*>(sb) + 3 * N;
     __shared__ EmitScratch es;
     __shared__ uint64_t red[2][32];
-    __shared__ uint32_t nties, nkids;
+    __shared__ uint32_t nties, nkids, npairs;
 
     Seg s = segs[blockIdx.x];
     const uint32_t t = threadIdx.x, lane = t & 31;
@@ -1072,6 +1073,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         bits[N / 32] = 1u;
         nties = 0;
         nkids = 0;
+        npairs = 0;
     }
 #pragma unroll 1
     for (uint32_t p = t; p < N; p += THREADS) {
@@ -1154,19 +1156,23 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
             }
             if (p == r0) kids[atomicAdd(&nkids, 1u)] = r0 | (g << 13) | (rexact ? 1u << 31 : 0u);
         } else if (p == r0) {
-            if (g == 2) {
-                const uint32_t sa = perm[p], sb2 = perm[p + 1];
-                uint64_t l;
-                const int c = walk_compare(A.arena, off1[sa], off1[sb2], depth + 8, &l, fetches);
-                if (A.lcp) A.lcp[dst] = l;
-                A.out[dst] = off1[c > 0 ? sb2 : sa];
-                A.out[dst + 1] = off1[c > 0 ? sa : sb2];
-            } else {
+            if (g == 2)
+                pairs[atomicAdd(&npairs, 1u)] = static_cast<uint16_t>(p);
+            else
                 ties[atomicAdd(&nties, 1u)] = r0 | (g << 13);
-            }
         }
     }
     __syncthreads();
+    // runs of two strings: one direct walk each, spread over all threads
+    const uint32_t np = npairs;
+    for (uint32_t q = t; q < np; q += THREADS) {
+        const uint32_t p = pairs[q], sa = perm[p], sb2 = perm[p + 1];
+        uint64_t l;
+        const int c = walk_compare(A.arena, off1[sa], off1[sb2], depth + 8, &l, fetches);
+        if (A.lcp) A.lcp[s.begin + p] = l;
+        A.out[s.begin + p] = off1[c > 0 ? sb2 : sa];
+        A.out[s.begin + p + 1] = off1[c > 0 ? sa : sb2];
+    }
     // runs of 3..small_max strings: one warp each
     const uint32_t nt = nties, nk = nkids;
     for (uint32_t q = t >> 5; q < nt; q += THREADS / 32) {
@@ -1223,7 +1229,8 @@ struct WarpLocalSmem {
     uint32_t bits[kWarpLocalMax / 32 + 1];
     uint32_t bits2[kWarpLocalMax / 32 + 1];
     uint32_t ties[kWarpLocalMax / 3 + 1];
-    uint32_t nties;
+    uint16_t pairs[kWarpLocalMax / 2];
+    uint32_t nties, npairs;
 };
 
 __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, const Seg* __restrict__ segs,
@@ -1319,6 +1326,7 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
         if (lane == 0) {
             W.bits[kWarpLocalMax / 32] = 1u;
             W.nties = 0;
+            W.npairs = 0;
         }
         __syncwarp();
         const uint32_t* rb = W.bits;
@@ -1387,19 +1395,21 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
                 if (p == r0)
                     emit_child(A, s.begin + r0, g, static_cast<uint32_t>(depth) + (rexact ? 8u : 0u), ns);
             } else if (p == r0) {
-                if (g == 2) {
-                    const uint32_t sa = W.perm[p], sb2 = W.perm[p + 1];
-                    uint64_t l;
-                    const int c = walk_compare(A.arena, W.off1[sa], W.off1[sb2], depth + 8, &l, fetches);
-                    if (A.lcp) A.lcp[dst] = l;
-                    A.out[dst] = W.off1[c > 0 ? sb2 : sa];
-                    A.out[dst + 1] = W.off1[c > 0 ? sa : sb2];
-                } else {
+                if (g == 2)
+                    W.pairs[atomicAdd(&W.npairs, 1u)] = static_cast<uint16_t>(p);
+                else
                     W.ties[atomicAdd(&W.nties, 1u)] = r0 | (g << 13);
-                }
             }
         }
         __syncwarp();
+        for (uint32_t q = lane; q < W.npairs; q += 32) {  // pairs spread over the lanes
+            const uint32_t p = W.pairs[q], sa = W.perm[p], sb2 = W.perm[p + 1];
+            uint64_t l;
+            const int c = walk_compare(A.arena, W.off1[sa], W.off1[sb2], depth + 8, &l, fetches);
+            if (A.lcp) A.lcp[s.begin + p] = l;
+            A.out[s.begin + p] = W.off1[c > 0 ? sb2 : sa];
+            A.out[s.begin + p + 1] = W.off1[c > 0 ? sa : sb2];
+        }
         const uint32_t nt = W.nties;
         for (uint32_t q = 0; q < nt; ++q) {
             const uint32_t x = W.ties[q];
