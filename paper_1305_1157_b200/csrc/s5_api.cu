@@ -575,10 +575,16 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     Prof prof;
     prof.on = stats && (c.flags & 2);
     prof.st = st;
-    prof.begin(S5_K_GATHER, n);
-    k_gather<<<grid_for(n, 256), 256, 0, st>>>(d_handles, static_cast<uint32_t>(n), depth,
-                                                arena_len, A);
-    prof.end();
+    // a wide root (table classifier) gathers its keys inside the level-0 count
+    // kernel; otherwise a separate gather pass
+    A.arena_len = arena_len;
+    const bool fuse_root = !audit && !c.classifier && n > c.narrow_max && !(c.flags & 64);
+    if (!fuse_root) {
+        prof.begin(S5_K_GATHER, n);
+        k_gather<<<grid_for(n, 256), 256, 0, st>>>(d_handles, static_cast<uint32_t>(n), depth,
+                                                    arena_len, A);
+        prof.end();
+    }
     prof.begin(S5_K_INIT);
     k_init_root<<<1, 32, 0, st>>>(A, static_cast<uint32_t>(n), static_cast<uint32_t>(depth));
     prof.end();
@@ -588,6 +594,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     uint32_t level = 0;
     for (;; ++level) {
         prof.level = level;
+        A.root = level == 0 && fuse_root ? d_handles : nullptr;
         S5_CUDA(cudaMemcpyAsync(hp.ctl, A.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         S5_CUDA(cudaStreamSynchronize(st));
         Ctl h = *hp.ctl;

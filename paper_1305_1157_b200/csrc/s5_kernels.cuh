@@ -65,6 +65,8 @@ struct SortArgs {
     uint32_t alpha;
     uint32_t flags;        // s5_config flags (bit2: no common-prefix skip)
     uint64_t seed;
+    const int64_t* root;   // level 0 only: the caller's handles (gather fused into the count)
+    uint64_t arena_len;
 };
 
 constexpr uint32_t kNarrowThreads = 512;
@@ -1538,8 +1540,20 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_tree(SortArgs A, WidePlan
     while (M < m) M <<= 1;
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
     const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
-    for (uint32_t t = threadIdx.x; t < M; t += kWideThreads)
-        sample[t] = t < m ? key[sample_index(sseed, t, s.size)] : ~0ull;
+    for (uint32_t t = threadIdx.x; t < M; t += kWideThreads) {
+        uint64_t x = ~0ull;
+        if (t < m) {
+            const uint32_t idx = sample_index(sseed, t, s.size);
+            if (A.root) {  // level 0: keys are not gathered yet
+                const int64_t h = A.root[s.begin + idx];
+                x = (h >= 0 && static_cast<uint64_t>(h) + s.depth < A.arena_len)
+                        ? load_key(A.arena, static_cast<uint64_t>(h) + s.depth) : 0;
+            } else {
+                x = key[idx];
+            }
+        }
+        sample[t] = x;
+    }
     __syncthreads();
     sort_sample<kWideThreads>(sample, M);
     uint64_t* tree = P.tree_pool + P.tree_off[blockIdx.x];
@@ -1600,6 +1614,43 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
         T.v = g.v;
         T.pf = tsrc[2 * g.v + 1 + kLutTabWords];
         T.lb = static_cast<uint32_t>(tsrc[2 * g.v + 1 + kLutTabWords + 1]);
+        if (A.root) {  // level 0: handle -> (offset, key) gather fused with the count
+            constexpr int R = 8;
+#pragma unroll 1
+            for (uint32_t base = lo; base < hi; base += R * kWideThreads) {
+                int64_t hh[R];
+                uint64_t kk[R];
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    const uint32_t i = base + j * kWideThreads + threadIdx.x;
+                    hh[j] = i < hi ? __ldcs(A.root + s.begin + i) : 0;
+                }
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    const uint32_t i = base + j * kWideThreads + threadIdx.x;
+                    if (i < hi && (hh[j] < 0 || static_cast<uint64_t>(hh[j]) + s.depth >= A.arena_len)) {
+                        atomicOr(&A.ctl->err, ERR_RANGE);
+                        hh[j] = 0;
+                    }
+                    kk[j] = i < hi ? load_key(A.arena, static_cast<uint64_t>(hh[j]) + s.depth) : 0;
+                }
+#pragma unroll
+                for (int j = 0; j < R; ++j) {
+                    const uint32_t i = base + j * kWideThreads + threadIdx.x;
+                    if (i < hi) {
+                        A.off[0][s.begin + i] = static_cast<uint32_t>(hh[j]);
+                        A.key[0][s.begin + i] = kk[j];
+                        const uint32_t b = classify_lut(kk[j], T);
+                        atomicAdd(&hist[b], 1u);
+                        bkt[i] = static_cast<uint16_t>(b);
+                    }
+                }
+            }
+            __syncthreads();
+            uint32_t* row = P.hist_pool + P.hist_off[si] + static_cast<uint64_t>(c) * g.k;
+            for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) row[b] = hist[b];
+            return;
+        }
         uint64_t nx[4];  // keys of the next round, loaded one round ahead
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
