@@ -181,6 +181,7 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_wide_count<false>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_count<true>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_scatter, WideScatterSmem::total);
+        if (!rc) rc = set_smem(k_wide_scatter_tma, WideTmaSmem::bytes(kWideDMax));
         if (!rc) rc = set_smem(k_build_tree, 227 * 1024);
         if (!rc) rc = set_smem(k_local<kLocalThreads>, LocalCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalSThreads>, LocalSCfg::total);
@@ -688,7 +689,13 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             k_wide_bscan<<<m[WIDE], 256, 0, st>>>(A, P);
             prof.end();
             prof.begin(S5_K_WIDE_SCATTER, h.elems[WIDE]);
-            k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::bytes(c.wide_dcap), st>>>(A, P);
+            // few, huge segments (the root level): tiles brought in by the bulk-copy
+            // engine, one tile in flight while the other is written out; many
+            // segments: register-staged tiles at two CTAs per SM
+            if ((c.flags & 32) || m[WIDE] <= 8)
+                k_wide_scatter_tma<<<ub, kTmaThreads, WideTmaSmem::bytes(c.wide_dcap), st>>>(A, P);
+            else
+                k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::bytes(c.wide_dcap), st>>>(A, P);
             prof.end();
         }
         if (m[NARROW]) {

@@ -1863,6 +1863,159 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
     if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
 }
 
+// Variant of the distribution with the tile inputs brought in by the bulk
+// copy engine (cp.async.bulk, completion on an mbarrier): while tile t is
+// ranked and written out, tile t+1 is already in flight into the other
+// stage -- no register staging, no load latency on the critical path.  The
+// write-out reads each string's key and offset straight from the stage
+// through a per-tile position -> element permutation.
+constexpr uint32_t kTmaThreads = 1024;
+constexpr uint32_t kTmaTile = 4096;
+
+struct TmaStage {
+    uint64_t key[kTmaTile + 2];
+    uint32_t off[kTmaTile + 4];
+    uint16_t bkt[kTmaTile + 8];
+};
+
+struct WideTmaSmem {
+    // stages | perm u16[tile] | cur, cnt, gb u32[kc] | warp sums | 2 mbarriers
+    __host__ __device__ static constexpr uint32_t bytes(uint32_t dcap) {
+        return 2 * static_cast<uint32_t>(sizeof(TmaStage)) + kTmaTile * 2 +
+               (3 * (2u << dcap) + 8) * 4 + 64 * 4 + 16;
+    }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte aligned superset of [src, src + bytes) into dst; returns the
+// element shift of src inside the copy
+template <typename T>
+__device__ __forceinline__ uint32_t bulk_in(T* dst, const T* src, uint32_t count, uint64_t* bar,
+                                            uint32_t& tx) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t a16 = a & ~static_cast<uintptr_t>(15);
+    const uint32_t bytes = static_cast<uint32_t>(((a + count * sizeof(T) + 15) & ~static_cast<uintptr_t>(15)) - a16);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        :: "r"(smem_u32(dst)), "l"(a16), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+    tx += bytes;
+    return static_cast<uint32_t>((a - a16) / sizeof(T));
+}
+
+__device__ __forceinline__ uint32_t elem_shift(const void* src, uint32_t size) {
+    return static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) & 15) / size);
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 1) k_wide_scatter_tma(SortArgs A, WidePlan P) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    const uint32_t G = blockIdx.x;
+    if (G >= A.ctl->wide_ctas) return;
+    TmaStage* stage = reinterpret_cast<TmaStage*>(sm);
+    uint16_t* perm = reinterpret_cast<uint16_t*>(sm + 2 * sizeof(TmaStage));
+    const uint32_t kc = 2u << A.wide_dcap;
+    uint32_t* cur = reinterpret_cast<uint32_t*>(perm + kTmaTile);
+    uint32_t* cnt = cur + kc;
+    uint32_t* gb = cnt + kc + 4;
+    uint32_t* warp_sums = gb + kc + 4;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(warp_sums + 64);
+    const uint32_t si = find_seg(P.cta_start, P.nsegs, G);
+    const Seg s = P.segs[si];
+    const WideGeom g = wide_geom(s, A);
+    const uint32_t c = G - P.cta_start[si];
+    const uint32_t chunk = (s.size + g.C - 1) / g.C;
+    const uint32_t lo = c * chunk;
+    const uint32_t hi = min(s.size, lo + chunk);
+    const uint64_t* tree = P.tree_pool + P.tree_off[si];
+    const uint32_t* rows = P.hist_pool + P.hist_off[si];
+    const uint32_t* starts = rows + static_cast<uint64_t>(g.C) * g.k;
+    const uint32_t* __restrict__ off = A.off[s.side] + s.begin;
+    const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
+    const uint16_t* __restrict__ bkt = P.bkt + s.begin;
+    auto issue = [&](uint32_t base, uint32_t buf) {
+        const uint32_t m = min(kTmaTile, hi - base);
+        uint32_t tx = 0;
+        bulk_in(stage[buf].key, key + base, m, &bar[buf], tx);
+        bulk_in(stage[buf].off, off + base, m, &bar[buf], tx);
+        bulk_in(stage[buf].bkt, bkt + base, m, &bar[buf], tx);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                     :: "r"(smem_u32(&bar[buf])), "r"(tx) : "memory");
+    };
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 2; ++q)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_u32(&bar[q])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (uint32_t b = threadIdx.x; b < g.k; b += kTmaThreads) {
+        uint32_t st = starts[b], n_b = starts[b + 1] - st;
+        bool fin = n_b == 1 || ((b & 1) && has_zero_byte(tree[node_of_rank(b >> 1, g.d)]));
+        cur[b] = (st + rows[static_cast<uint64_t>(c) * g.k + b]) | (fin ? 0x80000000u : 0u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (lo < hi) issue(lo, 0);
+        if (lo + kTmaTile < hi) issue(lo + kTmaTile, 1);
+    }
+    constexpr uint32_t IT = kTmaTile / kTmaThreads;
+    unsigned long long fetches = 0;
+    uint32_t t = 0;
+#pragma unroll 1
+    for (uint32_t base = lo; base < hi; base += kTmaTile, ++t) {
+        const uint32_t buf = t & 1;
+        const uint32_t m = min(kTmaTile, hi - base);
+        const uint32_t shk = elem_shift(key + base, 8), sho = elem_shift(off + base, 4),
+                       shb = elem_shift(bkt + base, 2);
+        for (uint32_t b = threadIdx.x; b <= g.k; b += kTmaThreads) cnt[b] = 0;
+        // wait for the tile's bytes
+        asm volatile(
+            "{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            " @!p bra W%=;\n}\n" :: "r"(smem_u32(&bar[buf])), "r"((t >> 1) & 1) : "memory");
+        __syncthreads();
+        const TmaStage& S = stage[buf];
+        uint32_t br[IT];  // bucket | rank-in-tile << 16
+#pragma unroll
+        for (uint32_t j = 0; j < IT; ++j) {
+            const uint32_t e = threadIdx.x + j * kTmaThreads;
+            if (e < m) {
+                const uint32_t b = S.bkt[e + shb];
+                br[j] = b | (atomicAdd(&cnt[b], 1u) << 16);
+            }
+        }
+        __syncthreads();
+        for (uint32_t b = threadIdx.x; b < g.k; b += kTmaThreads) {
+            uint32_t r = cur[b];
+            gb[b] = r;
+            cur[b] = r + cnt[b];
+        }
+        __syncthreads();
+        block_exclusive_scan<kTmaThreads>(cnt, g.k, warp_sums);
+#pragma unroll
+        for (uint32_t j = 0; j < IT; ++j) {
+            const uint32_t e = threadIdx.x + j * kTmaThreads;
+            if (e < m) perm[cnt[br[j] & 0xFFFFu] + (br[j] >> 16)] = static_cast<uint16_t>(e);
+        }
+        __syncthreads();
+        for (uint32_t q = threadIdx.x; q < m; q += kTmaThreads) {
+            const uint32_t e = perm[q];
+            const uint32_t b = S.bkt[e + shb];
+            const uint32_t r = gb[b];
+            const bool fin = r >> 31;
+            const uint32_t p = (r & 0x7FFFFFFFu) + (q - cnt[b]);
+            const uint32_t end = fin && (b & 1) ? starts[b + 1] : 0;
+            place(A, s, b, fin, p, end, S.off[e + sho], S.key[e + shk], fetches);
+        }
+        __syncthreads();  // every read of this stage is done: refill it
+        if (threadIdx.x == 0 && base + 2 * kTmaTile < hi) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(base + 2 * kTmaTile, buf);
+        }
+    }
+    for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
+    if ((threadIdx.x & 31) == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
+}
+
 // ---------------------------------------------------------------------------
 // LCP at bucket boundaries: the two strings differ within the 8-byte window
 // at the recorded depth (they were classified into different buckets).

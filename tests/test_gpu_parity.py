@@ -30,6 +30,9 @@ CONFIGS = {
     "local_only": SampleSortConfig(v=255, local_max=4096, narrow_max=4096, seed=7),
     "no_local": SampleSortConfig(local_max=32, seed=11),
     "local_small8": SampleSortConfig(v=63, small_max=8, local_max=256, narrow_max=1024),
+    # bulk-copy staged scatter at every level; bitonic local sort + separate gather pass
+    "wide_tma": SampleSortConfig(v=255, small_max=32, narrow_max=32, seed=5, flags=32),
+    "bitonic_gather": SampleSortConfig(seed=9, flags=16 | 64),
 }
 
 
