@@ -52,7 +52,7 @@ typedef struct {
     uint32_t small_max;   /* segments <= small_max: warp base case (<= 32)      */
     uint32_t narrow_max;  /* segments <= narrow_max: one-CTA S^5 step (<=16384; 0: 4096 = off) */
     uint32_t flags;       /* bit0: skip LCP fix-up (debug); bit1: per-kernel timing; bit2: no common-prefix
-                           * skip; bit3: partial-prefix skip; bit4: bitonic local sort; bit5: TMA-staged scatter at every level;
+                           * skip; bit3: partial-prefix skip; bit4: bitonic local sort; bit5: TMA-staged scatter at every level; bit7: 2048-tile TMA scatter below the root;
                            * bit6: separate gather pass at level 0 */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/

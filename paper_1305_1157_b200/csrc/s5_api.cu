@@ -181,7 +181,8 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_wide_count<false>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_count<true>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_scatter, WideScatterSmem::total);
-        if (!rc) rc = set_smem(k_wide_scatter_tma, WideTmaSmem::bytes(kWideDMax));
+        if (!rc) rc = set_smem(k_wide_scatter_tma<1024, 4096>, WideTmaSmem<4096>::bytes(kWideDMax));
+        if (!rc) rc = set_smem(k_wide_scatter_tma<512, 2048>, WideTmaSmem<2048>::bytes(kWideDMax));
         if (!rc) rc = set_smem(k_build_tree, 227 * 1024);
         if (!rc) rc = set_smem(k_local<kLocalThreads>, LocalCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalSThreads>, LocalSCfg::total);
@@ -689,11 +690,16 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             k_wide_bscan<<<m[WIDE], 256, 0, st>>>(A, P);
             prof.end();
             prof.begin(S5_K_WIDE_SCATTER, h.elems[WIDE]);
-            // few, huge segments (the root level): tiles brought in by the bulk-copy
-            // engine, one tile in flight while the other is written out; many
-            // segments: register-staged tiles at two CTAs per SM
+            // tiles brought in by the bulk-copy engine (one tile in flight while
+            // the other is written out) for few huge segments (the root: 4096-string
+            // tiles) and for small segments (2048, three CTAs per SM); register-
+            // staged 4096-string tiles at two CTAs per SM in between
             if ((c.flags & 32) || m[WIDE] <= 8)
-                k_wide_scatter_tma<<<ub, kTmaThreads, WideTmaSmem::bytes(c.wide_dcap), st>>>(A, P);
+                k_wide_scatter_tma<1024, 4096>
+                    <<<ub, 1024, WideTmaSmem<4096>::bytes(c.wide_dcap), st>>>(A, P);
+            else if ((c.flags & 128) || h.elems[WIDE] < uint64_t(m[WIDE]) * 32768)  // small segments
+                k_wide_scatter_tma<512, 2048>
+                    <<<ub, 512, WideTmaSmem<2048>::bytes(c.wide_dcap), st>>>(A, P);
             else
                 k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::bytes(c.wide_dcap), st>>>(A, P);
             prof.end();

@@ -1869,19 +1869,18 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
 // stage -- no register staging, no load latency on the critical path.  The
 // write-out reads each string's key and offset straight from the stage
 // through a per-tile position -> element permutation.
-constexpr uint32_t kTmaThreads = 1024;
-constexpr uint32_t kTmaTile = 4096;
-
+template <uint32_t TILE>
 struct TmaStage {
-    uint64_t key[kTmaTile + 2];
-    uint32_t off[kTmaTile + 4];
-    uint16_t bkt[kTmaTile + 8];
+    uint64_t key[TILE + 2];
+    uint32_t off[TILE + 4];
+    uint16_t bkt[TILE + 8];
 };
 
+template <uint32_t TILE>
 struct WideTmaSmem {
     // stages | perm u16[tile] | cur, cnt, gb u32[kc] | warp sums | 2 mbarriers
     __host__ __device__ static constexpr uint32_t bytes(uint32_t dcap) {
-        return 2 * static_cast<uint32_t>(sizeof(TmaStage)) + kTmaTile * 2 +
+        return 2 * static_cast<uint32_t>(sizeof(TmaStage<TILE>)) + TILE * 2 +
                (3 * (2u << dcap) + 8) * 4 + 64 * 4 + 16;
     }
 };
@@ -1909,7 +1908,10 @@ __device__ __forceinline__ uint32_t elem_shift(const void* src, uint32_t size) {
     return static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) & 15) / size);
 }
 
-__global__ void __launch_bounds__(kTmaThreads, 1) k_wide_scatter_tma(SortArgs A, WidePlan P) {
+template <uint32_t THREADS, uint32_t TILE>
+__global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePlan P) {
+    constexpr uint32_t kTmaThreads = THREADS, kTmaTile = TILE;
+    using TmaStage = s5::TmaStage<TILE>;
     extern __shared__ __align__(128) uint8_t sm[];
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;

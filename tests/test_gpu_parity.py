@@ -26,7 +26,7 @@ CONFIGS = {
     "equal": SampleSortConfig(classifier="equal"),
     "tiny_tiers": SampleSortConfig(v=15, small_max=8, narrow_max=64, seed=3),
     "wide_everywhere": SampleSortConfig(v=255, small_max=32, narrow_max=32, seed=5),
-    "alpha8": SampleSortConfig(v=1023, alpha=8, small_max=16, narrow_max=2048),
+    "alpha8": SampleSortConfig(v=1023, alpha=8, small_max=16, narrow_max=2048, flags=128),
     "local_only": SampleSortConfig(v=255, local_max=4096, narrow_max=4096, seed=7),
     "no_local": SampleSortConfig(local_max=32, seed=11),
     "local_small8": SampleSortConfig(v=63, small_max=8, local_max=256, narrow_max=1024),
