@@ -69,7 +69,7 @@ typedef struct {
     uint32_t level;
     uint64_t strings;  /* strings the launch processed */
     float ms;          /* device time (CUDA events on the stream) */
-    float pad_;
+    float start_ms;    /* launch start relative to the call's first event */
 } s5_launch_rec;
 typedef struct {
     uint32_t levels;                     /* level-synchronous passes run          */

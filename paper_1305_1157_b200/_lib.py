@@ -40,7 +40,7 @@ S5_MAX_LAUNCH_RECS = 512
 
 class S5LaunchRec(C.Structure):
     _fields_ = [("kernel", C.c_uint32), ("level", C.c_uint32), ("strings", C.c_uint64),
-                ("ms", C.c_float), ("pad_", C.c_float)]
+                ("ms", C.c_float), ("start_ms", C.c_float)]
 
 
 class S5Stats(C.Structure):
@@ -78,7 +78,8 @@ class S5Stats(C.Structure):
             "host_ms": {"h2d": float(self.host_h2d_ms), "sort": float(self.host_sort_ms),
                         "d2h": float(self.host_d2h_ms)},
             "launch_recs": [(KERNELS[r.kernel] if r.kernel < len(KERNELS) else str(r.kernel),
-                             int(r.level), int(r.strings), round(float(r.ms), 4))
+                             int(r.level), int(r.strings), round(float(r.ms), 4),
+                             round(float(r.start_ms), 4))
                             for r in self.launch_recs[:min(self.n_launch_recs, S5_MAX_LAUNCH_RECS)]],
             "kernels": {KERNELS[i]: {"ms": float(self.kern_ms[i]),
                                      "launches": int(self.kern_launches[i]),

@@ -265,6 +265,7 @@ struct Prof {
     void end() {
         if (on && !recs.empty()) cudaEventRecord(recs.back().b, st);
     }
+    cudaEvent_t origin = nullptr;
     void finish(s5_stats* stats) {
         if (stats) {
             stats->launches = launches;
@@ -275,13 +276,14 @@ struct Prof {
         }
         uint32_t nrec = 0;
         for (auto& r : recs) {
-            float ms = 0;
+            float ms = 0, t0 = 0;
             if (stats && cudaEventSynchronize(r.b) == cudaSuccess &&
                 cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
                 stats->kern_ms[r.k] += ms;
+                if (origin) cudaEventElapsedTime(&t0, origin, r.a);
                 if (nrec < S5_MAX_LAUNCH_RECS)
                     stats->launch_recs[nrec++] = s5_launch_rec{static_cast<uint32_t>(r.k), r.level,
-                                                               r.strings, ms, 0.0f};
+                                                               r.strings, ms, t0};
             }
             cudaEventDestroy(r.a);
             cudaEventDestroy(r.b);
@@ -577,6 +579,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     Prof prof;
     prof.on = stats && (c.flags & 2);
     prof.st = st;
+    prof.origin = ev0;
     // a wide root (table classifier) gathers its keys inside the level-0 count
     // kernel; otherwise a separate gather pass
     A.arena_len = arena_len;
@@ -767,13 +770,13 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         S5_CUDA(cudaEventRecord(ev1, st));
         S5_CUDA(cudaEventSynchronize(ev1));
         S5_CUDA(cudaEventElapsedTime(&stats->ms_total, ev0, ev1));
-        cudaEventDestroy(ev0);
-        cudaEventDestroy(ev1);
         stats->levels = level;
         stats->key_fetches = fetches_total;
         stats->boundary_lcps = hints_total;
     }
     prof.finish(stats);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
     if (stats) stats->n_launch_recs = static_cast<uint32_t>(std::min<size_t>(prof.recs_total, S5_MAX_LAUNCH_RECS));
     return 0;
 }
