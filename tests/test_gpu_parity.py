@@ -165,6 +165,34 @@ def test_partition_kernel_groups_by_full_string_rank():
         at += c
 
 
+@pytest.mark.parametrize("shape", ["identical", "empty", "prefix1000", "binary", "len1", "nested"])
+def test_adversarial_shapes_through_every_tier(shape):
+    # shapes that drive the wide tier's equality buckets, the local tiers'
+    # common-prefix skip, truncated sort words and long tie walks at sizes
+    # above the one-CTA limit
+    from paper_1305_1157_b200 import arena_from_strings
+    rng = np.random.default_rng(17)
+    n = 300_000
+    if shape == "identical":
+        strs = [b"the-same-string-repeated"] * n
+    elif shape == "empty":
+        strs = [b""] * (n // 2) + [b"x"] * (n // 2)
+    elif shape == "prefix1000":
+        base = bytes(rng.integers(97, 123, 1000).tolist())
+        strs = [base + bytes(rng.integers(97, 99, rng.integers(0, 12)).tolist()) for _ in range(n // 10)]
+    elif shape == "binary":
+        strs = [bytes(rng.integers(1, 256, rng.integers(0, 24)).tolist()) for _ in range(n)]
+    elif shape == "len1":
+        strs = [bytes([int(x)]) for x in rng.integers(1, 4, n)]
+    else:  # prefix chains: every string a prefix of the next ones
+        strs = [b"a" * int(k) for k in rng.integers(0, 300, n // 3)]
+    arena, h = arena_from_strings(strs)
+    want = h.copy()
+    O.parallel_sample_sort(arena, want, 8)
+    got, lcp = sort_with_lcp(arena, h.copy())
+    _check_sorted(arena, h, got, want, lcp, O.adjacent_lcps(arena, want), shape)
+
+
 def test_pack_keys_matches_reference():
     from conftest import GOLDEN
     z = np.load(os.path.join(GOLDEN, "pack_keys.npz"))
