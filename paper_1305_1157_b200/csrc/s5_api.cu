@@ -452,7 +452,7 @@ __global__ void k_widen32(const uint32_t* __restrict__ a, int64_t* __restrict__ 
 }
 
 template <typename T>
-__global__ void k_narrow(const int64_t* __restrict__ a, T* __restrict__ b, uint64_t n) {
+__global__ void k_shrink(const int64_t* __restrict__ a, T* __restrict__ b, uint64_t n) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x)
         b[i] = static_cast<T>(a[i]);
@@ -870,7 +870,7 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
     if (rc) return rc;
 
     // D2H: narrow on the device, DMA, widen into the caller's arrays
-    k_narrow<uint32_t><<<grid_for(n, 256), 256, 0, st>>>(dh, d32, n);
+    k_shrink<uint32_t><<<grid_for(n, 256), 256, 0, st>>>(dh, d32, n);
     uint32_t w = 8;
     if (h_lcp) {
         S5_CUDA(cudaMemsetAsync(H.dmax, 0, sizeof(unsigned long long), st));
@@ -880,9 +880,9 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
         const unsigned long long mx = *H.hmax;
         w = mx <= 0xFFull ? 1 : mx <= 0xFFFFull ? 2 : mx <= 0xFFFFFFFFull ? 4 : 8;
         const int g = grid_for(n - 1, 256);
-        if (w == 1) k_narrow<uint8_t><<<g, 256, 0, st>>>(dl, static_cast<uint8_t*>(dn), n - 1);
-        if (w == 2) k_narrow<uint16_t><<<g, 256, 0, st>>>(dl, static_cast<uint16_t*>(dn), n - 1);
-        if (w == 4) k_narrow<uint32_t><<<g, 256, 0, st>>>(dl, static_cast<uint32_t*>(dn), n - 1);
+        if (w == 1) k_shrink<uint8_t><<<g, 256, 0, st>>>(dl, static_cast<uint8_t*>(dn), n - 1);
+        if (w == 2) k_shrink<uint16_t><<<g, 256, 0, st>>>(dl, static_cast<uint16_t*>(dn), n - 1);
+        if (w == 4) k_shrink<uint32_t><<<g, 256, 0, st>>>(dl, static_cast<uint32_t*>(dn), n - 1);
     }
     S5_CUDA(cudaGetLastError());
     S5_CUDA(cudaStreamSynchronize(st));
