@@ -990,6 +990,13 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         rk[j] = i < s.size ? gkey[i] : 0;
         ro[j] = i < s.size ? goff[i] : 0;
     }
+    // keys and offsets by slot; the min/max reduction's barrier publishes them
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) {
+        uint32_t i = t + j * THREADS;
+        key1[i] = rk[j];
+        off1[i] = ro[j];
+    }
     // common prefix of the segment's keys; whole equal words advance the
     // depth in-CTA (the equality-bucket chain of long shared prefixes,
     // classifier.py:297-303, without a level per 8 bytes); all-identical
@@ -1033,6 +1040,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         for (uint32_t j = 0; j < 8; ++j) {
             if (t + j * THREADS < s.size) {
                 rk[j] = load_key(A.arena, static_cast<uint64_t>(ro[j]) + s.depth);
+                key1[t + j * THREADS] = rk[j];
                 ++fetches;
             }
         }
@@ -1044,12 +1052,6 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     // are only candidate ties, resolved from the segment depth
     const bool exact = L >= 2;
     uint64_t w[8];
-#pragma unroll
-    for (uint32_t j = 0; j < 8; ++j) {
-        uint32_t i = t + j * THREADS;
-        key1[i] = rk[j];
-        off1[i] = ro[j];
-    }
     if (A.flags & 16) {  // power-of-two bitonic network over the whole CTA
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j) {
@@ -1058,8 +1060,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         }
         block_sort8<THREADS>(w, sb);
     } else {  // merge sort of the live positions (slot i at position i)
-        __syncthreads();
-        load8(key1, 8 * t, w);
+        load8(key1, 8 * t, w);  // key1 published by the last min/max barrier
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j) {
             const uint32_t i = 8 * t + j;
