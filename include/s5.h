@@ -163,6 +163,30 @@ int s5_partition(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_ha
                  uint64_t n, const int64_t *d_splitters, uint32_t nsplit, int64_t *d_out,
                  uint64_t *h_counts, void *stream);
 
+/* load_lines (harness.py:72-95) on the device: d_raw[len] (one string per
+ * line) -> d_arena (newlines become terminators; a terminator is appended
+ * when the last line has none; capacity len + 1 + S5_ARENA_PAD, pad zeroed by
+ * the caller) and d_handles (string starts, capacity len + 2).  Results in
+ * host memory: *h_n strings, *h_arena_len bytes.  An input byte 0 is the
+ * reference's EmbeddedNul (harness.py:36-39, :75-79): S5_E_INVALID with its
+ * offset in *h_nul_offset. */
+int s5_ingest_lines(const uint8_t *d_raw, uint64_t len, uint8_t *d_arena, int64_t *d_handles,
+                    uint64_t *h_n, uint64_t *h_arena_len, int64_t *h_nul_offset, void *stream);
+
+/* _string_lengths (strings.py:85-96): distance from each handle to the next
+ * terminator (ordered compaction of the arena's terminators + binary search). */
+int s5_string_lengths(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_handles,
+                      uint64_t n, int64_t *d_len, void *stream);
+
+/* Sorted-string materialisation (tests/helpers.py:62-68 strings_of; SURVEY
+ * 8(f) #4): the strings of d_sorted gathered in order into d_out (each with
+ * its terminator), their new handles in d_out_handles[n].  *h_out_len gets
+ * the bytes needed; S5_E_WORKSPACE if they exceed out_cap (call with
+ * out_cap = 0 to size the buffer). */
+int s5_materialize(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_sorted, uint64_t n,
+                   uint8_t *d_out, uint64_t out_cap, int64_t *d_out_handles, uint64_t *h_out_len,
+                   void *stream);
+
 /* classify_tree_unrolled / classify_tree_equal (classifier.py:259-278):
  * buckets of n keys against v = 2^d-1 sorted splitters (in-order).
  * classifier: 0 branch-free descent, 1 equality descent, 2 12-bit table + binary

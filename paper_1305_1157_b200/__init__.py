@@ -10,15 +10,17 @@ executed by hand-written sm_100a kernels in ``libs5.so`` through a C-ABI
 from .counters import Counters
 from .samplesort import (SampleSortConfig, gpu_sort, parallel_sample_sort, sample_sort,
                          sort_with_lcp)
-from .strings import (DatasetStats, EmptyInput, StringArena, VerifyResult, WORD_CHARS,
-                      adjacent_lcps, arena_from_strings, compute_stats, distinguishing_prefix,
-                      extract_key, first_unsorted, lcp, pack_keys, string_lengths,
+from .strings import (DatasetStats, EmbeddedNul, EmptyInput, StringArena, VerifyResult,
+                      WORD_CHARS, adjacent_lcps, arena_from_strings, compute_stats,
+                      distinguishing_prefix, extract_key, first_unsorted, ingest_lines, lcp,
+                      load_lines, materialize, pack_keys, string_lengths,
                       verify_sorted_permutation)
 
 __all__ = [
-    "Counters", "DatasetStats", "EmptyInput", "SampleSortConfig", "StringArena",
+    "Counters", "DatasetStats", "EmbeddedNul", "EmptyInput", "SampleSortConfig", "StringArena",
     "VerifyResult", "WORD_CHARS", "adjacent_lcps", "arena_from_strings", "compute_stats",
-    "distinguishing_prefix", "extract_key", "first_unsorted", "gpu_sort", "lcp", "pack_keys",
+    "distinguishing_prefix", "extract_key", "first_unsorted", "gpu_sort", "ingest_lines", "lcp",
+    "load_lines", "materialize", "pack_keys",
     "parallel_sample_sort", "sample_sort", "sort_with_lcp", "string_lengths",
     "verify_sorted_permutation",
 ]

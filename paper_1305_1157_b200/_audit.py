@@ -27,7 +27,7 @@ def audited_sort(arena, handles, depth, cfg, counters, audit, lcp_out):
     d_h = handles if on_device else torch.from_numpy(np.ascontiguousarray(handles)).to(dev)
     d_lcp = torch.empty(n - 1, dtype=torch.int64, device=dev) if lcp_out is not None else None
     c = cfg.to_c()
-    need = int(_lib.lib().s5_workspace_bytes(n, arena.data.size, C.byref(c)))
+    need = int(_lib.lib().s5_workspace_bytes(n, arena.size, C.byref(c)))
     ws = _workspace(need, dev)
     errors = []
 
@@ -43,7 +43,7 @@ def audited_sort(arena, handles, depth, cfg, counters, audit, lcp_out):
 
     fn = _lib.AUDIT_FN(cb)
     st = _lib.S5Stats()
-    rc = _lib.lib().s5_sort_audit(arena.device(dev).data_ptr(), arena.data.size, d_h.data_ptr(), n,
+    rc = _lib.lib().s5_sort_audit(arena.device(dev).data_ptr(), arena.size, d_h.data_ptr(), n,
                                   int(depth), d_lcp.data_ptr() if d_lcp is not None else None,
                                   C.byref(c), ws.data_ptr(), ws.numel(), _lib.current_stream_ptr(),
                                   C.byref(st), fn, None)

@@ -1018,6 +1018,153 @@ int s5_partition(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_ha
     return 0;
 }
 
+namespace {
+struct AuxScratch {
+    std::mutex mu;
+    void* d = nullptr;
+    uint64_t bytes = 0;
+    unsigned long long* h = nullptr;  // pinned: two results
+};
+AuxScratch& aux() {
+    static AuxScratch a;
+    return a;
+}
+int aux_reserve(AuxScratch& X, uint64_t bytes) {
+    if (!X.h) S5_CUDA(cudaHostAlloc(&X.h, 16, cudaHostAllocDefault));
+    if (bytes <= X.bytes) return 0;
+    if (X.d) cudaFree(X.d);
+    X.d = nullptr;
+    X.bytes = 0;
+    S5_CUDA(cudaMalloc(&X.d, bytes));
+    X.bytes = bytes;
+    return 0;
+}
+// ordered zero positions of a[0, len) (+ shift) into pos; returns their count
+int zero_positions(const uint8_t* a, uint64_t len, int64_t* pos, int64_t shift, char* scratch,
+                   unsigned long long* h_tmp, cudaStream_t st, uint64_t* count) {
+    const uint64_t blocks = (len + kScanChunk - 1) / kScanChunk;
+    auto* counts = reinterpret_cast<uint32_t*>(scratch);
+    auto* base = reinterpret_cast<unsigned long long*>(scratch + align_up(blocks * 4));
+    k_term_count<1><<<blocks, kScanThreads, 0, st>>>(a, nullptr, len, counts, nullptr);
+    k_scan_small<uint32_t><<<1, 1024, 0, st>>>(counts, blocks, base);
+    k_term_write<<<blocks, kScanThreads, 0, st>>>(a, len, base, pos, shift);
+    S5_CUDA(cudaGetLastError());
+    S5_CUDA(cudaMemcpyAsync(h_tmp, base + blocks, 8, cudaMemcpyDeviceToHost, st));
+    S5_CUDA(cudaStreamSynchronize(st));
+    *count = *h_tmp;
+    return 0;
+}
+uint64_t zero_scratch_bytes(uint64_t len) {
+    const uint64_t blocks = (len + kScanChunk - 1) / kScanChunk;
+    return align_up(blocks * 4) + align_up((blocks + 1) * 8);
+}
+}  // namespace
+
+int s5_ingest_lines(const uint8_t* d_raw, uint64_t len, uint8_t* d_arena, int64_t* d_handles,
+                    uint64_t* h_n, uint64_t* h_arena_len, int64_t* h_nul_offset, void* stream) {
+    if (!h_n || !h_arena_len || !h_nul_offset) return fail(S5_E_INVALID, "null result pointer");
+    *h_n = 0;
+    *h_arena_len = 0;
+    *h_nul_offset = -1;
+    if (len == 0) return 0;
+    if (len >= 0xFFFFFFFFull) return fail(S5_E_RANGE, "input of %llu bytes: offsets are 32-bit",
+                                         static_cast<unsigned long long>(len));
+    AuxScratch& X = aux();
+    std::lock_guard<std::mutex> lock(X.mu);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t blocks = (len + kScanChunk - 1) / kScanChunk;
+    if (int rc = aux_reserve(X, zero_scratch_bytes(len) + 16)) return rc;
+    char* scratch = static_cast<char*>(X.d);
+    auto* counts = reinterpret_cast<uint32_t*>(scratch);
+    auto* base = reinterpret_cast<unsigned long long*>(scratch + align_up(blocks * 4));
+    auto* nul = reinterpret_cast<unsigned long long*>(scratch + zero_scratch_bytes(len));
+    S5_CUDA(cudaMemsetAsync(nul, 0xFF, 8, st));
+    // newlines -> terminators, counted per CTA; the first embedded 0 recorded
+    k_term_count<0><<<blocks, kScanThreads, 0, st>>>(d_raw, d_arena, len, counts, nul);
+    k_scan_small<uint32_t><<<1, 1024, 0, st>>>(counts, blocks, base);
+    // string k+1 starts right after terminator k; string 0 at offset 0
+    S5_CUDA(cudaMemsetAsync(d_handles, 0, 8, st));
+    k_term_write<<<blocks, kScanThreads, 0, st>>>(d_arena, len, base, d_handles + 1, 1);
+    S5_CUDA(cudaGetLastError());
+    S5_CUDA(cudaMemcpyAsync(X.h, nul, 8, cudaMemcpyDeviceToHost, st));
+    S5_CUDA(cudaMemcpyAsync(X.h + 1, base + blocks, 8, cudaMemcpyDeviceToHost, st));
+    uint8_t last = 0;
+    S5_CUDA(cudaMemcpyAsync(&last, d_raw + len - 1, 1, cudaMemcpyDeviceToHost, st));
+    S5_CUDA(cudaStreamSynchronize(st));
+    if (X.h[0] != ~0ull) {
+        *h_nul_offset = static_cast<int64_t>(X.h[0]);
+        return fail(S5_E_INVALID, "input contains byte 0 at offset %llu", X.h[0]);
+    }
+    uint64_t nterm = X.h[1];
+    uint64_t alen = len;
+    if (last != '\n') {  // the last line has no newline: append its terminator
+        S5_CUDA(cudaMemsetAsync(d_arena + len, 0, 1, st));
+        ++nterm;
+        ++alen;
+    }
+    S5_CUDA(cudaStreamSynchronize(st));
+    *h_n = nterm;
+    *h_arena_len = alen;
+    return 0;
+}
+
+int s5_string_lengths(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_handles,
+                      uint64_t n, int64_t* d_len, void* stream) {
+    if (n == 0) return 0;
+    AuxScratch& X = aux();
+    std::lock_guard<std::mutex> lock(X.mu);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t zs = zero_scratch_bytes(arena_len);
+    // zero positions: at most one per arena byte
+    if (int rc = aux_reserve(X, zs + align_up(arena_len * 8))) return rc;
+    char* scratch = static_cast<char*>(X.d);
+    auto* pos = reinterpret_cast<int64_t*>(scratch + zs);
+    uint64_t z = 0;
+    if (int rc = zero_positions(d_arena, arena_len, pos, 0, scratch, X.h, st, &z)) return rc;
+    k_lengths<<<grid_for(n, 256), 256, 0, st>>>(d_handles, n, pos, z, d_len);
+    S5_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int s5_materialize(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_sorted, uint64_t n,
+                   uint8_t* d_out, uint64_t out_cap, int64_t* d_out_handles, uint64_t* h_out_len,
+                   void* stream) {
+    if (!h_out_len) return fail(S5_E_INVALID, "null result pointer");
+    *h_out_len = 0;
+    if (n == 0) return 0;
+    AuxScratch& X = aux();
+    std::lock_guard<std::mutex> lock(X.mu);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const uint64_t zs = zero_scratch_bytes(arena_len);
+    const uint64_t nb = (n + 1023) / 1024;
+    const uint64_t need = zs + align_up(arena_len * 8) + align_up(n * 8) + align_up(nb * 8) +
+                          align_up((nb + 1) * 8);
+    if (int rc = aux_reserve(X, need)) return rc;
+    char* scratch = static_cast<char*>(X.d);
+    auto* pos = reinterpret_cast<int64_t*>(scratch + zs);
+    auto* len = reinterpret_cast<int64_t*>(scratch + zs + align_up(arena_len * 8));
+    auto* tot = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(len) + align_up(n * 8));
+    auto* bb = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(tot) + align_up(nb * 8));
+    uint64_t z = 0;
+    if (int rc = zero_positions(d_arena, arena_len, pos, 0, scratch, X.h, st, &z)) return rc;
+    k_lengths<<<grid_for(n, 256), 256, 0, st>>>(d_sorted, n, pos, z, len);
+    // exclusive prefix of (length + 1): the new handles
+    k_scan_len_block<<<nb, 1024, 0, st>>>(len, n, d_out_handles, tot);
+    k_scan_small<unsigned long long><<<1, 1024, 0, st>>>(tot, nb, bb);
+    k_scan_len_add<<<grid_for(n, 256), 256, 0, st>>>(d_out_handles, n, bb);
+    S5_CUDA(cudaGetLastError());
+    S5_CUDA(cudaMemcpyAsync(X.h, bb + nb, 8, cudaMemcpyDeviceToHost, st));
+    S5_CUDA(cudaStreamSynchronize(st));
+    *h_out_len = X.h[0];
+    if (X.h[0] > out_cap)
+        return fail(S5_E_WORKSPACE, "output of %llu bytes, capacity %llu", X.h[0],
+                    static_cast<unsigned long long>(out_cap));
+    k_gather_strings<<<grid_for(n * 32, 256), 256, 0, st>>>(d_arena, d_sorted, len, d_out_handles, n,
+                                                            d_out);
+    S5_CUDA(cudaGetLastError());
+    return 0;
+}
+
 int s5_classify(const uint64_t* d_keys, uint64_t n, const uint64_t* d_in_order, uint32_t v,
                 uint32_t classifier, uint16_t* d_buckets, void* stream) {
     uint32_t d = 0;

@@ -2236,4 +2236,173 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// the path's neighbours: line ingest (harness.py:72-95),
+// string lengths (strings.py:85-96) and sorted-string materialisation
+// (tests/helpers.py:62-68), all built on one ordered compaction of
+// terminator positions.
+
+constexpr uint32_t kScanThreads = 256;
+constexpr uint32_t kScanChunk = 16384;  // bytes per CTA, 64 per thread
+
+// ingest: raw bytes -> arena (newline -> 0), terminators counted per CTA,
+// first embedded 0 byte recorded; mode 0 = ingest (copy + convert),
+// mode 1 = count zeros of an existing arena
+template <int MODE>
+__global__ void __launch_bounds__(kScanThreads) k_term_count(
+        const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t len,
+        uint32_t* __restrict__ counts, unsigned long long* __restrict__ first_nul) {
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanChunk;
+    const uint64_t lo = base + threadIdx.x * (kScanChunk / kScanThreads);
+    const uint64_t hi = min(len, lo + kScanChunk / kScanThreads);
+    uint32_t c = 0;
+    for (uint64_t i = lo; i < hi; ++i) {
+        uint8_t x = src[i];
+        if (MODE == 0) {
+            if (x == 0) atomicMin(first_nul, static_cast<unsigned long long>(i));
+            if (x == '\n') x = 0;
+            dst[i] = x;
+        }
+        c += x == 0;
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    __shared__ uint32_t ws[kScanThreads / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (uint32_t w = 0; w < kScanThreads / 32; ++w) t += ws[w];
+        counts[blockIdx.x] = t;
+    }
+}
+
+// exclusive scan of n values in one CTA (widened to u64); out[n] = total
+template <typename T>
+__global__ void __launch_bounds__(1024) k_scan_small(const T* __restrict__ in, uint64_t n,
+                                                     unsigned long long* __restrict__ out) {
+    __shared__ unsigned long long ws[32], carry;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint64_t b = 0; b < n; b += 1024) {
+        const uint64_t i = b + threadIdx.x;
+        const unsigned long long x = i < n ? static_cast<unsigned long long>(in[i]) : 0;
+        unsigned long long v = x;
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        if (lane == 31) ws[w] = v;
+        __syncthreads();
+        if (w == 0) {
+            unsigned long long y = ws[lane];
+            for (uint32_t o = 1; o < 32; o <<= 1) {
+                const unsigned long long z = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y += z;
+            }
+            ws[lane] = y;
+        }
+        __syncthreads();
+        const unsigned long long excl = carry + v - x + (w ? ws[w - 1] : 0ull);
+        if (i < n) out[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = excl + x;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[n] = carry;
+}
+
+// ordered positions of the zero bytes of a[0, len): pos[k] = (k-th zero) + shift
+__global__ void __launch_bounds__(kScanThreads) k_term_write(
+        const uint8_t* __restrict__ a, uint64_t len, const unsigned long long* __restrict__ block_base,
+        int64_t* __restrict__ pos, int64_t shift) {
+    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanChunk;
+    const uint64_t lo = base + threadIdx.x * (kScanChunk / kScanThreads);
+    const uint64_t hi = min(len, lo + kScanChunk / kScanThreads);
+    uint32_t c = 0;
+    for (uint64_t i = lo; i < hi; ++i) c += a[i] == 0;
+    // exclusive prefix of the thread counts in position order
+    uint32_t incl = c;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    __shared__ uint32_t ws[kScanThreads / 32];
+    if (lane == 31) ws[w] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (uint32_t q = 0; q < w; ++q) before += ws[q];
+    unsigned long long k = block_base[blockIdx.x] + before + incl - c;
+    for (uint64_t i = lo; i < hi; ++i)
+        if (a[i] == 0) pos[k++] = static_cast<int64_t>(i) + shift;
+}
+
+// length of every string: distance to the first terminator at or after it
+__global__ void k_lengths(const int64_t* __restrict__ h, uint64_t n, const int64_t* __restrict__ term,
+                          uint64_t nterm, int64_t* __restrict__ len) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const int64_t x = h[i];
+        uint64_t lo = 0, hi = nterm;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (term[mid] < x) lo = mid + 1; else hi = mid;
+        }
+        len[i] = (lo < nterm ? term[lo] : x) - x;
+    }
+}
+
+// exclusive scan of (len + 1) over n strings (block-local pass + totals)
+__global__ void __launch_bounds__(1024) k_scan_len_block(const int64_t* __restrict__ len, uint64_t n,
+                                                         int64_t* __restrict__ out,
+                                                         unsigned long long* __restrict__ block_tot) {
+    // block totals may exceed 32 bits only for > 4 GiB outputs (rejected on the host)
+    __shared__ unsigned long long ws[32];
+    const uint64_t i = blockIdx.x * 1024ull + threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned long long x = i < n ? static_cast<unsigned long long>(len[i]) + 1 : 0;
+    unsigned long long v = x;
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) ws[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        unsigned long long y = ws[lane];
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const unsigned long long z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z;
+        }
+        ws[lane] = y;
+    }
+    __syncthreads();
+    if (i < n) out[i] = static_cast<int64_t>(v - x + (w ? ws[w - 1] : 0ull));
+    if (threadIdx.x == 1023) block_tot[blockIdx.x] = ws[31];
+}
+
+__global__ void k_scan_len_add(int64_t* __restrict__ out, uint64_t n,
+                               const unsigned long long* __restrict__ block_base) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] += static_cast<int64_t>(block_base[i >> 10]);
+}
+
+// one warp per string: its bytes and terminator to the new arena
+__global__ void __launch_bounds__(256) k_gather_strings(const uint8_t* __restrict__ arena,
+                                                        const int64_t* __restrict__ h,
+                                                        const int64_t* __restrict__ len,
+                                                        const int64_t* __restrict__ dst, uint64_t n,
+                                                        uint8_t* __restrict__ out) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint64_t i = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5; i < n;
+         i += (uint64_t(gridDim.x) * blockDim.x) >> 5) {
+        const uint64_t a = static_cast<uint64_t>(h[i]), b = static_cast<uint64_t>(dst[i]);
+        const uint64_t L = static_cast<uint64_t>(len[i]) + 1;
+        for (uint64_t j = lane; j < L; j += 32) out[b + j] = j + 1 < L ? arena[a + j] : 0;
+    }
+}
+
 }  // namespace s5

@@ -66,7 +66,7 @@ class GpuBackend:
         out = torch.empty_like(handles)
         counts = (C.c_uint64 * (ns + 1))()
         rc = _lib.lib().s5_partition(self.arena.device(self.device).data_ptr(),
-                                     self.arena.data.size, handles.data_ptr(), n,
+                                     self.arena.size, handles.data_ptr(), n,
                                      splitters.contiguous().data_ptr(), ns, out.data_ptr(), counts,
                                      _lib.current_stream_ptr())
         _lib.check(rc, "s5_partition")
@@ -79,7 +79,7 @@ class GpuBackend:
         from . import _lib
         out = torch.empty(1, dtype=torch.int64, device=pair.device)
         rc = _lib.lib().s5_adjacent_lcp(self.arena.device(self.device).data_ptr(),
-                                        self.arena.data.size, pair.contiguous().data_ptr(), 2,
+                                        self.arena.size, pair.contiguous().data_ptr(), 2,
                                         out.data_ptr(), _lib.current_stream_ptr())
         _lib.check(rc, "s5_adjacent_lcp")
         self.launches += 1

@@ -111,7 +111,7 @@ def gpu_sort(arena: StringArena, d_handles, depth: int = 0, cfg: SampleSortConfi
     dev = d_handles.device
     arena_dev = arena.device(dev)
     c = cfg.to_c()
-    need = int(_lib.lib().s5_workspace_bytes(n, arena.data.size, C.byref(c)))
+    need = int(_lib.lib().s5_workspace_bytes(n, arena.size, C.byref(c)))
     if need == 0:
         _lib.check(-1, "s5_workspace_bytes")
     ws = _workspace(need, dev)
@@ -120,7 +120,7 @@ def gpu_sort(arena: StringArena, d_handles, depth: int = 0, cfg: SampleSortConfi
     st = stats if stats is not None else _lib.S5Stats()
     with torch.cuda.device(dev):
         rc = _lib.lib().s5_sort(
-            arena_dev.data_ptr(), arena.data.size, d_handles.data_ptr(), n, int(depth),
+            arena_dev.data_ptr(), arena.size, d_handles.data_ptr(), n, int(depth),
             d_lcp.data_ptr() if d_lcp is not None else None, C.byref(c), ws.data_ptr(),
             ws.numel(), _lib.current_stream_ptr(), C.byref(st))
     _lib.check(rc, "s5_sort")
@@ -185,7 +185,7 @@ def _sort_host(arena, handles, depth, cfg, counters, lcp_out, dev):
     st = _lib.S5Stats()
     with torch.cuda.device(dev):
         arena_dev = arena.device(dev)
-        rc = _lib.lib().s5_sort_host(arena_dev.data_ptr(), arena.data.size, h.ctypes.data, n,
+        rc = _lib.lib().s5_sort_host(arena_dev.data_ptr(), arena.size, h.ctypes.data, n,
                                      int(depth), lcp_buf.ctypes.data if lcp_buf is not None
                                      else None, C.byref(c), _lib.current_stream_ptr(),
                                      C.byref(st))

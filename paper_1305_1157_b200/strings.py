@@ -35,15 +35,38 @@ class StringArena:
     ``torch.uint8`` CUDA tensor), uploaded on first use.
     """
 
-    __slots__ = ("data", "_dev", "_dev_key")
+    __slots__ = ("_data", "_size", "_dev", "_dev_key")
 
     def __init__(self, data):
         data = np.ascontiguousarray(data, dtype=np.uint8)
         if data.size and data[-1] != 0:
             raise ValueError("arena must end with a terminator byte")
-        self.data = data
+        self._data = data
+        self._size = int(data.size)
         self._dev = None
         self._dev_key = None
+
+    @classmethod
+    def from_device(cls, buf, size: int):
+        """An arena born in HBM (``ingest_lines``, ``materialize``): ``buf`` is
+        the padded CUDA mirror; ``data`` is downloaded on first access."""
+        obj = cls.__new__(cls)
+        obj._data = None
+        obj._size = int(size)
+        obj._dev = buf
+        obj._dev_key = ("born", str(buf.device))
+        return obj
+
+    @property
+    def data(self):
+        if self._data is None:
+            self._data = self._dev[: self._size].cpu().numpy()
+        return self._data
+
+    @property
+    def size(self) -> int:
+        """Arena bytes (without the device pad)."""
+        return self._size
 
     @property
     def sigma(self) -> int:
@@ -60,7 +83,7 @@ class StringArena:
         return int(np.argmax(self.data[handle:] == 0))
 
     def __len__(self):
-        return self.data.size
+        return self._size
 
     def device(self, device=None):
         """Padded device mirror of the arena (uploaded once, then cached)."""
@@ -68,16 +91,24 @@ class StringArena:
         dev = torch.device(device if device is not None else "cuda")
         if dev.type == "cuda" and dev.index is None:
             dev = torch.device("cuda", torch.cuda.current_device())
+        if self._dev_key is not None and self._dev_key[0] == "born":
+            if self._dev_key[1] == str(dev):
+                return self._dev
+            self.data  # noqa: B018 -- host copy, then a mirror on the other device
+            self._dev_key = None
         key = (str(dev), self.data.ctypes.data, self.data.size)
         if self._dev is None or self._dev_key != key:
             buf = torch.zeros(self.data.size + ARENA_PAD, dtype=torch.uint8, device=dev)
             if self.data.size:
-                buf[: self.data.size].copy_(torch.from_numpy(self.data), non_blocking=False)
+                src = self.data if self.data.flags.writeable else self.data.copy()
+                buf[: self.data.size].copy_(torch.from_numpy(src), non_blocking=False)
             self._dev = buf
             self._dev_key = key
         return self._dev
 
     def drop_device(self):
+        if self._data is None:
+            self.data  # noqa: B018 -- keep the host copy of a device-born arena
         self._dev = None
         self._dev_key = None
 
@@ -152,7 +183,7 @@ def pack_keys(arena: StringArena, handles, depth: int = 0, out=None):
     h = _to_dev_handles(handles, dev)
     keys = torch.empty(h.numel(), dtype=torch.int64, device=dev)
     if h.numel():
-        rc = _lib.lib().s5_pack_keys(arena.device(dev).data_ptr(), arena.data.size, h.data_ptr(),
+        rc = _lib.lib().s5_pack_keys(arena.device(dev).data_ptr(), arena.size, h.data_ptr(),
                                      h.numel(), int(depth), keys.data_ptr(),
                                      _lib.current_stream_ptr())
         _lib.check(rc, "s5_pack_keys")
@@ -180,7 +211,7 @@ def adjacent_lcps(arena: StringArena, sorted_handles):
     n = h.numel()
     out = torch.empty(max(n - 1, 0), dtype=torch.int64, device=dev)
     if n > 1:
-        rc = _lib.lib().s5_adjacent_lcp(arena.device(dev).data_ptr(), arena.data.size,
+        rc = _lib.lib().s5_adjacent_lcp(arena.device(dev).data_ptr(), arena.size,
                                         h.data_ptr(), n, out.data_ptr(), _lib.current_stream_ptr())
         _lib.check(rc, "s5_adjacent_lcp")
     if isinstance(sorted_handles, torch.Tensor) and sorted_handles.is_cuda:
@@ -200,7 +231,7 @@ def first_unsorted(arena: StringArena, handles) -> int:
     dev = handles.device if isinstance(handles, torch.Tensor) and handles.is_cuda else _dev()
     h = _to_dev_handles(handles, dev)
     res = torch.empty(1, dtype=torch.int64, device=dev)
-    rc = _lib.lib().s5_first_unsorted(arena.device(dev).data_ptr(), arena.data.size, h.data_ptr(),
+    rc = _lib.lib().s5_first_unsorted(arena.device(dev).data_ptr(), arena.size, h.data_ptr(),
                                       h.numel(), res.data_ptr(), _lib.current_stream_ptr())
     _lib.check(rc, "s5_first_unsorted")
     return int(res.item())
@@ -224,16 +255,90 @@ def verify_sorted_permutation(arena: StringArena, original, result) -> VerifyRes
 
 
 def string_lengths(arena: StringArena, handles):
-    """Distance from every handle to its terminator (strings.py:85-96, 249-253)."""
+    """Distance from every handle to its terminator (strings.py:85-96, 249-253):
+    ordered compaction of the arena's terminators + binary search (s5_string_lengths)."""
     import torch
+    from . import _lib
     dev = handles.device if isinstance(handles, torch.Tensor) and handles.is_cuda else _dev()
     h = _to_dev_handles(handles, dev)
-    zeros = torch.nonzero(arena.device(dev)[: arena.data.size] == 0).flatten()
-    nxt = zeros[torch.searchsorted(zeros, h)]
-    out = nxt - h
+    out = torch.empty(h.numel(), dtype=torch.int64, device=dev)
+    if h.numel():
+        rc = _lib.lib().s5_string_lengths(arena.device(dev).data_ptr(), arena.size, h.data_ptr(),
+                                          h.numel(), out.data_ptr(), _lib.current_stream_ptr())
+        _lib.check(rc, "s5_string_lengths")
     if isinstance(handles, torch.Tensor) and handles.is_cuda:
         return out
     return out.cpu().numpy()
+
+
+class EmbeddedNul(ValueError):
+    """The input holds a 0 byte (harness.py:36-39)."""
+
+    def __init__(self, offset: int):
+        super().__init__(f"input contains byte 0 at offset {offset}")
+        self.offset = offset
+
+
+def ingest_lines(raw, device=None):
+    """load_lines (harness.py:72-95) on the device: one string per line of
+    ``raw`` (bytes / uint8 array / CUDA uint8 tensor), newlines become
+    terminators, a terminator is appended after an unterminated last line.
+    Returns (StringArena born in HBM, CUDA int64 handles)."""
+    import ctypes as C
+    import torch
+    from . import _lib
+    dev = torch.device(device) if device is not None else _dev()
+    if isinstance(raw, torch.Tensor):
+        d_raw = raw.to(dev, torch.uint8).contiguous()
+    else:
+        arr = np.frombuffer(raw, np.uint8) if isinstance(raw, (bytes, bytearray, memoryview)) \
+            else np.ascontiguousarray(raw, np.uint8)
+        d_raw = torch.from_numpy(arr.copy() if not arr.flags.writeable else arr).to(dev)
+    n = d_raw.numel()
+    buf = torch.zeros(n + 1 + ARENA_PAD, dtype=torch.uint8, device=dev)
+    handles = torch.empty(n + 2, dtype=torch.int64, device=dev)
+    hn, hlen, hnul = C.c_uint64(0), C.c_uint64(0), C.c_int64(-1)
+    rc = _lib.lib().s5_ingest_lines(d_raw.data_ptr(), n, buf.data_ptr(), handles.data_ptr(),
+                                    C.byref(hn), C.byref(hlen), C.byref(hnul),
+                                    _lib.current_stream_ptr())
+    if rc != 0 and hnul.value >= 0:
+        raise EmbeddedNul(int(hnul.value))
+    _lib.check(rc, "s5_ingest_lines")
+    return StringArena.from_device(buf, hlen.value), handles[: hn.value]
+
+
+def load_lines(path, device=None):
+    """load_lines (harness.py:83-95): read the file, ingest on the device."""
+    with open(path, "rb") as f:
+        raw = f.read()
+    return ingest_lines(raw, device)
+
+
+def materialize(arena: StringArena, sorted_handles):
+    """The strings of ``sorted_handles`` gathered in order into a new arena
+    (strings_of, tests/helpers.py:62-68), on the device.
+    Returns (StringArena born in HBM, CUDA int64 handles into it)."""
+    import ctypes as C
+    import torch
+    from . import _lib
+    dev = (sorted_handles.device if isinstance(sorted_handles, torch.Tensor)
+           and sorted_handles.is_cuda else _dev())
+    h = _to_dev_handles(sorted_handles, dev)
+    n = h.numel()
+    out_h = torch.empty(n, dtype=torch.int64, device=dev)
+    need = C.c_uint64(0)
+    ad = arena.device(dev).data_ptr()
+    L = _lib.lib()
+    # size, then gather
+    rc = L.s5_materialize(ad, arena.size, h.data_ptr(), n, None, 0, out_h.data_ptr(),
+                          C.byref(need), _lib.current_stream_ptr())
+    if rc not in (0, -3):
+        _lib.check(rc, "s5_materialize")
+    buf = torch.zeros(need.value + ARENA_PAD, dtype=torch.uint8, device=dev)
+    rc = L.s5_materialize(ad, arena.size, h.data_ptr(), n, buf.data_ptr(), need.value,
+                          out_h.data_ptr(), C.byref(need), _lib.current_stream_ptr())
+    _lib.check(rc, "s5_materialize")
+    return StringArena.from_device(buf, need.value), out_h
 
 
 def distinguishing_prefix(arena: StringArena, sorted_handles, lcp_arr=None) -> int:

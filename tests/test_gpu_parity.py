@@ -193,6 +193,71 @@ def test_adversarial_shapes_through_every_tier(shape):
     _check_sorted(arena, h, got, want, lcp, O.adjacent_lcps(arena, want), shape)
 
 
+def _load_lines_reference(raw: bytes):
+    # harness.py:83-95 restated on numpy (newline -> terminator, one appended
+    # after an unterminated last line)
+    data = np.frombuffer(raw, np.uint8).copy()
+    if data.size == 0:
+        return data, np.zeros(0, np.int64)
+    data[data == ord("\n")] = 0
+    if data[-1] != 0:
+        data = np.append(data, np.uint8(0))
+    ends = np.nonzero(data == 0)[0]
+    handles = np.zeros(ends.size, np.int64)
+    handles[1:] = ends[:-1] + 1
+    return data, handles
+
+
+@pytest.mark.parametrize("tail", [b"", b"\n", b"last-line-no-newline", b"\n\n"])
+def test_ingest_lines_matches_harness(tail):
+    from paper_1305_1157_b200 import ingest_lines
+    rng = np.random.default_rng(4)
+    lines = [bytes(rng.integers(32, 127, rng.integers(0, 40)).tolist()) for _ in range(70_000)]
+    raw = b"\n".join(lines) + tail
+    want_data, want_h = _load_lines_reference(raw)
+    arena, h = ingest_lines(raw)
+    assert arena.size == want_data.size
+    assert np.array_equal(arena.data, want_data)
+    assert np.array_equal(h.cpu().numpy(), want_h)
+    # the device-born arena sorts like any other
+    got, lcp = sort_with_lcp(arena, h.cpu().numpy())
+    ref_arena = StringArena(want_data)
+    want = want_h.copy()
+    O.parallel_sample_sort(ref_arena, want, 4)
+    assert O.contents_equal(ref_arena, got, want)
+    assert np.array_equal(lcp, O.adjacent_lcps(ref_arena, want))
+
+
+def test_ingest_rejects_embedded_nul_and_handles_empty():
+    from paper_1305_1157_b200 import EmbeddedNul, ingest_lines
+    with pytest.raises(EmbeddedNul) as e:
+        ingest_lines(b"abc\ndef\x00gh\nij\x00")
+    assert e.value.offset == 7
+    arena, h = ingest_lines(b"")
+    assert arena.size == 0 and h.numel() == 0
+
+
+def test_string_lengths_and_materialize():
+    from paper_1305_1157_b200 import arena_from_strings, materialize, string_lengths
+    rng = np.random.default_rng(9)
+    strs = [bytes(rng.integers(1, 256, rng.integers(0, 50)).tolist()) for _ in range(50_000)]
+    arena, h = arena_from_strings(strs)
+    assert np.array_equal(string_lengths(arena, h), np.array([len(x) for x in strs]))
+    sh, _ = sort_with_lcp(arena, h.copy())
+    out, oh = materialize(arena, sh)
+    want = sorted(strs)
+    assert out.size == sum(len(x) + 1 for x in strs)
+    raw = out.data.tobytes()
+    oh = oh.cpu().numpy()
+    assert [raw[a:raw.index(0, a)] for a in oh] == want
+    assert np.array_equal(np.diff(oh), np.array([len(x) + 1 for x in want[:-1]]))
+    # suffix-mode arena: one terminator at the end
+    text = bytes(rng.integers(97, 100, 3000).tolist()) + b"\x00"
+    sa = StringArena(np.frombuffer(text, np.uint8))
+    hh = np.arange(3000, dtype=np.int64)
+    assert np.array_equal(string_lengths(sa, hh), 3000 - hh)
+
+
 def test_pack_keys_matches_reference():
     from conftest import GOLDEN
     z = np.load(os.path.join(GOLDEN, "pack_keys.npz"))
