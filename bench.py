@@ -483,8 +483,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    elif dist_env()[0] > 1:
-        run_distributed(args)
+    elif dist_env()[0] > 1 or os.environ.get("S5_BENCH_DISTRIBUTED") == "1":
+        run_distributed(args)  # (the env switch runs the multi-GPU path on one rank: a smoke test)
     else:
         run_ours(args)
 

@@ -30,9 +30,23 @@ by the test.
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass
 
 import numpy as np
+
+PHASES = None  # profiles/dist_phases.py sets a dict: per-phase wall ms (device synchronised)
+
+
+def _mark(name, t):
+    """Phase timing for profiles/dist_phases.py (no-op unless PHASES is a dict)."""
+    if PHASES is None:
+        return t
+    import torch
+    torch.cuda.synchronize()
+    now = time.perf_counter()
+    PHASES[name] = PHASES.get(name, 0.0) + 1e3 * (now - t)
+    return now
 
 
 class GpuBackend:
@@ -54,6 +68,11 @@ class GpuBackend:
     def lengths(self, handles):
         from .strings import string_lengths
         return string_lengths(self.arena, handles)
+
+    def ends_at(self, handles, pos):
+        """True where the string at ``handles`` has its terminator at ``pos``."""
+        buf = self.arena.device(self.device)
+        return buf[(handles + pos).clamp(0, self.arena.size - 1)] == 0
 
     def partition(self, handles, splitters):
         """Handles grouped by destination rank (s5_partition) and the group
@@ -162,21 +181,26 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
     h = local_handles.contiguous()
     n_local = h.numel()
 
+    t = time.perf_counter()
     # 1. samples (with replacement, seeded per rank) -> all_gather
     s = oversample * G
-    gen = torch.Generator(device="cpu").manual_seed(seed * 1_000_003 + rank)
-    if n_local:
-        pick = torch.randint(0, n_local, (s,), generator=gen).to(dev)
-        samp = h[pick]
+    if n_local:  # drawn on the device: no host round trip
+        gen = torch.Generator(device=dev).manual_seed(seed * 1_000_003 + rank)
+        samp = h[torch.randint(0, n_local, (s,), generator=gen, device=dev)]
     else:
         samp = torch.full((s,), -1, dtype=torch.int64, device=dev)
-    gathered = [torch.empty_like(samp) for _ in range(G)]
-    dist.all_gather(gathered, samp, group=group)
-    allsamp = torch.cat(gathered)
-    allsamp = allsamp[allsamp >= 0]
+    allsamp = torch.empty(G * s, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allsamp, samp, group=group)
+    top = allsamp.max()
+    if int(top.item()) < 0:  # no strings on any rank
+        allsamp = allsamp[:0]
+    else:  # empty ranks' slots repeat a drawn handle (splitters stay strings)
+        allsamp = torch.where(allsamp >= 0, allsamp, top)
 
+    t = _mark("sample", t)
     # 2. identical splitters on every rank: sort by (string, handle)
     splitters = _pick_splitters(be, allsamp, G)
+    t = _mark("splitters", t)
 
     # 3. destination of every local string, handles grouped by destination
     if G == 1 or splitters.numel() == 0:  # one rank, or no strings on any rank
@@ -184,6 +208,7 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
     else:
         send, counts = be.partition(h, splitters)
     send_counts = torch.tensor(counts, dtype=torch.int64, device=dev)
+    t = _mark("partition", t)
 
     # 4. exchange counts, then handles
     recv_counts = torch.empty_like(send_counts)
@@ -192,26 +217,29 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
     dist.all_to_all_single(recv, send, output_split_sizes=recv_counts.tolist(),
                            input_split_sizes=send_counts.tolist(), group=group)
 
+    t = _mark("exchange", t)
     # 5. local sort + LCP
     recv, lcp = be.sort(recv)
+    t = _mark("local_sort", t)
 
-    # 6. boundary LCPs and global offsets
-    sizes = torch.tensor([recv.numel()], dtype=torch.int64, device=dev)
-    all_sizes = [torch.empty_like(sizes) for _ in range(G)]
-    dist.all_gather(all_sizes, sizes, group=group)
-    counts = [int(x.item()) for x in all_sizes]
-    first = recv[:1] if recv.numel() else torch.full((1,), -1, dtype=torch.int64, device=dev)
-    firsts = [torch.empty_like(first) for _ in range(G)]
-    dist.all_gather(firsts, first, group=group)
+    # 6. boundary LCPs and global offsets: one all-gather of (size, first handle)
+    mine = torch.tensor([recv.numel(), -1], dtype=torch.int64, device=dev)
+    if recv.numel():
+        mine[1:] = recv[:1]
+    allm = torch.empty(2 * G, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allm, mine, group=group)
+    meta = allm.view(G, 2).tolist()
+    counts = [int(m[0]) for m in meta]
     nxt = None
     for r in range(rank + 1, G):
         if counts[r]:
-            nxt = firsts[r]
+            nxt = int(meta[r][1])
             break
     if recv.numel() and nxt is not None:
-        pair = torch.cat([recv[-1:], nxt])
+        pair = torch.cat([recv[-1:], torch.tensor([nxt], dtype=torch.int64, device=dev)])
         lcp = torch.cat([lcp, be.lcp_pair(pair)])
     offset = sum(counts[:rank])
+    _mark("boundary", t)
     return ShardResult(recv, lcp, offset, counts)
 
 
@@ -223,9 +251,9 @@ def _pick_splitters(be, samples, G: int):
     s = samples.clone()
     s, lcp = be.sort(s)
     # identical strings: order by handle so every rank picks the same splitters
-    lens = be.lengths(s)
+    # (neighbours are identical iff both end right after their common prefix)
     if s.numel() > 1:
-        same = (lcp == lens[:-1]) & (lcp == lens[1:])
+        same = be.ends_at(s[:-1], lcp) & be.ends_at(s[1:], lcp)
         run = torch.cat([torch.zeros(1, dtype=torch.int64, device=s.device),
                          torch.cumsum((~same).to(torch.int64), 0)])
         key = run * 0  # stable two-key sort: by handle, then by run

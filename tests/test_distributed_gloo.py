@@ -28,6 +28,10 @@ class OracleBackend:
     def lengths(self, handles):
         return torch.from_numpy(O.string_lengths(self.arena, handles.numpy()))
 
+    def ends_at(self, handles, pos):
+        data = torch.from_numpy(self.arena.data)
+        return data[(handles + pos).clamp(0, self.arena.size - 1)] == 0
+
     def partition(self, h, splitters):
         # binary search over the splitters with full-string comparison
         n, G = h.numel(), splitters.numel() + 1
