@@ -153,6 +153,16 @@ int s5_adjacent_lcp(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d
 int s5_first_unsorted(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_handles,
                       uint64_t n, int64_t *d_result, void *stream);
 
+/* The host-buffer staging of s5_sort_host on its own (the multi-GPU path's
+ * shards): int64 handles in host memory -> d_handles (crossing PCIe as u32,
+ * range-checked against arena_len); and d_handles[n] (+ d_lcp[n_lcp]) ->
+ * host int64 arrays (u32 handles, LCPs in the narrowest width that holds
+ * their maximum).  h_lcp may be null. */
+int s5_upload_handles(const int64_t *h_handles, uint64_t n, uint64_t arena_len, int64_t *d_handles,
+                      void *stream);
+int s5_download(const int64_t *d_handles, uint64_t n, const int64_t *d_lcp, uint64_t n_lcp,
+                int64_t *h_handles, int64_t *h_lcp, void *stream);
+
 /* Multi-GPU partition step (the reference's only parallel
  * split is the pS^5 worker split, samplesort.py:369-434): the destination
  * rank of each of n local strings is the number of the nsplit splitter

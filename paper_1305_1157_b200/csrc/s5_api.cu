@@ -475,12 +475,125 @@ struct HostPath {
     cudaEvent_t ev[2] = {nullptr, nullptr};
     unsigned long long* dmax = nullptr;
     unsigned long long* hmax = nullptr;
+    void* xbuf = nullptr;  // narrowing scratch of the standalone transfer entries
+    uint64_t xbytes = 0;
     static constexpr uint64_t kChunk = 32ull << 20;  // bytes per staging buffer
 };
 
 HostPath& host_path() {
     static HostPath hp;
     return hp;
+}
+
+int host_path_init(HostPath& H) {
+    if (H.stage[0]) return 0;
+    for (int i = 0; i < 2; ++i) {
+        S5_CUDA(cudaHostAlloc(&H.stage[i], HostPath::kChunk, cudaHostAllocDefault));
+        S5_CUDA(cudaEventCreateWithFlags(&H.ev[i], cudaEventDisableTiming));
+    }
+    S5_CUDA(cudaMalloc(&H.dmax, sizeof(unsigned long long)));
+    S5_CUDA(cudaHostAlloc(&H.hmax, sizeof(unsigned long long), cudaHostAllocDefault));
+    return 0;
+}
+
+int host_scratch(HostPath& H, uint64_t bytes) {
+    if (bytes <= H.xbytes) return 0;
+    if (H.xbuf) cudaFree(H.xbuf);
+    H.xbuf = nullptr;
+    H.xbytes = 0;
+    S5_CUDA(cudaMalloc(&H.xbuf, bytes));
+    H.xbytes = bytes;
+    return 0;
+}
+
+// H2D: narrow + range-check into pinned staging (host workers), DMA, widen
+// on the device; chunk i is narrowed while chunk i-1 is in flight
+int host_upload(HostPath& H, const int64_t* h_handles, uint64_t n, uint64_t arena_len,
+                uint32_t* d32, int64_t* dh, cudaStream_t st) {
+    Pool& pool = Pool::get();
+    const uint64_t per = HostPath::kChunk / 4;
+    std::atomic<bool> bad{false};
+    uint64_t ci = 0;
+    for (uint64_t off = 0; off < n; off += per, ++ci) {
+        const uint64_t len = std::min(per, n - off);
+        const int b = static_cast<int>(ci & 1);
+        if (ci >= 2) S5_CUDA(cudaEventSynchronize(H.ev[b]));
+        uint32_t* s32 = static_cast<uint32_t*>(H.stage[b]);
+        const int64_t* src = h_handles + off;
+        pool.par_for(len, [&](uint64_t a, uint64_t e) {
+            if (narrow_u32(src + a, s32 + a, e - a, arena_len)) bad.store(true, std::memory_order_relaxed);
+        });
+        S5_CUDA(cudaMemcpyAsync(d32 + off, s32, len * 4, cudaMemcpyHostToDevice, st));
+        S5_CUDA(cudaEventRecord(H.ev[b], st));
+    }
+    k_widen32<<<grid_for(n, 256), 256, 0, st>>>(d32, dh, n);
+    S5_CUDA(cudaStreamSynchronize(st));
+    if (bad.load()) return fail(S5_E_RANGE, "handle outside the arena");
+    return 0;
+}
+
+// D2H: handles narrowed to u32 and the LCP array to the narrowest width
+// holding its maximum on the device, DMA, widened into the caller's arrays
+// (chunk i widened while chunk i+1 is in flight)
+int host_download(HostPath& H, const int64_t* dh, uint64_t n, const int64_t* dl, uint64_t nl,
+                  uint32_t* d32, void* dn, int64_t* h_handles, int64_t* h_lcp, cudaStream_t st,
+                  uint64_t* bytes) {
+    Pool& pool = Pool::get();
+    const uint64_t per = HostPath::kChunk / 4;
+    if (n) k_shrink<uint32_t><<<grid_for(n, 256), 256, 0, st>>>(dh, d32, n);
+    uint32_t w = 8;
+    if (dl && h_lcp && nl) {
+        S5_CUDA(cudaMemsetAsync(H.dmax, 0, sizeof(unsigned long long), st));
+        k_max64<<<grid_for(nl, 256), 256, 0, st>>>(dl, nl, H.dmax);
+        S5_CUDA(cudaMemcpyAsync(H.hmax, H.dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        S5_CUDA(cudaStreamSynchronize(st));
+        const unsigned long long mx = *H.hmax;
+        w = mx <= 0xFFull ? 1 : mx <= 0xFFFFull ? 2 : mx <= 0xFFFFFFFFull ? 4 : 8;
+        const int g = grid_for(nl, 256);
+        if (w == 1) k_shrink<uint8_t><<<g, 256, 0, st>>>(dl, static_cast<uint8_t*>(dn), nl);
+        if (w == 2) k_shrink<uint16_t><<<g, 256, 0, st>>>(dl, static_cast<uint16_t*>(dn), nl);
+        if (w == 4) k_shrink<uint32_t><<<g, 256, 0, st>>>(dl, static_cast<uint32_t*>(dn), nl);
+    }
+    S5_CUDA(cudaGetLastError());
+    struct Piece { const char* d; int64_t* h; uint64_t count; uint32_t w; };
+    std::vector<Piece> pieces;
+    for (uint64_t off = 0; off < n; off += per)
+        pieces.push_back({reinterpret_cast<const char*>(d32 + off), h_handles + off,
+                          std::min(per, n - off), 4});
+    if (dl && h_lcp && nl) {
+        const char* src = w == 8 ? reinterpret_cast<const char*>(dl) : static_cast<const char*>(dn);
+        const uint64_t pl = HostPath::kChunk / w;
+        for (uint64_t off = 0; off < nl; off += pl)
+            pieces.push_back({src + off * w, h_lcp + off, std::min(pl, nl - off), w});
+    }
+    *bytes = n * 4 + (dl && h_lcp ? nl * w : 0);
+    if (pieces.empty()) return 0;
+    auto issue = [&](uint64_t k) -> int {
+        int b = static_cast<int>(k & 1);
+        S5_CUDA(cudaMemcpyAsync(H.stage[b], pieces[k].d, pieces[k].count * pieces[k].w,
+                                cudaMemcpyDeviceToHost, st));
+        S5_CUDA(cudaEventRecord(H.ev[b], st));
+        return 0;
+    };
+    if (int e = issue(0)) return e;
+    for (uint64_t k = 0; k < pieces.size(); ++k) {
+        if (k + 1 < pieces.size())
+            if (int e = issue(k + 1)) return e;
+        const int b = static_cast<int>(k & 1);
+        S5_CUDA(cudaEventSynchronize(H.ev[b]));
+        const Piece P = pieces[k];
+        const void* sp = H.stage[b];
+        pool.par_for(P.count, [&](uint64_t a, uint64_t e) {
+            switch (P.w) {
+                case 1: widen(static_cast<const uint8_t*>(sp) + a, P.h + a, e - a); break;
+                case 2: widen(static_cast<const uint16_t*>(sp) + a, P.h + a, e - a); break;
+                case 4: widen(static_cast<const uint32_t*>(sp) + a, P.h + a, e - a); break;
+                default: memcpy(P.h + a, static_cast<const int64_t*>(sp) + a, (e - a) * 8);
+            }
+        });
+    }
+    S5_CUDA(cudaStreamSynchronize(st));
+    return 0;
 }
 
 }  // namespace
@@ -827,14 +940,7 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
         S5_CUDA(cudaMalloc(&H.dbuf, need));
         H.dbytes = need;
     }
-    if (!H.stage[0]) {
-        for (int i = 0; i < 2; ++i) {
-            S5_CUDA(cudaHostAlloc(&H.stage[i], HostPath::kChunk, cudaHostAllocDefault));
-            S5_CUDA(cudaEventCreateWithFlags(&H.ev[i], cudaEventDisableTiming));
-        }
-        S5_CUDA(cudaMalloc(&H.dmax, sizeof(unsigned long long)));
-        S5_CUDA(cudaHostAlloc(&H.hmax, sizeof(unsigned long long), cudaHostAllocDefault));
-    }
+    if (int rc = host_path_init(H)) return rc;
     cudaStream_t st = static_cast<cudaStream_t>(stream_);
     char* base = static_cast<char*>(H.dbuf);
     int64_t* dh = reinterpret_cast<int64_t*>(base);
@@ -842,97 +948,55 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
     uint32_t* d32 = reinterpret_cast<uint32_t*>(base + 2 * align_up(n * 8));
     void* dn = base + 2 * align_up(n * 8) + align_up(n * 4);
     void* dws = base + 2 * align_up(n * 8) + 2 * align_up(n * 4);
-    Pool& pool = Pool::get();
 
-    // H2D: narrow + range-check into pinned staging, DMA, widen on the device
     auto t0 = std::chrono::steady_clock::now();
-    const uint64_t per = HostPath::kChunk / 4;
-    std::atomic<bool> bad{false};
-    uint64_t ci = 0;
-    for (uint64_t off = 0; off < n; off += per, ++ci) {
-        const uint64_t len = std::min(per, n - off);
-        const int b = static_cast<int>(ci & 1);
-        if (ci >= 2) S5_CUDA(cudaEventSynchronize(H.ev[b]));
-        uint32_t* s32 = static_cast<uint32_t*>(H.stage[b]);
-        const int64_t* src = h_handles + off;
-        pool.par_for(len, [&](uint64_t a, uint64_t e) {
-            if (narrow_u32(src + a, s32 + a, e - a, arena_len)) bad.store(true, std::memory_order_relaxed);
-        });
-        S5_CUDA(cudaMemcpyAsync(d32 + off, s32, len * 4, cudaMemcpyHostToDevice, st));
-        S5_CUDA(cudaEventRecord(H.ev[b], st));
-    }
-    k_widen32<<<grid_for(n, 256), 256, 0, st>>>(d32, dh, n);
-    S5_CUDA(cudaStreamSynchronize(st));
-    if (bad.load()) return fail(S5_E_RANGE, "handle outside the arena");
+    if (int rc = host_upload(H, h_handles, n, arena_len, d32, dh, st)) return rc;
     auto t1 = std::chrono::steady_clock::now();
     int rc = s5_sort(d_arena, arena_len, dh, n, depth, h_lcp ? dl : nullptr, cfg, dws, ws,
                      stream_, stats);
     if (rc) return rc;
-
-    // D2H: narrow on the device, DMA, widen into the caller's arrays
-    k_shrink<uint32_t><<<grid_for(n, 256), 256, 0, st>>>(dh, d32, n);
-    uint32_t w = 8;
-    if (h_lcp) {
-        S5_CUDA(cudaMemsetAsync(H.dmax, 0, sizeof(unsigned long long), st));
-        k_max64<<<grid_for(n - 1, 256), 256, 0, st>>>(dl, n - 1, H.dmax);
-        S5_CUDA(cudaMemcpyAsync(H.hmax, H.dmax, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        S5_CUDA(cudaStreamSynchronize(st));
-        const unsigned long long mx = *H.hmax;
-        w = mx <= 0xFFull ? 1 : mx <= 0xFFFFull ? 2 : mx <= 0xFFFFFFFFull ? 4 : 8;
-        const int g = grid_for(n - 1, 256);
-        if (w == 1) k_shrink<uint8_t><<<g, 256, 0, st>>>(dl, static_cast<uint8_t*>(dn), n - 1);
-        if (w == 2) k_shrink<uint16_t><<<g, 256, 0, st>>>(dl, static_cast<uint16_t*>(dn), n - 1);
-        if (w == 4) k_shrink<uint32_t><<<g, 256, 0, st>>>(dl, static_cast<uint32_t*>(dn), n - 1);
-    }
-    S5_CUDA(cudaGetLastError());
     S5_CUDA(cudaStreamSynchronize(st));
     auto t2 = std::chrono::steady_clock::now();
-
-    struct Piece { const char* d; int64_t* h; uint64_t count; uint32_t w; };
-    std::vector<Piece> pieces;
-    for (uint64_t off = 0; off < n; off += per)
-        pieces.push_back({reinterpret_cast<const char*>(d32 + off), h_handles + off,
-                          std::min(per, n - off), 4});
-    if (h_lcp) {
-        const char* src = w == 8 ? reinterpret_cast<const char*>(dl) : static_cast<const char*>(dn);
-        const uint64_t pl = HostPath::kChunk / w;
-        for (uint64_t off = 0; off < n - 1; off += pl)
-            pieces.push_back({src + off * w, h_lcp + off, std::min(pl, n - 1 - off), w});
-    }
-    auto issue = [&](uint64_t k) -> int {
-        int b = static_cast<int>(k & 1);
-        S5_CUDA(cudaMemcpyAsync(H.stage[b], pieces[k].d, pieces[k].count * pieces[k].w,
-                                cudaMemcpyDeviceToHost, st));
-        S5_CUDA(cudaEventRecord(H.ev[b], st));
-        return 0;
-    };
-    if (int e = issue(0)) return e;
-    for (uint64_t k = 0; k < pieces.size(); ++k) {
-        if (k + 1 < pieces.size())
-            if (int e = issue(k + 1)) return e;
-        const int b = static_cast<int>(k & 1);
-        S5_CUDA(cudaEventSynchronize(H.ev[b]));
-        const Piece P = pieces[k];
-        const void* sp = H.stage[b];
-        pool.par_for(P.count, [&](uint64_t a, uint64_t e) {
-            switch (P.w) {
-                case 1: widen(static_cast<const uint8_t*>(sp) + a, P.h + a, e - a); break;
-                case 2: widen(static_cast<const uint16_t*>(sp) + a, P.h + a, e - a); break;
-                case 4: widen(static_cast<const uint32_t*>(sp) + a, P.h + a, e - a); break;
-                default: memcpy(P.h + a, static_cast<const int64_t*>(sp) + a, (e - a) * 8);
-            }
-        });
-    }
-    S5_CUDA(cudaStreamSynchronize(st));
+    uint64_t d2h_bytes = 0;
+    if (int e = host_download(H, dh, n, h_lcp ? dl : nullptr, n - 1, d32, dn, h_handles, h_lcp, st,
+                              &d2h_bytes))
+        return e;
     auto t3 = std::chrono::steady_clock::now();
     if (stats) {
         stats->host_h2d_ms = std::chrono::duration<float, std::milli>(t1 - t0).count();
         stats->host_sort_ms = std::chrono::duration<float, std::milli>(t2 - t1).count();
         stats->host_d2h_ms = std::chrono::duration<float, std::milli>(t3 - t2).count();
         stats->host_h2d_bytes = n * 4;
-        stats->host_d2h_bytes = n * 4 + (h_lcp ? (n - 1) * w : 0);
+        stats->host_d2h_bytes = d2h_bytes;
     }
     return 0;
+}
+
+// Host-buffer transfers on their own (the multi-GPU path's shards): the same
+// u32 / narrowest-LCP staging as s5_sort_host.
+int s5_upload_handles(const int64_t* h_handles, uint64_t n, uint64_t arena_len, int64_t* d_handles,
+                      void* stream) {
+    HostPath& H = host_path();
+    std::lock_guard<std::mutex> lock(H.mu);
+    if (n == 0) return 0;
+    if (arena_len > 0xFFFFFFFFull) return fail(S5_E_RANGE, "offsets are 32-bit (arena < 4 GiB)");
+    if (int rc = host_path_init(H)) return rc;
+    if (int rc = host_scratch(H, align_up(n * 4))) return rc;
+    return host_upload(H, h_handles, n, arena_len, static_cast<uint32_t*>(H.xbuf), d_handles,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int s5_download(const int64_t* d_handles, uint64_t n, const int64_t* d_lcp, uint64_t n_lcp,
+                int64_t* h_handles, int64_t* h_lcp, void* stream) {
+    HostPath& H = host_path();
+    std::lock_guard<std::mutex> lock(H.mu);
+    if (int rc = host_path_init(H)) return rc;
+    if (int rc = host_scratch(H, align_up(n * 4) + align_up(n_lcp * 4))) return rc;
+    uint32_t* d32 = static_cast<uint32_t*>(H.xbuf);
+    void* dn = static_cast<char*>(H.xbuf) + align_up(n * 4);
+    uint64_t bytes = 0;
+    return host_download(H, d_handles, n, h_lcp ? d_lcp : nullptr, n_lcp, d32, dn, h_handles, h_lcp,
+                         static_cast<cudaStream_t>(stream), &bytes);
 }
 
 int s5_pack_keys(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_handles,

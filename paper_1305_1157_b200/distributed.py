@@ -104,6 +104,31 @@ class GpuBackend:
         self.launches += 1
         return out
 
+    def upload(self, host_handles):
+        """Host int64 shard -> device tensor through the library's pinned u32
+        staging (s5_upload_handles)."""
+        import torch
+        from . import _lib
+        h = np.ascontiguousarray(host_handles, np.int64)
+        out = torch.empty(h.size, dtype=torch.int64, device=self.device)
+        rc = _lib.lib().s5_upload_handles(h.ctypes.data, h.size, self.arena.size, out.data_ptr(),
+                                          _lib.current_stream_ptr())
+        _lib.check(rc, "s5_upload_handles")
+        return out
+
+    def download(self, handles, lcp, out_h=None, out_l=None):
+        """Device slice + LCPs -> host int64 arrays (s5_download); reuses the
+        given host buffers (their leading elements) when large enough."""
+        from . import _lib
+        n, nl = handles.numel(), lcp.numel()
+        hh = out_h[:n] if out_h is not None and out_h.size >= n else np.empty(n, np.int64)
+        hl = out_l[:nl] if out_l is not None and out_l.size >= nl else np.empty(nl, np.int64)
+        rc = _lib.lib().s5_download(handles.data_ptr(), hh.size, lcp.data_ptr(), hl.size,
+                                    hh.ctypes.data, hl.ctypes.data if hl.size else None,
+                                    _lib.current_stream_ptr())
+        _lib.check(rc, "s5_download")
+        return hh, hl
+
     def sort(self, handles):
         """Sort a device int64 tensor in place; returns (handles, lcp)."""
         import torch
