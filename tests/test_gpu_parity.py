@@ -258,6 +258,26 @@ def test_string_lengths_and_materialize():
     assert np.array_equal(string_lengths(sa, hh), 3000 - hh)
 
 
+def test_standalone_upload_download_roundtrip():
+    # the multi-GPU path's host staging (s5_upload_handles / s5_download)
+    import torch
+    from paper_1305_1157_b200 import arena_from_strings
+    from paper_1305_1157_b200.distributed import GpuBackend
+    strs = [b"x" * (i % 700) + b"y" for i in range(40_000)]
+    arena, h = arena_from_strings(strs)
+    be = GpuBackend(arena)
+    d = be.upload(h)
+    assert torch.equal(d.cpu(), torch.from_numpy(h))
+    d2, lcp = be.sort(d.clone())
+    hh, hl = be.download(d2, lcp)
+    assert np.array_equal(hh, d2.cpu().numpy()) and np.array_equal(hl, lcp.cpu().numpy())
+    assert hl.max() > 255  # two-byte LCP transfer
+    bad = h.copy()
+    bad[5] = arena.size + 3
+    with pytest.raises(ValueError):
+        be.upload(bad)
+
+
 def test_pack_keys_matches_reference():
     from conftest import GOLDEN
     z = np.load(os.path.join(GOLDEN, "pack_keys.npz"))
