@@ -33,6 +33,8 @@ CONFIGS = {
     # bulk-copy staged scatter at every level; bitonic local sort + separate gather pass
     "wide_tma": SampleSortConfig(v=255, small_max=32, narrow_max=32, seed=5, flags=32),
     "bitonic_gather": SampleSortConfig(seed=9, flags=16 | 64),
+    # one-CTA S^5 step (narrow tier) for segments of 4097..16384 strings
+    "narrow_tier": SampleSortConfig(narrow_max=16384, seed=13),
 }
 
 
