@@ -216,6 +216,11 @@ int s5_build_tree(const uint64_t *d_sorted_sample, uint32_t m, uint32_t v,
 int s5_host_markov_text(const double *cdf, const double *u, uint64_t n, uint32_t sigma,
                         uint8_t *out);
 
+/* Frees the library's cached device buffers, pinned staging and side
+ * streams on every device (no call may be in flight); they are re-created
+ * on demand. */
+int s5_release_caches(void);
+
 const char *s5_last_error(void);
 int s5_version(void);
 

@@ -118,6 +118,7 @@ SIGNATURES = {
     "s5_first_unsorted": (C.c_int, [_vp, _u64, _vp, _u64, _vp, _vp]),
     "s5_partition": (C.c_int, [_vp, _u64, _vp, _u64, _vp, C.c_uint32, _vp, _vp, _vp]),
     "s5_ingest_lines": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "s5_release_caches": (C.c_int, []),
     "s5_upload_handles": (C.c_int, [_vp, _u64, _u64, _vp, _vp]),
     "s5_download": (C.c_int, [_vp, _u64, _vp, _u64, _vp, _vp, _vp]),
     "s5_string_lengths": (C.c_int, [_vp, _u64, _vp, _u64, _vp, _vp]),

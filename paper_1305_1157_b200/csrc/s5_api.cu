@@ -206,6 +206,25 @@ Pinned& pinned() {
     return p;
 }
 
+// One instance per CUDA device (the library's cached buffers live on the
+// device that was current when they were made).
+std::mutex& registry_mutex() {
+    static std::mutex m;
+    return m;
+}
+template <class T>
+std::map<int, T>& registry() {
+    static std::map<int, T> r;  // node-based: references stay valid
+    return r;
+}
+template <class T>
+T& per_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(registry_mutex());
+    return registry<T>()[dev];
+}
+
 int grid_for(uint64_t n, int threads, int max_blocks = 148 * 16) {
     uint64_t b = (n + threads - 1) / threads;
     return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(b, max_blocks)));
@@ -225,12 +244,10 @@ struct Side {
 };
 
 Side* side_streams() {
-    static std::mutex mu;
-    static std::map<int, Side> per_device;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-    std::lock_guard<std::mutex> g(mu);
-    Side& sd = per_device[dev];
+    std::lock_guard<std::mutex> g(registry_mutex());
+    Side& sd = registry<Side>()[dev];
     if (!sd.ok) {
         bool good = cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) == cudaSuccess;
         for (int i = 0; good && i < Side::kLanes; ++i)
@@ -480,10 +497,14 @@ struct HostPath {
     static constexpr uint64_t kChunk = 32ull << 20;  // bytes per staging buffer
 };
 
-HostPath& host_path() {
-    static HostPath hp;
-    return hp;
-}
+HostPath& host_path() { return per_device<HostPath>(); }
+
+struct PartScratch {  // s5_partition
+    std::mutex mu;
+    void* d = nullptr;
+    uint64_t bytes = 0;
+    unsigned long long* h = nullptr;
+};
 
 int host_path_init(HostPath& H) {
     if (H.stage[0]) return 0;
@@ -1034,11 +1055,6 @@ int s5_first_unsorted(const uint8_t* d_arena, uint64_t arena_len, const int64_t*
 int s5_partition(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_handles, uint64_t n,
                  const int64_t* d_splitters, uint32_t nsplit, int64_t* d_out, uint64_t* h_counts,
                  void* stream) {
-    static std::mutex mu;
-    static void* scratch = nullptr;
-    static uint64_t scratch_bytes = 0;
-    static unsigned long long* h_tot = nullptr;
-    std::lock_guard<std::mutex> lock(mu);
     (void)arena_len;
     const uint32_t G = nsplit + 1;
     if (G > kPartMaxRanks) return fail(S5_E_INVALID, "at most %u ranks", kPartMaxRanks);
@@ -1058,15 +1074,18 @@ int s5_partition(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_ha
     const uint32_t C = static_cast<uint32_t>(std::min<uint64_t>(1184, std::max<uint64_t>(1, n / 2048)));
     const uint32_t chunk = static_cast<uint32_t>((n + C - 1) / C);
     const uint64_t need = align_up(n * 2) + align_up(uint64_t(C) * G * 4) + align_up(G * 8ull);
-    if (need > scratch_bytes) {
-        if (scratch) cudaFree(scratch);
-        scratch = nullptr;
-        scratch_bytes = 0;
-        S5_CUDA(cudaMalloc(&scratch, need));
-        scratch_bytes = need;
+    PartScratch& X = per_device<PartScratch>();
+    std::lock_guard<std::mutex> lock(X.mu);
+    if (need > X.bytes) {
+        if (X.d) cudaFree(X.d);
+        X.d = nullptr;
+        X.bytes = 0;
+        S5_CUDA(cudaMalloc(&X.d, need));
+        X.bytes = need;
     }
-    if (!h_tot) S5_CUDA(cudaHostAlloc(&h_tot, kPartMaxRanks * 8, cudaHostAllocDefault));
-    char* p = static_cast<char*>(scratch);
+    if (!X.h) S5_CUDA(cudaHostAlloc(&X.h, kPartMaxRanks * 8, cudaHostAllocDefault));
+    unsigned long long* h_tot = X.h;
+    char* p = static_cast<char*>(X.d);
     uint16_t* dest = reinterpret_cast<uint16_t*>(p);
     uint32_t* rows = reinterpret_cast<uint32_t*>(p + align_up(n * 2));
     auto* tot = reinterpret_cast<unsigned long long*>(p + align_up(n * 2) + align_up(uint64_t(C) * G * 4));
@@ -1089,10 +1108,7 @@ struct AuxScratch {
     uint64_t bytes = 0;
     unsigned long long* h = nullptr;  // pinned: two results
 };
-AuxScratch& aux() {
-    static AuxScratch a;
-    return a;
-}
+AuxScratch& aux() { return per_device<AuxScratch>(); }
 int aux_reserve(AuxScratch& X, uint64_t bytes) {
     if (!X.h) S5_CUDA(cudaHostAlloc(&X.h, 16, cudaHostAllocDefault));
     if (bytes <= X.bytes) return 0;
@@ -1289,6 +1305,64 @@ int s5_host_markov_text(const double* cdf, const double* u, uint64_t n, uint32_t
         a = b;
         b = s;
     }
+    return 0;
+}
+
+int s5_release_caches(void) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    std::lock_guard<std::mutex> g(registry_mutex());
+    for (auto& kv : registry<HostPath>()) {
+        HostPath& H = kv.second;
+        std::lock_guard<std::mutex> l(H.mu);
+        cudaSetDevice(kv.first);
+        if (H.dbuf) cudaFree(H.dbuf);
+        if (H.xbuf) cudaFree(H.xbuf);
+        if (H.dmax) cudaFree(H.dmax);
+        if (H.hmax) cudaFreeHost(H.hmax);
+        for (int i = 0; i < 2; ++i) {
+            if (H.stage[i]) cudaFreeHost(H.stage[i]);
+            if (H.ev[i]) cudaEventDestroy(H.ev[i]);
+            H.stage[i] = nullptr;
+            H.ev[i] = nullptr;
+        }
+        H.dbuf = H.xbuf = nullptr;
+        H.dbytes = H.xbytes = 0;
+        H.dmax = nullptr;
+        H.hmax = nullptr;
+    }
+    for (auto& kv : registry<AuxScratch>()) {
+        AuxScratch& X = kv.second;
+        std::lock_guard<std::mutex> l(X.mu);
+        cudaSetDevice(kv.first);
+        if (X.d) cudaFree(X.d);
+        if (X.h) cudaFreeHost(X.h);
+        X.d = nullptr;
+        X.h = nullptr;
+        X.bytes = 0;
+    }
+    for (auto& kv : registry<PartScratch>()) {
+        PartScratch& X = kv.second;
+        std::lock_guard<std::mutex> l(X.mu);
+        cudaSetDevice(kv.first);
+        if (X.d) cudaFree(X.d);
+        if (X.h) cudaFreeHost(X.h);
+        X.d = nullptr;
+        X.h = nullptr;
+        X.bytes = 0;
+    }
+    for (auto& kv : registry<Side>()) {
+        Side& sd = kv.second;
+        if (!sd.ok) continue;
+        cudaSetDevice(kv.first);
+        for (int i = 0; i < Side::kLanes; ++i) {
+            cudaStreamDestroy(sd.s[i]);
+            cudaEventDestroy(sd.join[i]);
+        }
+        cudaEventDestroy(sd.fork);
+        sd = Side{};
+    }
+    cudaSetDevice(cur);
     return 0;
 }
 

@@ -1913,7 +1913,7 @@ template <uint32_t THREADS, uint32_t TILE>
 __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePlan P) {
     constexpr uint32_t kTmaThreads = THREADS, kTmaTile = TILE;
     using TmaStage = s5::TmaStage<TILE>;
-    extern __shared__ __align__(128) uint8_t sm[];
+    extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;
     TmaStage* stage = reinterpret_cast<TmaStage*>(sm);

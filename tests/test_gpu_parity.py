@@ -280,6 +280,16 @@ def test_standalone_upload_download_roundtrip():
         be.upload(bad)
 
 
+def test_release_caches_then_sort_again(sort_cases):
+    from paper_1305_1157_b200 import _lib
+    c = sort_cases["random_20000"]
+    arena = StringArena(c["arena"])
+    for _ in range(2):
+        h, lcp = sort_with_lcp(arena, c["handles"].copy())
+        _check_sorted(arena, c["handles"], h, c["sorted"], lcp, c["lcp"], "after release")
+        assert _lib.lib().s5_release_caches() == 0
+
+
 def test_pack_keys_matches_reference():
     from conftest import GOLDEN
     z = np.load(os.path.join(GOLDEN, "pack_keys.npz"))
