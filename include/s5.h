@@ -56,8 +56,8 @@ typedef struct {
                            * bit6: separate gather pass at level 0 */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
-    uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (255)  */
-    uint32_t wide_target; /* multi-CTA steps aim at children of this size (0: 3/16 local_max) */
+    uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (511)  */
+    uint32_t wide_target; /* multi-CTA steps aim at children of this size (0: local_max / 8) */
     uint32_t local_target; /* one-CTA steps aim at inner buckets of this size (0: 8) */
 } s5_config;
 

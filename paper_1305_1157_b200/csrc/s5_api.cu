@@ -73,7 +73,7 @@ int resolve(const s5_config* c, Cfg* o) {
     o->small_max = c && c->small_max ? c->small_max : 32;
     o->narrow_max = c && c->narrow_max ? c->narrow_max : 4096;  // narrow tier off by default
     o->local_max = c && c->local_max ? c->local_max : LocalCfg::maxn;
-    uint32_t wv = c && c->wide_v ? c->wide_v : 255;
+    uint32_t wv = c && c->wide_v ? c->wide_v : 511;
     uint32_t wd = 0;
     while (wd < 31 && ((1u << wd) - 1) < wv) ++wd;
     if (((1u << wd) - 1) != wv || wd > kWideDMax)
@@ -689,7 +689,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     A.wide_chunk = kWideChunkMin;
     A.wide_sample = wide_sample_words(c);
     if (const char* e = getenv("S5_WIDE_CHUNK")) A.wide_chunk = std::max(1024, atoi(e));  // tuning
-    A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max * 3 / 16);
+    A.wide_target = std::max<uint32_t>(16, c.wide_target ? c.wide_target : c.local_max / 8);
     A.narrow_max = c.narrow_max;
     A.dmax = c.dmax;
     A.alpha = c.alpha;

@@ -53,8 +53,8 @@ class SampleSortConfig:
     small_max: int = 32
     narrow_max: int = 4096
     local_max: int = 4096
-    wide_v: int = 255
-    wide_target: int = 768
+    wide_v: int = 511
+    wide_target: int = 512
     local_target: int = 8
     flags: int = 0
 
