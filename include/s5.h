@@ -47,7 +47,7 @@ enum {
  * Zero fields take defaults. */
 typedef struct {
     uint32_t v;           /* max splitters per step, 2^d-1 (default 8191)       */
-    uint32_t alpha;       /* oversampling factor (default 2)                    */
+    uint32_t alpha;       /* oversampling factor (default 4; the reference's 2)  */
     uint32_t classifier;  /* 0 = "unroll", 1 = "equal" (samplesort.py:43)      */
     uint32_t small_max;   /* segments <= small_max: warp base case (<= 32)      */
     uint32_t narrow_max;  /* segments <= narrow_max: one-CTA S^5 step (<=16384; 0: 4096 = off) */

@@ -68,7 +68,7 @@ using LocalMCfg = LocalSmem<kLocalMThreads>;
 
 int resolve(const s5_config* c, Cfg* o) {
     o->v = c && c->v ? c->v : 8191;
-    o->alpha = c && c->alpha ? c->alpha : 2;
+    o->alpha = c && c->alpha ? c->alpha : 4;
     o->classifier = c ? c->classifier : 0;
     o->small_max = c && c->small_max ? c->small_max : 32;
     o->narrow_max = c && c->narrow_max ? c->narrow_max : 4096;  // narrow tier off by default

@@ -41,10 +41,13 @@ class SampleSortConfig:
 
     ``t_m``/``t_i``/``interleave`` are kept for signature compatibility; the
     GPU tiers are ``narrow_max`` (one-CTA S^5 step, <= 16384 strings) and
-    ``small_max`` (warp base case, <= 32 strings).
+    ``small_max`` (warp base case, <= 32 strings).  ``alpha`` defaults to 4
+    (the reference's 2 is accepted): the wide steps' samples are cheap on the
+    device and better balanced buckets pay (measured 1-2 %); splitters only
+    move the order of identical strings, never the output.
     """
     v: int = 8191
-    alpha: int = 2
+    alpha: int = 4
     t_m: int = T_MEDIUM
     t_i: int = T_INSERTION
     classifier: str = "unroll"
