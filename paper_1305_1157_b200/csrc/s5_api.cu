@@ -1106,6 +1106,8 @@ struct AuxScratch {
     std::mutex mu;
     void* d = nullptr;
     uint64_t bytes = 0;
+    void* d2 = nullptr;  // materialisation: lengths and prefix sums
+    uint64_t bytes2 = 0;
     unsigned long long* h = nullptr;  // pinned: two results
 };
 AuxScratch& aux() { return per_device<AuxScratch>(); }
@@ -1137,6 +1139,32 @@ int zero_positions(const uint8_t* a, uint64_t len, int64_t* pos, int64_t shift, 
 uint64_t zero_scratch_bytes(uint64_t len) {
     const uint64_t blocks = (len + kScanChunk - 1) / kScanChunk;
     return align_up(blocks * 4) + align_up((blocks + 1) * 8);
+}
+// lengths of n strings into d_len: a short SWAR walk, then (only if some
+// string is longer than 64 bytes) the ordered terminator compaction + search
+int lengths_into(AuxScratch& X, const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_h,
+                 uint64_t n, int64_t* d_len, cudaStream_t st) {
+    if (int rc = aux_reserve(X, 64)) return rc;
+    auto* longer = static_cast<unsigned long long*>(X.d);
+    S5_CUDA(cudaMemsetAsync(longer, 0, 8, st));
+    // walk cap from the arena bytes per handle (line arenas: a few times the
+    // mean string; suffix arenas, ~1 byte per handle: short, then the search);
+    // the device arena's pad covers the over-read
+    const uint64_t per = (arena_len / std::max<uint64_t>(n, 1) + 7) / 8;
+    const uint32_t words = static_cast<uint32_t>(std::min<uint64_t>(14, 2 + 2 * per));
+    k_lengths_walk<<<grid_for(n, 256), 256, 0, st>>>(d_arena, d_h, n, words, d_len, longer);
+    S5_CUDA(cudaMemcpyAsync(X.h, longer, 8, cudaMemcpyDeviceToHost, st));
+    S5_CUDA(cudaStreamSynchronize(st));
+    if (X.h[0] == 0) return 0;
+    const uint64_t zs = zero_scratch_bytes(arena_len);
+    if (int rc = aux_reserve(X, zs + align_up(arena_len * 8))) return rc;
+    char* scratch = static_cast<char*>(X.d);
+    auto* pos = reinterpret_cast<int64_t*>(scratch + zs);
+    uint64_t z = 0;
+    if (int rc = zero_positions(d_arena, arena_len, pos, 0, scratch, X.h, st, &z)) return rc;
+    k_lengths<<<grid_for(n, 256), 256, 0, st>>>(d_h, n, pos, z, d_len);
+    S5_CUDA(cudaGetLastError());
+    return 0;
 }
 }  // namespace
 
@@ -1193,17 +1221,7 @@ int s5_string_lengths(const uint8_t* d_arena, uint64_t arena_len, const int64_t*
     if (n == 0) return 0;
     AuxScratch& X = aux();
     std::lock_guard<std::mutex> lock(X.mu);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const uint64_t zs = zero_scratch_bytes(arena_len);
-    // zero positions: at most one per arena byte
-    if (int rc = aux_reserve(X, zs + align_up(arena_len * 8))) return rc;
-    char* scratch = static_cast<char*>(X.d);
-    auto* pos = reinterpret_cast<int64_t*>(scratch + zs);
-    uint64_t z = 0;
-    if (int rc = zero_positions(d_arena, arena_len, pos, 0, scratch, X.h, st, &z)) return rc;
-    k_lengths<<<grid_for(n, 256), 256, 0, st>>>(d_handles, n, pos, z, d_len);
-    S5_CUDA(cudaGetLastError());
-    return 0;
+    return lengths_into(X, d_arena, arena_len, d_handles, n, d_len, static_cast<cudaStream_t>(stream));
 }
 
 int s5_materialize(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_sorted, uint64_t n,
@@ -1215,19 +1233,20 @@ int s5_materialize(const uint8_t* d_arena, uint64_t arena_len, const int64_t* d_
     AuxScratch& X = aux();
     std::lock_guard<std::mutex> lock(X.mu);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const uint64_t zs = zero_scratch_bytes(arena_len);
     const uint64_t nb = (n + 1023) / 1024;
-    const uint64_t need = zs + align_up(arena_len * 8) + align_up(n * 8) + align_up(nb * 8) +
-                          align_up((nb + 1) * 8);
-    if (int rc = aux_reserve(X, need)) return rc;
-    char* scratch = static_cast<char*>(X.d);
-    auto* pos = reinterpret_cast<int64_t*>(scratch + zs);
-    auto* len = reinterpret_cast<int64_t*>(scratch + zs + align_up(arena_len * 8));
+    // lengths and prefix sums in their own buffer (lengths_into reuses the aux scratch)
+    const uint64_t need = align_up(n * 8) + align_up(nb * 8) + align_up((nb + 1) * 8);
+    if (need > X.bytes2) {
+        if (X.d2) cudaFree(X.d2);
+        X.d2 = nullptr;
+        X.bytes2 = 0;
+        S5_CUDA(cudaMalloc(&X.d2, need));
+        X.bytes2 = need;
+    }
+    auto* len = static_cast<int64_t*>(X.d2);
     auto* tot = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(len) + align_up(n * 8));
     auto* bb = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(tot) + align_up(nb * 8));
-    uint64_t z = 0;
-    if (int rc = zero_positions(d_arena, arena_len, pos, 0, scratch, X.h, st, &z)) return rc;
-    k_lengths<<<grid_for(n, 256), 256, 0, st>>>(d_sorted, n, pos, z, len);
+    if (int rc = lengths_into(X, d_arena, arena_len, d_sorted, n, len, st)) return rc;
     // exclusive prefix of (length + 1): the new handles
     k_scan_len_block<<<nb, 1024, 0, st>>>(len, n, d_out_handles, tot);
     k_scan_small<unsigned long long><<<1, 1024, 0, st>>>(tot, nb, bb);
@@ -1336,10 +1355,11 @@ int s5_release_caches(void) {
         std::lock_guard<std::mutex> l(X.mu);
         cudaSetDevice(kv.first);
         if (X.d) cudaFree(X.d);
+        if (X.d2) cudaFree(X.d2);
         if (X.h) cudaFreeHost(X.h);
-        X.d = nullptr;
+        X.d = X.d2 = nullptr;
         X.h = nullptr;
-        X.bytes = 0;
+        X.bytes = X.bytes2 = 0;
     }
     for (auto& kv : registry<PartScratch>()) {
         PartScratch& X = kv.second;

@@ -2246,25 +2246,52 @@ __global__ void __launch_bounds__(kPartThreads) k_part_scatter(
 constexpr uint32_t kScanThreads = 256;
 constexpr uint32_t kScanChunk = 16384;  // bytes per CTA, 64 per thread
 
+// SWAR masks over the 8 bytes of a little-endian word: bit 7 of byte i set
+// iff byte i is 0 (exact: no borrow-induced false positives above a real
+// zero matter because every flagged byte is recomputed per byte below)
+__device__ __forceinline__ uint64_t zero_bytes(uint64_t w) {
+    // exact per-byte zero test: (b | (b + 0x7F)) has bit 7 clear iff b == 0
+    const uint64_t low7 = 0x7F7F7F7F7F7F7F7Full;
+    return ~(((w & low7) + low7) | w | low7);
+}
+
 // ingest: raw bytes -> arena (newline -> 0), terminators counted per CTA,
 // first embedded 0 byte recorded; mode 0 = ingest (copy + convert),
-// mode 1 = count zeros of an existing arena
+// mode 1 = count zeros of an existing arena.  64 bytes per thread, read and
+// written as 8-byte words (the chunk bases are 64-byte aligned; the tail of
+// the input is handled bytewise).
 template <int MODE>
 __global__ void __launch_bounds__(kScanThreads) k_term_count(
         const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t len,
         uint32_t* __restrict__ counts, unsigned long long* __restrict__ first_nul) {
-    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanChunk;
-    const uint64_t lo = base + threadIdx.x * (kScanChunk / kScanThreads);
-    const uint64_t hi = min(len, lo + kScanChunk / kScanThreads);
+    constexpr uint32_t B = kScanChunk / kScanThreads;  // 64
+    const uint64_t lo = static_cast<uint64_t>(blockIdx.x) * kScanChunk + threadIdx.x * B;
+    const uint64_t hi = min(len, lo + B);
     uint32_t c = 0;
-    for (uint64_t i = lo; i < hi; ++i) {
-        uint8_t x = src[i];
-        if (MODE == 0) {
-            if (x == 0) atomicMin(first_nul, static_cast<unsigned long long>(i));
-            if (x == '\n') x = 0;
-            dst[i] = x;
+    if (hi == lo + B) {
+        const uint64_t* s8 = reinterpret_cast<const uint64_t*>(src + lo);
+#pragma unroll
+        for (uint32_t q = 0; q < B / 8; ++q) {
+            uint64_t w = s8[q];
+            if (MODE == 0) {
+                const uint64_t z = zero_bytes(w);
+                if (z) atomicMin(first_nul, static_cast<unsigned long long>(lo + 8 * q + (__ffsll(z) - 1) / 8));
+                const uint64_t nl = zero_bytes(w ^ 0x0A0A0A0A0A0A0A0Aull);  // '\n' bytes
+                w &= ~((nl >> 7) * 0xFFull);
+                reinterpret_cast<uint64_t*>(dst + lo)[q] = w;
+            }
+            c += __popcll(zero_bytes(w));
         }
-        c += x == 0;
+    } else {
+        for (uint64_t i = lo; i < hi; ++i) {
+            uint8_t x = src[i];
+            if (MODE == 0) {
+                if (x == 0) atomicMin(first_nul, static_cast<unsigned long long>(i));
+                if (x == '\n') x = 0;
+                dst[i] = x;
+            }
+            c += x == 0;
+        }
     }
     c = __reduce_add_sync(0xffffffffu, c);
     __shared__ uint32_t ws[kScanThreads / 32];
@@ -2317,11 +2344,26 @@ __global__ void __launch_bounds__(1024) k_scan_small(const T* __restrict__ in, u
 __global__ void __launch_bounds__(kScanThreads) k_term_write(
         const uint8_t* __restrict__ a, uint64_t len, const unsigned long long* __restrict__ block_base,
         int64_t* __restrict__ pos, int64_t shift) {
-    const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanChunk;
-    const uint64_t lo = base + threadIdx.x * (kScanChunk / kScanThreads);
-    const uint64_t hi = min(len, lo + kScanChunk / kScanThreads);
+    constexpr uint32_t B = kScanChunk / kScanThreads;
+    const uint64_t lo = static_cast<uint64_t>(blockIdx.x) * kScanChunk + threadIdx.x * B;
+    const uint64_t hi = min(len, lo + B);
+    const bool full = hi == lo + B;
+    uint64_t zm[B / 8];
     uint32_t c = 0;
-    for (uint64_t i = lo; i < hi; ++i) c += a[i] == 0;
+#pragma unroll
+    for (uint32_t q = 0; q < B / 8; ++q) {
+        uint64_t z = 0;
+        if (full) {
+            z = zero_bytes(reinterpret_cast<const uint64_t*>(a + lo)[q]);
+        } else {
+            for (uint32_t b = 0; b < 8; ++b) {
+                const uint64_t i = lo + 8 * q + b;
+                if (i < hi && a[i] == 0) z |= 0x80ull << (8 * b);
+            }
+        }
+        zm[q] = z;
+        c += __popcll(z);
+    }
     // exclusive prefix of the thread counts in position order
     uint32_t incl = c;
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -2335,8 +2377,45 @@ __global__ void __launch_bounds__(kScanThreads) k_term_write(
     uint32_t before = 0;
     for (uint32_t q = 0; q < w; ++q) before += ws[q];
     unsigned long long k = block_base[blockIdx.x] + before + incl - c;
-    for (uint64_t i = lo; i < hi; ++i)
-        if (a[i] == 0) pos[k++] = static_cast<int64_t>(i) + shift;
+#pragma unroll
+    for (uint32_t q = 0; q < B / 8; ++q) {
+        uint64_t z = zm[q];
+        while (z) {
+            const uint32_t bit = __ffsll(z) - 1;
+            pos[k++] = static_cast<int64_t>(lo + 8 * q + bit / 8) + shift;
+            z &= z - 1;
+        }
+    }
+}
+
+// length of strings that end within `words` 8-byte words of their start
+// (SWAR walk); the others get -1 and are counted in *longer for the search
+__global__ void k_lengths_walk(const uint8_t* __restrict__ arena, const int64_t* __restrict__ h,
+                               uint64_t n, uint32_t words, int64_t* __restrict__ len,
+                               unsigned long long* __restrict__ longer) {
+    unsigned long long nl = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t p = static_cast<uint64_t>(h[i]);
+        uint64_t a = p & ~7ull;
+        uint64_t w = *reinterpret_cast<const uint64_t*>(arena + a);
+        w |= (1ull << (8 * (p - a))) - 1;  // bytes before the start are not terminators
+        int64_t L = -1;
+#pragma unroll 1
+        for (uint32_t q = 0; q < words; ++q) {
+            const uint64_t z = zero_bytes(w);
+            if (z) {
+                L = static_cast<int64_t>(a + (__ffsll(z) - 1) / 8 - p);
+                break;
+            }
+            a += 8;
+            w = *reinterpret_cast<const uint64_t*>(arena + a);
+        }
+        len[i] = L;
+        nl += L < 0;
+    }
+    for (uint32_t x = 16; x > 0; x >>= 1) nl += __shfl_xor_sync(0xffffffffu, nl, x);
+    if ((threadIdx.x & 31) == 0 && nl) atomicAdd(longer, nl);
 }
 
 // length of every string: distance to the first terminator at or after it
@@ -2344,6 +2423,7 @@ __global__ void k_lengths(const int64_t* __restrict__ h, uint64_t n, const int64
                           uint64_t nterm, int64_t* __restrict__ len) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
          i += uint64_t(gridDim.x) * blockDim.x) {
+        if (len[i] >= 0) continue;  // found by the short walk
         const int64_t x = h[i];
         uint64_t lo = 0, hi = nterm;
         while (lo < hi) {
