@@ -51,14 +51,17 @@ typedef struct {
     uint32_t classifier;  /* 0 = "unroll", 1 = "equal" (samplesort.py:43)      */
     uint32_t small_max;   /* segments <= small_max: warp base case (<= 32)      */
     uint32_t narrow_max;  /* segments <= narrow_max: one-CTA S^5 step (<=16384; 0: 4096 = off) */
-    uint32_t flags;       /* bit0: skip LCP fix-up (debug); bit1: per-kernel timing; bit2: no common-prefix
-                           * skip; bit3: partial-prefix skip; bit4: bitonic local sort; bit5: TMA-staged scatter at every level; bit7: 2048-tile TMA scatter below the root;
-                           * bit6: separate gather pass at level 0 */
+    uint32_t flags;       /* bit0: skip the LCP fix-up (debug); bit1: per-kernel timing;
+                           * bit2: no common-prefix skip; bit3: also skip partial prefixes
+                           * of >= 4 bytes; bit4: bitonic local sort (power-of-two network);
+                           * bit5: bulk-copy (TMA) scatter at every level; bit6: separate
+                           * gather pass at level 0; bit7: 2048-tile bulk-copy scatter below
+                           * the root */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
     uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (511)  */
     uint32_t wide_target; /* multi-CTA steps aim at children of this size (0: local_max / 8) */
-    uint32_t local_target; /* one-CTA steps aim at inner buckets of this size (0: 8) */
+    uint32_t local_target; /* unused since the local tier sorts whole segments (ABI) */
 } s5_config;
 
 /* Per-call statistics (Counters, counters.py:8-37; SURVEY 8(d) n_p log). */
