@@ -12,7 +12,8 @@ import subprocess
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libs5.so")
+# S5_LIB: an alternative build of the same library (A/B timing of kernel variants)
+SO_PATH = os.environ.get("S5_LIB") or os.path.join(_HERE, "libs5.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 S5_ARENA_PAD = 128
