@@ -488,8 +488,10 @@ struct HostPath {
     std::mutex mu;
     void* dbuf = nullptr;
     uint64_t dbytes = 0;
-    void* stage[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    static constexpr int kStages = 3;
+    void* stage[kStages] = {};
+    cudaEvent_t ev[kStages] = {};
+    uint64_t piece = 0;  // elements per staged piece (S5_HOST_PIECE overrides)
     unsigned long long* dmax = nullptr;
     unsigned long long* hmax = nullptr;
     void* xbuf = nullptr;  // narrowing scratch of the standalone transfer entries
@@ -508,7 +510,10 @@ struct PartScratch {  // s5_partition
 
 int host_path_init(HostPath& H) {
     if (H.stage[0]) return 0;
-    for (int i = 0; i < 2; ++i) {
+    const char* e = getenv("S5_HOST_PIECE");
+    H.piece = e ? strtoull(e, nullptr, 10) : (8ull << 20);
+    H.piece = std::max<uint64_t>(1, std::min(H.piece, HostPath::kChunk / 8));
+    for (int i = 0; i < HostPath::kStages; ++i) {
         S5_CUDA(cudaHostAlloc(&H.stage[i], HostPath::kChunk, cudaHostAllocDefault));
         S5_CUDA(cudaEventCreateWithFlags(&H.ev[i], cudaEventDisableTiming));
     }
@@ -532,13 +537,14 @@ int host_scratch(HostPath& H, uint64_t bytes) {
 int host_upload(HostPath& H, const int64_t* h_handles, uint64_t n, uint64_t arena_len,
                 uint32_t* d32, int64_t* dh, cudaStream_t st) {
     Pool& pool = Pool::get();
-    const uint64_t per = HostPath::kChunk / 4;
+    const uint64_t per = H.piece;
+    constexpr int NS = HostPath::kStages;
     std::atomic<bool> bad{false};
     uint64_t ci = 0;
     for (uint64_t off = 0; off < n; off += per, ++ci) {
         const uint64_t len = std::min(per, n - off);
-        const int b = static_cast<int>(ci & 1);
-        if (ci >= 2) S5_CUDA(cudaEventSynchronize(H.ev[b]));
+        const int b = static_cast<int>(ci % NS);
+        if (ci >= NS) S5_CUDA(cudaEventSynchronize(H.ev[b]));
         uint32_t* s32 = static_cast<uint32_t*>(H.stage[b]);
         const int64_t* src = h_handles + off;
         pool.par_for(len, [&](uint64_t a, uint64_t e) {
@@ -560,7 +566,8 @@ int host_download(HostPath& H, const int64_t* dh, uint64_t n, const int64_t* dl,
                   uint32_t* d32, void* dn, int64_t* h_handles, int64_t* h_lcp, cudaStream_t st,
                   uint64_t* bytes) {
     Pool& pool = Pool::get();
-    const uint64_t per = HostPath::kChunk / 4;
+    const uint64_t per = H.piece;
+    constexpr int NS = HostPath::kStages;
     if (n) k_shrink<uint32_t><<<grid_for(n, 256), 256, 0, st>>>(dh, d32, n);
     uint32_t w = 8;
     if (dl && h_lcp && nl) {
@@ -583,24 +590,24 @@ int host_download(HostPath& H, const int64_t* dh, uint64_t n, const int64_t* dl,
                           std::min(per, n - off), 4});
     if (dl && h_lcp && nl) {
         const char* src = w == 8 ? reinterpret_cast<const char*>(dl) : static_cast<const char*>(dn);
-        const uint64_t pl = HostPath::kChunk / w;
-        for (uint64_t off = 0; off < nl; off += pl)
-            pieces.push_back({src + off * w, h_lcp + off, std::min(pl, nl - off), w});
+        for (uint64_t off = 0; off < nl; off += per)
+            pieces.push_back({src + off * w, h_lcp + off, std::min(per, nl - off), w});
     }
     *bytes = n * 4 + (dl && h_lcp ? nl * w : 0);
     if (pieces.empty()) return 0;
     auto issue = [&](uint64_t k) -> int {
-        int b = static_cast<int>(k & 1);
+        int b = static_cast<int>(k % NS);
         S5_CUDA(cudaMemcpyAsync(H.stage[b], pieces[k].d, pieces[k].count * pieces[k].w,
                                 cudaMemcpyDeviceToHost, st));
         S5_CUDA(cudaEventRecord(H.ev[b], st));
         return 0;
     };
-    if (int e = issue(0)) return e;
+    for (uint64_t k = 0; k + 1 < NS && k < pieces.size(); ++k)
+        if (int e = issue(k)) return e;
     for (uint64_t k = 0; k < pieces.size(); ++k) {
-        if (k + 1 < pieces.size())
-            if (int e = issue(k + 1)) return e;
-        const int b = static_cast<int>(k & 1);
+        if (k + NS - 1 < pieces.size())
+            if (int e = issue(k + NS - 1)) return e;
+        const int b = static_cast<int>(k % NS);
         S5_CUDA(cudaEventSynchronize(H.ev[b]));
         const Piece P = pieces[k];
         const void* sp = H.stage[b];
@@ -1339,7 +1346,7 @@ int s5_release_caches(void) {
         if (H.xbuf) cudaFree(H.xbuf);
         if (H.dmax) cudaFree(H.dmax);
         if (H.hmax) cudaFreeHost(H.hmax);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < HostPath::kStages; ++i) {
             if (H.stage[i]) cudaFreeHost(H.stage[i]);
             if (H.ev[i]) cudaEventDestroy(H.ev[i]);
             H.stage[i] = nullptr;
