@@ -56,7 +56,8 @@ typedef struct {
                            * of >= 4 bytes; bit4: bitonic local sort (power-of-two network);
                            * bit5: bulk-copy (TMA) scatter at every level; bit6: separate
                            * gather pass at level 0; bit7: 2048-tile bulk-copy scatter below
-                           * the root */
+                           * the root; bit8: never carry second key words from the root
+                           * to level 1 (otherwise chosen from the root sample) */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
     uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (511)  */

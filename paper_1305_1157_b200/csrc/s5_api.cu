@@ -104,7 +104,7 @@ int resolve(const s5_config* c, Cfg* o) {
 uint64_t align_up(uint64_t x, uint64_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
-    uint64_t off[2], key[2], lists[2][NCLS], cta_start, tree_off, hist_off, tree_pool, hist_pool,
+    uint64_t off[2], key[2], key2[2], lists[2][NCLS], cta_start, tree_off, hist_off, tree_pool, hist_pool,
         ctl, hints, bkt, total;
     uint32_t cap[NCLS];
     uint64_t tree_cap, hist_cap;
@@ -142,6 +142,7 @@ Layout make_layout(uint64_t n, const Cfg& c) {
     L.hints = take(n * sizeof(uint2));
     L.bkt = take(n * 2);
     L.ctl = take(sizeof(Ctl));
+    for (int s = 0; s < 2; ++s) L.key2[s] = take(n > c.narrow_max ? n * 8 : 0);
     L.total = at;
     return L;
 }
@@ -678,7 +679,9 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     for (int s = 0; s < 2; ++s) {
         A.off[s] = reinterpret_cast<uint32_t*>(ws + L.off[s]);
         A.key[s] = reinterpret_cast<uint64_t*>(ws + L.key[s]);
+        A.key2[s] = reinterpret_cast<uint64_t*>(ws + L.key2[s]);
     }
+    A.k2_depth = static_cast<uint32_t>(depth);
     A.out = d_handles;
     A.lcp = d_lcp;
     A.hint_list = reinterpret_cast<uint2*>(ws + L.hints);
@@ -744,6 +747,9 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         S5_CUDA(cudaMemcpyAsync(hp.ctl, A.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         S5_CUDA(cudaStreamSynchronize(st));
         Ctl h = *hp.ctl;
+        // second key words: gathered at the root, read at level 1 when the root
+        // tree chose to carry them (ctl->k2)
+        A.k2_stage = !fuse_root ? 0u : level == 0 ? 1u : (level == 1 && h.k2) ? 2u : 0u;
         if (h.err & ERR_RANGE) return fail(S5_E_RANGE, "handle outside the arena");
         if (h.err & ERR_LIST) return fail(S5_E_INTERNAL, "segment list overflow");
         if (h.err & ERR_POOL) return fail(S5_E_INTERNAL, "wide pool overflow");
@@ -845,7 +851,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
                 k_wide_scatter_tma<512, 2048>
                     <<<ub, 512, WideTmaSmem<2048>::bytes(c.wide_dcap), st>>>(A, P);
             else
-                k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::bytes(c.wide_dcap), st>>>(A, P);
+                k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::bytes(c.wide_dcap, A.k2_stage != 0), st>>>(A, P);
             prof.end();
         }
         if (m[NARROW]) {

@@ -36,7 +36,7 @@ struct Ctl {
     unsigned long long fetches;   // arena key gathers
     unsigned long long hints;     // boundary LCP hints appended to the hint list
     uint32_t wide_ctas;           // plan: CTAs of the current wide launch
-    uint32_t pad;
+    uint32_t k2;                  // root tree: carry second key words to level 1
     unsigned long long tree_words, hist_words;  // plan: pool use of the current level
 };
 
@@ -67,6 +67,15 @@ struct SortArgs {
     uint64_t seed;
     const int64_t* root;   // level 0 only: the caller's handles (gather fused into the count)
     uint64_t arena_len;
+    // Second key words (string bytes depth+8..depth+15), gathered by the root
+    // count while its reads are in arena order and carried to level 1, whose
+    // equality buckets then need no random arena refetch.  k2_stage: 1 at the
+    // root (count fills key2[0], scatter carries it to key2[1]), 2 at level 1
+    // (scatter reads key2[1] for segments still at the root depth).  Active
+    // only when the root tree set ctl->k2 (k_wide_tree's estimate).
+    uint64_t* key2[2];
+    uint32_t k2_stage;
+    uint32_t k2_depth;
 };
 
 constexpr uint32_t kNarrowThreads = 512;
@@ -354,6 +363,36 @@ __device__ __forceinline__ void place(const SortArgs& A, const Seg& s, uint32_t 
         A.off[ns][dst] = o;
         A.key[ns][dst] = k;
     }
+}
+
+// place() of the root and level-1 scatters when second key words are live
+// (mode 1: root, mode 2: level 1; src = the string's absolute source index)
+__device__ __forceinline__ void place_k2(const SortArgs& A, const Seg& s, uint32_t b, bool fin,
+                                         uint32_t p, uint32_t bucket_end, uint32_t o, uint64_t k,
+                                         uint32_t mode, uint32_t src, unsigned long long& fetches) {
+    if (!mode) {
+        place(A, s, b, fin, p, bucket_end, o, k, fetches);
+        return;
+    }
+    const uint32_t dst = s.begin + p;
+    const uint32_t ns = s.side ^ 1u;
+    if (fin) {
+        A.out[dst] = o;
+        if ((b & 1) && A.lcp && p + 1 < bucket_end) A.lcp[dst] = s.depth + zero_index(k);
+    } else if (b & 1) {  // equality bucket: its next key is the carried word
+        A.off[ns][dst] = o;
+        A.key[ns][dst] = A.key2[mode - 1][src];
+    } else {
+        A.off[ns][dst] = o;
+        A.key[ns][dst] = k;
+        if (mode == 1) A.key2[1][dst] = A.key2[0][src];
+    }
+}
+
+__device__ __forceinline__ uint32_t k2_mode(const SortArgs& A, const Seg& s) {
+    if (!A.k2_stage || !A.ctl->k2) return 0;
+    if (A.k2_stage == 1) return 1;
+    return s.depth == A.k2_depth ? 2u : 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -1541,6 +1580,9 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_tree(SortArgs A, WidePlan
     while (M < m) M <<= 1;
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
     const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
+    __shared__ uint32_t bytemask[8][8];  // root: byte values seen per key position
+    if (threadIdx.x < 64) bytemask[threadIdx.x >> 3][threadIdx.x & 7] = 0;
+    __syncthreads();
     for (uint32_t t = threadIdx.x; t < M; t += kWideThreads) {
         uint64_t x = ~0ull;
         if (t < m) {
@@ -1552,10 +1594,31 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_tree(SortArgs A, WidePlan
             } else {
                 x = key[idx];
             }
+            if (A.k2_stage == 1 && t < 256) {  // 256 random samples suffice for the estimate
+#pragma unroll
+                for (uint32_t j = 0; j < 8; ++j) {
+                    const uint32_t v = static_cast<uint32_t>(x >> (56 - 8 * j)) & 0xFFu;
+                    atomicOr(&bytemask[j][v >> 5], 1u << (v & 31));
+                }
+            }
         }
         sample[t] = x;
     }
     __syncthreads();
+    if (A.k2_stage == 1 && threadIdx.x == 0) {
+        // distinct 8-byte keys <= product of the distinct byte values per
+        // position; far fewer than the strings -> level 1 is dominated by
+        // equality buckets, whose next words are cheapest to read now
+        double est = 1.0;
+        for (uint32_t j = 0; j < 8; ++j) {
+            uint32_t c = 0;
+            for (uint32_t q = 0; q < 8; ++q) c += __popc(bytemask[j][q]);
+            est *= c ? c : 1;
+        }
+        // (and only when the root's children will be wide steps themselves)
+        A.ctl->k2 = (A.flags & 256) == 0 && static_cast<double>(s.size) > 16.0 * est &&
+                    s.size / (g.v + 1) > A.narrow_max;
+    }
     sort_sample<kWideThreads>(sample, M);
     uint64_t* tree = P.tree_pool + P.tree_off[blockIdx.x];
     build_tree_levels<kWideThreads>(sample, m, g.d, tree, na, nb, nf);
@@ -1581,6 +1644,50 @@ __device__ __forceinline__ uint32_t find_seg(const uint32_t* cta_start, uint32_t
 // Per-CTA histogram of a contiguous chunk (stage 2, samplesort.py:383-400).
 // Every string's bucket is kept (u16, 2 B) so the scatter does not classify
 // again.
+// Level 0 of k_wide_count with second key words: handle -> (offset, key,
+// next word) gather fused with the classification and the histogram.
+template <bool K2>
+__device__ __forceinline__ void root_gather_count(const SortArgs& A, const Seg& s, uint32_t lo,
+                                                  uint32_t hi, const LutTree& T, uint32_t* hist,
+                                                  uint16_t* __restrict__ bkt) {
+    constexpr int R = 4;  // (8 would lift the whole count kernel's register budget)
+#pragma unroll 1
+    for (uint32_t base = lo; base < hi; base += R * kWideThreads) {
+        int64_t hh[R];
+        uint64_t kk[R], k2w[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const uint32_t i = base + j * kWideThreads + threadIdx.x;
+            hh[j] = i < hi ? __ldcs(A.root + s.begin + i) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const uint32_t i = base + j * kWideThreads + threadIdx.x;
+            if (i < hi && (hh[j] < 0 || static_cast<uint64_t>(hh[j]) + s.depth >= A.arena_len)) {
+                atomicOr(&A.ctl->err, ERR_RANGE);
+                hh[j] = 0;
+            }
+            kk[j] = k2w[j] = 0;
+            if (i < hi) {
+                if (K2) load_key2(A.arena, static_cast<uint64_t>(hh[j]) + s.depth, kk[j], k2w[j]);
+                else kk[j] = load_key(A.arena, static_cast<uint64_t>(hh[j]) + s.depth);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const uint32_t i = base + j * kWideThreads + threadIdx.x;
+            if (i < hi) {
+                A.off[0][s.begin + i] = static_cast<uint32_t>(hh[j]);
+                A.key[0][s.begin + i] = kk[j];
+                if (K2) A.key2[0][s.begin + i] = k2w[j];
+                const uint32_t b = classify_lut(kk[j], T);
+                atomicAdd(&hist[b], 1u);
+                bkt[i] = static_cast<uint16_t>(b);
+            }
+        }
+    }
+}
+
 template <bool EQUAL>
 __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePlan P) {
     extern __shared__ __align__(16) uint8_t sm[];
@@ -1616,34 +1723,38 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
         T.pf = tsrc[2 * g.v + 1 + kLutTabWords];
         T.lb = static_cast<uint32_t>(tsrc[2 * g.v + 1 + kLutTabWords + 1]);
         if (A.root) {  // level 0: handle -> (offset, key) gather fused with the count
-            constexpr int R = 8;
+            if (A.k2_stage == 1 && A.ctl->k2) {
+                root_gather_count<true>(A, s, lo, hi, T, hist, bkt);
+            } else {
+                constexpr int R = 8;
 #pragma unroll 1
-            for (uint32_t base = lo; base < hi; base += R * kWideThreads) {
-                int64_t hh[R];
-                uint64_t kk[R];
+                for (uint32_t base = lo; base < hi; base += R * kWideThreads) {
+                    int64_t hh[R];
+                    uint64_t kk[R];
 #pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    const uint32_t i = base + j * kWideThreads + threadIdx.x;
-                    hh[j] = i < hi ? __ldcs(A.root + s.begin + i) : 0;
-                }
-#pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    const uint32_t i = base + j * kWideThreads + threadIdx.x;
-                    if (i < hi && (hh[j] < 0 || static_cast<uint64_t>(hh[j]) + s.depth >= A.arena_len)) {
-                        atomicOr(&A.ctl->err, ERR_RANGE);
-                        hh[j] = 0;
+                    for (int j = 0; j < R; ++j) {
+                        const uint32_t i = base + j * kWideThreads + threadIdx.x;
+                        hh[j] = i < hi ? __ldcs(A.root + s.begin + i) : 0;
                     }
-                    kk[j] = i < hi ? load_key(A.arena, static_cast<uint64_t>(hh[j]) + s.depth) : 0;
-                }
 #pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    const uint32_t i = base + j * kWideThreads + threadIdx.x;
-                    if (i < hi) {
-                        A.off[0][s.begin + i] = static_cast<uint32_t>(hh[j]);
-                        A.key[0][s.begin + i] = kk[j];
-                        const uint32_t b = classify_lut(kk[j], T);
-                        atomicAdd(&hist[b], 1u);
-                        bkt[i] = static_cast<uint16_t>(b);
+                    for (int j = 0; j < R; ++j) {
+                        const uint32_t i = base + j * kWideThreads + threadIdx.x;
+                        if (i < hi && (hh[j] < 0 || static_cast<uint64_t>(hh[j]) + s.depth >= A.arena_len)) {
+                            atomicOr(&A.ctl->err, ERR_RANGE);
+                            hh[j] = 0;
+                        }
+                        kk[j] = i < hi ? load_key(A.arena, static_cast<uint64_t>(hh[j]) + s.depth) : 0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < R; ++j) {
+                        const uint32_t i = base + j * kWideThreads + threadIdx.x;
+                        if (i < hi) {
+                            A.off[0][s.begin + i] = static_cast<uint32_t>(hh[j]);
+                            A.key[0][s.begin + i] = kk[j];
+                            const uint32_t b = classify_lut(kk[j], T);
+                            atomicAdd(&hist[b], 1u);
+                            bkt[i] = static_cast<uint16_t>(b);
+                        }
                     }
                 }
             }
@@ -1764,10 +1875,11 @@ __global__ void __launch_bounds__(256) k_wide_bscan(SortArgs A, WidePlan P) {
 // whole sectors) instead of one scattered 4 B + 8 B store per string.
 struct WideScatterSmem {
     static constexpr uint32_t kcap = 2u << kWideDMax;
-    static constexpr uint32_t total = (3 * kcap + 8) * 4 + kWideTile * (8 + 4 + 2) + 64 * 4;
-    // shared memory for a launch whose trees have depth <= dcap
-    __host__ __device__ static constexpr uint32_t bytes(uint32_t dcap) {
-        return (3 * (2u << dcap) + 8) * 4 + kWideTile * (8 + 4 + 2) + 64 * 4;
+    static constexpr uint32_t total = (3 * kcap + 8) * 4 + kWideTile * (8 + 4 + 2 + 2) + 64 * 4;
+    // shared memory for a launch whose trees have depth <= dcap (k2: with the
+    // tile's source indices for second key words)
+    __host__ __device__ static constexpr uint32_t bytes(uint32_t dcap, bool k2) {
+        return (3 * (2u << dcap) + 8) * 4 + kWideTile * (8 + 4 + 2 + (k2 ? 2 : 0)) + 64 * 4;
     }
 };
 
@@ -1778,8 +1890,9 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
     uint64_t* sk = reinterpret_cast<uint64_t*>(sm);
     uint32_t* so = reinterpret_cast<uint32_t*>(sk + kWideTile);
     uint16_t* sb = reinterpret_cast<uint16_t*>(so + kWideTile);
+    uint16_t* sx = sb + kWideTile;  // tile-relative source index (second key words)
     const uint32_t kc = 2u << A.wide_dcap;
-    uint32_t* cur = reinterpret_cast<uint32_t*>(sb + kWideTile);
+    uint32_t* cur = reinterpret_cast<uint32_t*>(A.k2_stage ? sx + kWideTile : sx);
     uint32_t* cnt = cur + kc;
     uint32_t* gb = cnt + kc + 4;
     uint32_t* warp_sums = gb + kc + 4;
@@ -1803,6 +1916,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
     const uint16_t* __restrict__ bkt = P.bkt + s.begin;
     const uint32_t lane = threadIdx.x & 31;
     unsigned long long fetches = 0;
+    const uint32_t k2m = k2_mode(A, s);
     constexpr uint32_t IT = kWideTile / kWideThreads;
     uint64_t kk[IT];
     uint32_t oo[IT], br[IT];  // bucket | rank-in-tile << 16
@@ -1845,6 +1959,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
                 sk[p] = kk[j];
                 so[p] = oo[j];
                 sb[p] = static_cast<uint16_t>(b);
+                if (k2m) sx[p] = static_cast<uint16_t>(j * kWideThreads + threadIdx.x);
             }
         }
         if (base + kWideTile < hi) load_tile(base + kWideTile);
@@ -1856,7 +1971,10 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
             bool fin = r >> 31;
             uint32_t p = (r & 0x7FFFFFFFu) + (t - cnt[b]);
             uint32_t end = fin && (b & 1) ? starts[b + 1] : 0;
-            place(A, s, b, fin, p, end, so[t], sk[t], fetches);
+            if (k2m)
+                place_k2(A, s, b, fin, p, end, so[t], sk[t], k2m, s.begin + base + sx[t], fetches);
+            else
+                place(A, s, b, fin, p, end, so[t], sk[t], fetches);
         }
         __syncthreads();
     }
@@ -1963,6 +2081,7 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
     }
     constexpr uint32_t IT = kTmaTile / kTmaThreads;
     unsigned long long fetches = 0;
+    const uint32_t k2m = k2_mode(A, s);
     uint32_t t = 0;
 #pragma unroll 1
     for (uint32_t base = lo; base < hi; base += kTmaTile, ++t) {
@@ -2007,7 +2126,11 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
             const bool fin = r >> 31;
             const uint32_t p = (r & 0x7FFFFFFFu) + (q - cnt[b]);
             const uint32_t end = fin && (b & 1) ? starts[b + 1] : 0;
-            place(A, s, b, fin, p, end, S.off[e + sho], S.key[e + shk], fetches);
+            if (k2m)
+                place_k2(A, s, b, fin, p, end, S.off[e + sho], S.key[e + shk], k2m, s.begin + base + e,
+                         fetches);
+            else
+                place(A, s, b, fin, p, end, S.off[e + sho], S.key[e + shk], fetches);
         }
         __syncthreads();  // every read of this stage is done: refill it
         if (threadIdx.x == 0 && base + 2 * kTmaTile < hi) {

@@ -460,3 +460,35 @@ def test_identical_strings_equality_chain():
     _, lcp = sort_with_lcp(arena, h, cfg=SampleSortConfig(v=31), counters=ctr)
     assert ctr.get("parallel_steps") == 3
     assert np.all(lcp == 17)
+
+
+@pytest.mark.parametrize("alphabet", [b"AB", b"ACGT"])
+def test_second_key_words_carried_to_level1(alphabet):
+    """Few distinct 8-byte prefixes (n > 16 x the root sample's estimate):
+    the root gathers 16 bytes per string and level 1's equality buckets take
+    their next key from the carried word instead of the arena.  Same output as
+    the oracle and as the path with the carry disabled (flags bit8); fewer
+    arena key fetches."""
+    from paper_1305_1157_b200 import arena_from_strings
+    rng = np.random.default_rng(21)
+    n = 600_000 if len(alphabet) == 2 else 1_200_000
+    lens = rng.integers(8, 40, n)
+    sym = np.frombuffer(alphabet, np.uint8)[rng.integers(0, len(alphabet), int(lens.sum()))].tobytes()
+    strs, at = [], 0
+    for ln in lens.tolist():
+        strs.append(sym[at:at + ln])
+        at += ln
+    arena, h0 = arena_from_strings(strs)
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, O.max_threads())
+    want_lcp = O.adjacent_lcps(arena, want)
+    fetches = {}
+    for flags in (0, 256):
+        h = h0.copy()
+        ctr = Counters()
+        # (wide_v 63: the root's children are wide steps at these n)
+        cfg = SampleSortConfig(flags=flags, wide_v=63)
+        _, lcp = sort_with_lcp(arena, h, cfg=cfg, counters=ctr)
+        _check_sorted(arena, h0, h, want, lcp, want_lcp, f"flags{flags}")
+        fetches[flags] = ctr.get("fetches")
+    assert fetches[0] < fetches[256]
