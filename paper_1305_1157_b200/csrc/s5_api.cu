@@ -193,18 +193,58 @@ int init_attributes() {
     return rc;
 }
 
+// ctl and seq are mapped (zero-copy, usable from every device under UVA):
+// the level loop's control block is published by k_publish and read by a
+// host spin on seq instead of a copy + stream synchronisation
 struct Pinned {
     Ctl* ctl = nullptr;
     long long* ll = nullptr;
+    uint32_t* seq = nullptr;
+    uint32_t next = 0;
 };
 
 Pinned& pinned() {
     thread_local Pinned p;
     if (!p.ctl) {
-        cudaHostAlloc(&p.ctl, sizeof(Ctl), cudaHostAllocDefault);
+        const unsigned fl = cudaHostAllocMapped | cudaHostAllocPortable;
+        if (cudaHostAlloc(&p.ctl, sizeof(Ctl), fl) != cudaSuccess) p.ctl = nullptr;
+        if (cudaHostAlloc(&p.seq, 64, fl) != cudaSuccess) p.seq = nullptr;
         cudaHostAlloc(&p.ll, 64, cudaHostAllocDefault);
+        if (p.seq) *p.seq = 0;
     }
     return p;
+}
+
+// copy of the device control block into mapped host memory, then the
+// sequence number (system-scope fence between them)
+__global__ void k_publish(const Ctl* __restrict__ src, Ctl* dst, uint32_t* seq, uint32_t val) {
+    constexpr uint32_t W = sizeof(Ctl) / 4;
+    const uint32_t* a = reinterpret_cast<const uint32_t*>(src);
+    volatile uint32_t* b = reinterpret_cast<volatile uint32_t*>(dst);
+    for (uint32_t i = threadIdx.x; i < W; i += blockDim.x) b[i] = a[i];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t*>(seq) = val;
+}
+
+// wait for k_publish(val): spin on the mapped word; a failed stream ends the
+// wait with its error
+int wait_published(Pinned& hp, uint32_t val, cudaStream_t st) {
+    const volatile uint32_t* q = hp.seq;
+    for (uint32_t spins = 0; *q != val; ++spins) {
+        if ((spins & 1023) == 1023) {
+            const cudaError_t e = cudaStreamQuery(st);
+            if (e != cudaSuccess && e != cudaErrorNotReady)
+                return fail(S5_E_CUDA, "level kernels: %s", cudaGetErrorString(e));
+            if (e == cudaSuccess && *q != val)  // stream drained: the word must be there
+                return fail(S5_E_INTERNAL, "control block not published");
+        }
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return 0;
 }
 
 // One instance per CUDA device (the library's cached buffers live on the
@@ -665,7 +705,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     cudaStream_t st = static_cast<cudaStream_t>(stream_);
     char* ws = static_cast<char*>(d_ws);
     Pinned& hp = pinned();
-    if (!hp.ctl) return fail(S5_E_CUDA, "pinned host allocation failed");
+    if (!hp.ctl || !hp.seq) return fail(S5_E_CUDA, "pinned host allocation failed");
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (stats) {
@@ -744,9 +784,13 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     for (;; ++level) {
         prof.level = level;
         A.root = level == 0 && fuse_root ? d_handles : nullptr;
-        S5_CUDA(cudaMemcpyAsync(hp.ctl, A.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-        S5_CUDA(cudaStreamSynchronize(st));
-        Ctl h = *hp.ctl;
+        const uint32_t tag = ++hp.next;
+        k_publish<<<1, 32, 0, st>>>(A.ctl, hp.ctl, hp.seq, tag);
+        ++prof.launches;
+        S5_CUDA(cudaGetLastError());
+        if (int e = wait_published(hp, tag, st)) return e;
+        Ctl h;
+        memcpy(&h, hp.ctl, sizeof(Ctl));
         // second key words: gathered at the root, read at level 1 when the root
         // tree chose to carry them (ctl->k2)
         A.k2_stage = !fuse_root ? 0u : level == 0 ? 1u : (level == 1 && h.k2) ? 2u : 0u;
