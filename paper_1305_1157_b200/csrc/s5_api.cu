@@ -57,6 +57,10 @@ struct Cfg {
     uint64_t seed;
 };
 
+#ifndef S5_ROOT_STAGES
+#define S5_ROOT_STAGES 3
+#endif
+constexpr uint32_t kRootStages = S5_ROOT_STAGES;  // bulk-copy stages of the root scatter
 constexpr uint32_t kLocalThreads = 512;   // segments of <= 4096 strings
 using LocalCfg = LocalSmem<kLocalThreads>;
 constexpr uint32_t kLocalXSThreads = 64;  // <= 512
@@ -149,6 +153,7 @@ Layout make_layout(uint64_t n, const Cfg& c) {
 
 template <typename K>
 int set_smem(K kernel, int bytes) {
+    if (bytes > 232448) return fail(S5_E_CUDA, "shared memory request of %d bytes", bytes);
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess)
         return fail(S5_E_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(e));
@@ -183,6 +188,8 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_wide_count<true>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_scatter, WideScatterSmem::total);
         if (!rc) rc = set_smem(k_wide_scatter_tma<1024, 4096>, WideTmaSmem<4096>::bytes(kWideDMax));
+        if (!rc) rc = set_smem(k_wide_scatter_tma<1024, 4096, kRootStages>,
+                               WideTmaSmem<4096, kRootStages>::bytes(kWideDMax));
         if (!rc) rc = set_smem(k_wide_scatter_tma<512, 2048>, WideTmaSmem<2048>::bytes(kWideDMax));
         if (!rc) rc = set_smem(k_build_tree, 227 * 1024);
         if (!rc) rc = set_smem(k_local<kLocalThreads>, LocalCfg::total);
@@ -889,8 +896,8 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             // tiles) and for small segments (2048, three CTAs per SM); register-
             // staged 4096-string tiles at two CTAs per SM in between
             if ((c.flags & 32) || m[WIDE] <= 8)
-                k_wide_scatter_tma<1024, 4096>
-                    <<<ub, 1024, WideTmaSmem<4096>::bytes(c.wide_dcap), st>>>(A, P);
+                k_wide_scatter_tma<1024, 4096, kRootStages>
+                    <<<ub, 1024, WideTmaSmem<4096, kRootStages>::bytes(c.wide_dcap), st>>>(A, P);
             else if ((c.flags & 128) || h.elems[WIDE] < uint64_t(m[WIDE]) * 32768)  // small segments
                 k_wide_scatter_tma<512, 2048>
                     <<<ub, 512, WideTmaSmem<2048>::bytes(c.wide_dcap), st>>>(A, P);

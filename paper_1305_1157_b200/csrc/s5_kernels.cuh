@@ -1995,12 +1995,12 @@ struct TmaStage {
     uint16_t bkt[TILE + 8];
 };
 
-template <uint32_t TILE>
+template <uint32_t TILE, uint32_t NS = 2>
 struct WideTmaSmem {
-    // stages | perm u16[tile] | cur, cnt, gb u32[kc] | warp sums | 2 mbarriers
+    // NS stages | perm u16[tile] | cur, cnt, gb u32[kc] | warp sums | NS mbarriers
     __host__ __device__ static constexpr uint32_t bytes(uint32_t dcap) {
-        return 2 * static_cast<uint32_t>(sizeof(TmaStage<TILE>)) + TILE * 2 +
-               (3 * (2u << dcap) + 8) * 4 + 64 * 4 + 16;
+        return NS * static_cast<uint32_t>(sizeof(TmaStage<TILE>)) + TILE * 2 +
+               (3 * (2u << dcap) + 8) * 4 + 64 * 4 + 8 * NS;
     }
 };
 
@@ -2027,7 +2027,7 @@ __device__ __forceinline__ uint32_t elem_shift(const void* src, uint32_t size) {
     return static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) & 15) / size);
 }
 
-template <uint32_t THREADS, uint32_t TILE>
+template <uint32_t THREADS, uint32_t TILE, uint32_t NS = 2>
 __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePlan P) {
     constexpr uint32_t kTmaThreads = THREADS, kTmaTile = TILE;
     using TmaStage = s5::TmaStage<TILE>;
@@ -2035,7 +2035,7 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;
     TmaStage* stage = reinterpret_cast<TmaStage*>(sm);
-    uint16_t* perm = reinterpret_cast<uint16_t*>(sm + 2 * sizeof(TmaStage));
+    uint16_t* perm = reinterpret_cast<uint16_t*>(sm + NS * sizeof(TmaStage));
     const uint32_t kc = 2u << A.wide_dcap;
     uint32_t* cur = reinterpret_cast<uint32_t*>(perm + kTmaTile);
     uint32_t* cnt = cur + kc;
@@ -2065,7 +2065,7 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
                      :: "r"(smem_u32(&bar[buf])), "r"(tx) : "memory");
     };
     if (threadIdx.x == 0) {
-        for (int q = 0; q < 2; ++q)
+        for (uint32_t q = 0; q < NS; ++q)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" :: "r"(smem_u32(&bar[q])) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -2075,17 +2075,15 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
         cur[b] = (st + rows[static_cast<uint64_t>(c) * g.k + b]) | (fin ? 0x80000000u : 0u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        if (lo < hi) issue(lo, 0);
-        if (lo + kTmaTile < hi) issue(lo + kTmaTile, 1);
-    }
+    if (threadIdx.x == 0)
+        for (uint32_t q = 0; q < NS; ++q)
+            if (lo + q * kTmaTile < hi) issue(lo + q * kTmaTile, q);
     constexpr uint32_t IT = kTmaTile / kTmaThreads;
     unsigned long long fetches = 0;
     const uint32_t k2m = k2_mode(A, s);
-    uint32_t t = 0;
+    uint32_t t = 0, buf = 0, phase = 0;
 #pragma unroll 1
     for (uint32_t base = lo; base < hi; base += kTmaTile, ++t) {
-        const uint32_t buf = t & 1;
         const uint32_t m = min(kTmaTile, hi - base);
         const uint32_t shk = elem_shift(key + base, 8), sho = elem_shift(off + base, 4),
                        shb = elem_shift(bkt + base, 2);
@@ -2093,7 +2091,7 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
         // wait for the tile's bytes
         asm volatile(
             "{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-            " @!p bra W%=;\n}\n" :: "r"(smem_u32(&bar[buf])), "r"((t >> 1) & 1) : "memory");
+            " @!p bra W%=;\n}\n" :: "r"(smem_u32(&bar[buf])), "r"(phase) : "memory");
         __syncthreads();
         const TmaStage& S = stage[buf];
         uint32_t br[IT];  // bucket | rank-in-tile << 16
@@ -2133,9 +2131,13 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
                 place(A, s, b, fin, p, end, S.off[e + sho], S.key[e + shk], fetches);
         }
         __syncthreads();  // every read of this stage is done: refill it
-        if (threadIdx.x == 0 && base + 2 * kTmaTile < hi) {
+        if (threadIdx.x == 0 && base + NS * kTmaTile < hi) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            issue(base + 2 * kTmaTile, buf);
+            issue(base + NS * kTmaTile, buf);
+        }
+        if (++buf == NS) {  // stage ring: parity flips each time it wraps
+            buf = 0;
+            phase ^= 1u;
         }
     }
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
