@@ -868,7 +868,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             k_wide_plan<<<1, 1024, 0, st>>>(A, P);
             prof.end();
             prof.begin(S5_K_WIDE_TREE);
-            k_wide_tree<<<m[WIDE], kWideThreads, wide_tree_smem(c), st>>>(A, P);
+            k_wide_tree<<<m[WIDE], kTreeThreads, wide_tree_smem(c), st>>>(A, P);
             prof.end();
             // upper bound on CTAs; surplus CTAs exit on ctl->wide_ctas
             uint32_t ub = static_cast<uint32_t>(std::min<uint64_t>(
