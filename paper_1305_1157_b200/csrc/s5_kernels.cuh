@@ -1181,7 +1181,10 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         const uint32_t o = off1[slot];
         const uint32_t r0 = run_begin(rb, p), r1 = run_end(rb, p);
         const uint32_t g = r1 - r0;
-        const bool rexact = exact || g <= kTruncFix;  // keys of the run are equal
+        // keys of the run are equal: exact words, a re-ranked short run, or a
+        // terminator inside the bytes the truncated words kept whole ([0, L+6):
+        // the run's strings are then identical -- short duplicates finish here)
+        const bool rexact = exact || g <= kTruncFix || zero_index(k) < L + 6;
         const uint32_t dst = s.begin + p;
         if (A.lcp && p + 1 == r1 && r1 < s.size)
             A.lcp[dst] = depth + diff_bytes(k, key1[(perm[r1])]);
@@ -1419,7 +1422,7 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
             const uint32_t o = W.off1[slot];
             const uint32_t r0 = run_begin(rb, p), r1 = run_end(rb, p);
             const uint32_t g = r1 - r0;
-            const bool rexact = exact || g <= kTruncFix;
+            const bool rexact = exact || g <= kTruncFix || zero_index(k) < L + 6;  // as in k_local
             const uint32_t dst = s.begin + p;
             if (A.lcp && p + 1 == r1 && r1 < s.size)
                 A.lcp[dst] = depth + diff_bytes(k, W.key1[W.perm[r1]]);
