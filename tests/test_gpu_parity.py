@@ -492,3 +492,29 @@ def test_second_key_words_carried_to_level1(alphabet):
         _check_sorted(arena, h0, h, want, lcp, want_lcp, f"flags{flags}")
         fetches[flags] = ctr.get("fetches")
     assert fetches[0] < fetches[256]
+
+
+@pytest.mark.parametrize("n_dup", [40, 100, 700])
+def test_duplicate_short_strings_in_truncated_segments(n_dup):
+    """A local segment with no common prefix (truncated sort words) holding
+    long runs of identical short strings: the runs finish in the segment
+    (terminator inside the compared bytes), next to longer strings that share
+    those short strings as prefixes."""
+    from paper_1305_1157_b200 import arena_from_strings
+    rng = np.random.default_rng(n_dup)
+    strs = []
+    for w in (b"a", b"ab", b"abcdef", b"\x7f", b"zzzzz"):
+        strs += [w] * n_dup
+    for _ in range(1500):
+        ln = int(rng.integers(1, 14))
+        strs.append(bytes(rng.integers(33, 127, ln, dtype=np.uint8)))
+    strs += [b"abcdefg", b"abcdefgh", b"abcdef\x01"] * 30
+    order = rng.permutation(len(strs))
+    arena, h0 = arena_from_strings([strs[i] for i in order])
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, 2)
+    want_lcp = O.adjacent_lcps(arena, want)
+    for cfg in (SampleSortConfig(), SampleSortConfig(local_max=256, narrow_max=256, small_max=8)):
+        h = h0.copy()
+        _, lcp = sort_with_lcp(arena, h, cfg=cfg)
+        _check_sorted(arena, h0, h, want, lcp, want_lcp, f"dup{n_dup}")
