@@ -171,6 +171,10 @@ def run_distributed(args):
     from paper_1305_1157_b200.distributed import GpuBackend, distributed_sample_sort
     from paper_1305_1157_b200.strings import first_unsorted
 
+    if "RANK" not in os.environ:  # one-rank smoke run without torchrun
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
