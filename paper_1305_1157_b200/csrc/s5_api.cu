@@ -183,7 +183,8 @@ int init_attributes() {
     std::call_once(once, [] {
         rc = set_smem(k_narrow<false>, NarrowSmem::total);
         if (!rc) rc = set_smem(k_narrow<true>, NarrowSmem::total);
-        if (!rc) rc = set_smem(k_wide_tree, kWideTreeSmem);
+        if (!rc) rc = set_smem(k_wide_tree<kTreeThreads>, kWideTreeSmem);
+        if (!rc) rc = set_smem(k_wide_tree<kTreeThreadsFew>, kWideTreeSmem);
         if (!rc) rc = set_smem(k_wide_count<false>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_count<true>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_scatter, WideScatterSmem::total);
@@ -868,7 +869,10 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             k_wide_plan<<<1, 1024, 0, st>>>(A, P);
             prof.end();
             prof.begin(S5_K_WIDE_TREE);
-            k_wide_tree<<<m[WIDE], kTreeThreads, wide_tree_smem(c), st>>>(A, P);
+            if (m[WIDE] <= 8)  // few segments: one CTA's sample sort is the level's critical path
+                k_wide_tree<kTreeThreadsFew><<<m[WIDE], kTreeThreadsFew, wide_tree_smem(c), st>>>(A, P);
+            else
+                k_wide_tree<kTreeThreads><<<m[WIDE], kTreeThreads, wide_tree_smem(c), st>>>(A, P);
             prof.end();
             // upper bound on CTAs; surplus CTAs exit on ctl->wide_ctas
             uint32_t ub = static_cast<uint32_t>(std::min<uint64_t>(

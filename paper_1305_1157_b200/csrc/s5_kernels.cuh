@@ -1572,7 +1572,13 @@ __global__ void __launch_bounds__(1024) k_wide_plan(SortArgs A, WidePlan P) {
 #endif
 constexpr uint32_t kTreeThreads = S5_TREE_THREADS;  // one CTA per wide segment
 
-__global__ void __launch_bounds__(kTreeThreads) k_wide_tree(SortArgs A, WidePlan P) {
+// TT threads per CTA: kTreeThreads in general, kTreeThreadsFew for levels
+// with few wide segments (the root), where the one CTA's sample sort is on
+// the critical path of the level
+constexpr uint32_t kTreeThreadsFew = 1024;
+
+template <uint32_t TT>
+__global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P) {
     extern __shared__ __align__(16) uint8_t sm[];
     if (A.ctl->wide_ctas == 0) return;
     const uint32_t dw = A.dmax < A.wide_dcap ? A.dmax : A.wide_dcap;
@@ -1591,7 +1597,7 @@ __global__ void __launch_bounds__(kTreeThreads) k_wide_tree(SortArgs A, WidePlan
     __shared__ uint32_t bytemask[8][8];  // root: byte values seen per key position
     if (threadIdx.x < 64) bytemask[threadIdx.x >> 3][threadIdx.x & 7] = 0;
     __syncthreads();
-    for (uint32_t t = threadIdx.x; t < M; t += kTreeThreads) {
+    for (uint32_t t = threadIdx.x; t < M; t += TT) {
         uint64_t x = ~0ull;
         if (t < m) {
             const uint32_t idx = sample_index(sseed, t, s.size);
@@ -1627,12 +1633,12 @@ __global__ void __launch_bounds__(kTreeThreads) k_wide_tree(SortArgs A, WidePlan
         A.ctl->k2 = (A.flags & 256) == 0 && static_cast<double>(s.size) > 16.0 * est &&
                     s.size / (g.v + 1) > A.narrow_max;
     }
-    sort_sample<kTreeThreads>(sample, M);
+    sort_sample<TT>(sample, M);
     uint64_t* tree = P.tree_pool + P.tree_off[blockIdx.x];
-    build_tree_levels<kTreeThreads>(sample, m, g.d, tree, na, nb, nf);
+    build_tree_levels<TT>(sample, m, g.d, tree, na, nb, nf);
     // classification table for k_wide_count, once per segment
     uint64_t* spl = tree + g.v + 1;
-    const LutTree T = lut_build<kTreeThreads>(tree, g.d, spl, reinterpret_cast<uint16_t*>(spl + g.v));
+    const LutTree T = lut_build<TT>(tree, g.d, spl, reinterpret_cast<uint16_t*>(spl + g.v));
     if (threadIdx.x == 0) {
         spl[g.v + kLutTabWords] = T.pf;
         spl[g.v + kLutTabWords + 1] = T.lb;
