@@ -886,7 +886,9 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             prof.end();
             dim3 cg(m[WIDE], ((2u << std::min(c.dmax, c.wide_dcap)) + 31) / 32);
             prof.begin(S5_K_WIDE_COLSCAN);
-            if (m[WIDE] <= 32)  // few, large segments: many rows per column
+            if (m[WIDE] <= 8)  // the root: 8 buckets per CTA, so ~kc/8 CTAs share the rows
+                k_wide_colscan_g<32, 8><<<dim3(m[WIDE], cg.y * 4), 1024, 0, st>>>(A, P);
+            else if (m[WIDE] <= 32)  // few, large segments: many rows per column
                 k_wide_colscan<32><<<cg, 1024, 0, st>>>(A, P);
             else
                 k_wide_colscan<8><<<cg, 256, 0, st>>>(A, P);

@@ -1869,6 +1869,53 @@ __global__ void __launch_bounds__(NW * 32) k_wide_colscan(SortArgs A, WidePlan P
     }
 }
 
+// The same scan with BW < 32 buckets per CTA, for levels with few wide
+// segments (the root: C ~ 1000 rows x k ~ 1000 buckets would otherwise be
+// ~32 CTAs on the level's critical path).  A warp reads G = 32 / BW rows at
+// a time (BW consecutive buckets each, whole sectors for BW >= 8); the rows'
+// running prefix is a shuffle scan over the G row lanes of each bucket.
+template <uint32_t NW, uint32_t BW>
+__global__ void __launch_bounds__(NW * 32) k_wide_colscan_g(SortArgs A, WidePlan P) {
+    constexpr uint32_t G = 32 / BW;
+    __shared__ uint32_t part[NW][BW];
+    if (A.ctl->wide_ctas == 0) return;
+    const uint32_t si = blockIdx.x;
+    const Seg s = P.segs[si];
+    const WideGeom g = wide_geom(s, A);
+    if (blockIdx.y * BW >= g.k) return;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t sub = lane / BW, col = lane % BW, b = blockIdx.y * BW + col;
+    uint32_t* rows = P.hist_pool + P.hist_off[si];
+    const uint32_t R = (g.C + NW - 1) / NW;
+    const uint32_t r0 = min(g.C, w * R), r1 = min(g.C, r0 + R);
+    uint32_t sum = 0;
+    if (b < g.k) {
+#pragma unroll 4
+        for (uint32_t c = r0 + sub; c < r1; c += G) sum += rows[static_cast<uint64_t>(c) * g.k + b];
+    }
+#pragma unroll
+    for (uint32_t o = BW; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (sub == 0) part[w][col] = sum;
+    __syncthreads();
+    uint32_t run = 0;
+    for (uint32_t q = 0; q < w; ++q) run += part[q][col];
+    for (uint32_t c0 = r0; c0 < r1; c0 += G) {  // warp-uniform
+        const uint32_t c = c0 + sub;
+        const bool ok = b < g.k && c < r1;
+        const uint64_t at = static_cast<uint64_t>(c) * g.k + b;
+        const uint32_t x = ok ? rows[at] : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (uint32_t o = BW; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (ok) rows[at] = run + inc - x;
+        run += __shfl_sync(0xffffffffu, inc, (G - 1) * BW + col);
+    }
+    if (w == NW - 1 && sub == 0 && b < g.k) rows[static_cast<uint64_t>(g.C) * g.k + b] = run;
+}
+
 // Bucket starts (stage 3) and the per-bucket epilogue (children, LCP hints).
 __global__ void __launch_bounds__(256) k_wide_bscan(SortArgs A, WidePlan P) {
     __shared__ uint32_t warp_sums[32];
