@@ -795,6 +795,13 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         const uint32_t tag = ++hp.next;
         k_publish<<<1, 32, 0, st>>>(A.ctl, hp.ctl, hp.seq, tag);
         ++prof.launches;
+        // the wide plan reads this level's segment count on the device, so it
+        // runs while the host waits for the published control block
+        P.segs = reinterpret_cast<const Seg*>(ws + L.lists[cur][WIDE]);
+        P.nsegs = 0;
+        prof.begin(S5_K_WIDE_PLAN);
+        k_wide_plan<<<1, 1024, 0, st>>>(A, P);
+        prof.end();
         S5_CUDA(cudaGetLastError());
         if (int e = wait_published(hp, tag, st)) return e;
         Ctl h;
@@ -804,7 +811,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         A.k2_stage = !fuse_root ? 0u : level == 0 ? 1u : (level == 1 && h.k2) ? 2u : 0u;
         if (h.err & ERR_RANGE) return fail(S5_E_RANGE, "handle outside the arena");
         if (h.err & ERR_LIST) return fail(S5_E_INTERNAL, "segment list overflow");
-        if (h.err & ERR_POOL) return fail(S5_E_INTERNAL, "wide pool overflow");
+        if ((h.err | h.plan_err) & ERR_POOL) return fail(S5_E_INTERNAL, "wide pool overflow");
         fetches_total = h.fetches;
         hints_total = h.hints;
         uint32_t m[NCLS];
@@ -865,9 +872,6 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         if (m[WIDE]) {
             P.segs = segs[WIDE];
             P.nsegs = m[WIDE];
-            prof.begin(S5_K_WIDE_PLAN);
-            k_wide_plan<<<1, 1024, 0, st>>>(A, P);
-            prof.end();
             prof.begin(S5_K_WIDE_TREE);
             if (m[WIDE] <= 8)  // few segments: one CTA's sample sort is the level's critical path
                 k_wide_tree<kTreeThreadsFew><<<m[WIDE], kTreeThreadsFew, wide_tree_smem(c), st>>>(A, P);

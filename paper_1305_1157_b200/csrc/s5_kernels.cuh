@@ -38,6 +38,8 @@ struct Ctl {
     uint32_t wide_ctas;           // plan: CTAs of the current wide launch
     uint32_t k2;                  // root tree: carry second key words to level 1
     unsigned long long tree_words, hist_words;  // plan: pool use of the current level
+    uint32_t plan_err;            // plan: ERR_POOL (sticky; the plan runs before the level's reset)
+    uint32_t pad_;
 };
 
 enum : uint32_t { ERR_RANGE = 1, ERR_LIST = 2, ERR_POOL = 4 };
@@ -1505,15 +1507,18 @@ __device__ __forceinline__ WideGeom wide_geom(const Seg& s, const SortArgs& A) {
 
 // Exclusive scans of CTA counts and pool sizes over the wide segments.
 __global__ void __launch_bounds__(1024) k_wide_plan(SortArgs A, WidePlan P) {
+    // the level's wide segment count straight from the control block: the
+    // plan is enqueued before the host has read it (overlapping the level gap)
+    const uint32_t nsegs = A.ctl->n_list[WIDE];
     __shared__ unsigned long long s_carry[3];
     __shared__ unsigned long long s_w[3][32];
     if (threadIdx.x == 0) s_carry[0] = s_carry[1] = s_carry[2] = 0;
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (uint32_t base = 0; base < P.nsegs; base += 1024) {
+    for (uint32_t base = 0; base < nsegs; base += 1024) {
         uint32_t i = base + threadIdx.x;
         unsigned long long x[3] = {0, 0, 0};
-        if (i < P.nsegs) {
+        if (i < nsegs) {
             WideGeom g = wide_geom(P.segs[i], A);
             x[0] = g.C;
             x[1] = 2 * g.v + 1 + kLutWords;
@@ -1541,7 +1546,7 @@ __global__ void __launch_bounds__(1024) k_wide_plan(SortArgs A, WidePlan P) {
             }
         }
         __syncthreads();
-        if (i < P.nsegs) {
+        if (i < nsegs) {
             unsigned long long e[3];
             for (int q = 0; q < 3; ++q)
                 e[q] = s_carry[q] + incl[q] - x[q] + (w ? s_w[q][w - 1] : 0ull);
@@ -1555,12 +1560,12 @@ __global__ void __launch_bounds__(1024) k_wide_plan(SortArgs A, WidePlan P) {
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        P.cta_start[P.nsegs] = static_cast<uint32_t>(s_carry[0]);
+        P.cta_start[nsegs] = static_cast<uint32_t>(s_carry[0]);
         A.ctl->wide_ctas = static_cast<uint32_t>(s_carry[0]);
         A.ctl->tree_words = s_carry[1];
         A.ctl->hist_words = s_carry[2];
         if (s_carry[1] > P.tree_cap || s_carry[2] > P.hist_cap) {
-            atomicOr(&A.ctl->err, ERR_POOL);
+            atomicOr(&A.ctl->plan_err, ERR_POOL);
             A.ctl->wide_ctas = 0;  // skip the level's wide kernels; host reports the error
         }
     }
