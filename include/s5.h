@@ -57,7 +57,10 @@ typedef struct {
                            * bit5: bulk-copy (TMA) scatter at every level; bit6: separate
                            * gather pass at level 0; bit7: 2048-tile bulk-copy scatter below
                            * the root; bit8: never carry second key words from the root
-                           * to level 1 (otherwise chosen from the root sample) */
+                           * to level 1 (otherwise chosen from the root sample); bit9: the
+                           * input handles are n u32 offsets packed into the first 4n bytes
+                           * of d_handles (the multi-GPU exchange payload); the output is
+                           * still n int64 handles in d_handles (n >= 2) */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
     uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (511)  */
@@ -219,6 +222,11 @@ int s5_build_tree(const uint64_t *d_sorted_sample, uint32_t m, uint32_t v,
  * (SURVEY 8(d) recipe 5). */
 int s5_host_markov_text(const double *cdf, const double *u, uint64_t n, uint32_t sigma,
                         uint8_t *out);
+
+/* Host helper for the config-3 generator: dst[dst_start[i] + j] =
+ * blob[src_start[i] + j] for j < lengths[i], i < m (host worker threads). */
+int s5_host_copy_pieces(uint8_t *dst, const int64_t *dst_start, const int64_t *src_start,
+                        const int64_t *lengths, const uint8_t *blob, uint64_t m);
 
 /* Frees the library's cached device buffers, pinned staging and side
  * streams on every device (no call may be in flight); they are re-created

@@ -127,6 +127,7 @@ SIGNATURES = {
     "s5_classify": (C.c_int, [_vp, _u64, _vp, _u32, _u32, _vp, _vp]),
     "s5_build_tree": (C.c_int, [_vp, _u32, _u32, _vp, _vp, _vp]),
     "s5_host_markov_text": (C.c_int, [_vp, _vp, _u64, _u32, _vp]),
+    "s5_host_copy_pieces": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _u64]),
     "s5_last_error": (C.c_char_p, []),
     "s5_version": (C.c_int, []),
 }

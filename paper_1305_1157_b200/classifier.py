@@ -9,8 +9,11 @@ functions here expose the same device code as operation surfaces:
   device tree builder (classifier.py:85-126);
 - ``classify_tree_unrolled`` / ``classify_tree_equal`` run the device
   classifiers (classifier.py:259-278);
-- ``build_tree`` and ``bucket_layout`` are the small host-side bookkeeping
-  records of the reference (classifier.py:159-176, :284-304).
+- ``build_tree`` is the host-side record of a tree (classifier.py:159-176).
+
+The bucket layout (boundaries, depth gains, finished flags;
+classifier.py:284-304) exists only on the device: ``k_wide_bscan`` and
+``emit_block`` in csrc/s5_kernels.cuh (audited by the Eq. (1) tests).
 """
 
 from __future__ import annotations
@@ -48,24 +51,6 @@ class SplitterTree:
     @property
     def num_buckets(self) -> int:
         return 2 * self.in_order.size + 1
-
-
-@dataclass
-class BucketLayout:
-    """classifier.py:56-61."""
-    counts: np.ndarray
-    boundaries: np.ndarray
-    depth_delta: np.ndarray
-    finished: np.ndarray
-
-
-def effective_v(v_max: int, segment_size: int) -> int:
-    """classifier.py:67-73."""
-    m = max(1, segment_size // 2)
-    x = (1 << m.bit_length()) - 1
-    if x > m:
-        x >>= 1
-    return max(1, min(v_max, x))
 
 
 def _depth_of(v: int) -> int:
@@ -177,20 +162,3 @@ def classify_tree_lut(keys, tree: SplitterTree, out=None):
     """Table over the 12 key bits after the splitters' common prefix + binary
     search: the classifier of the multi-CTA count kernel (same buckets)."""
     return _classify(keys, tree, 2, out)
-
-
-def bucket_layout(counts, tree: SplitterTree, parent_depth: int) -> BucketLayout:
-    """Boundaries, depth gains and finished flags (classifier.py:284-304)."""
-    v = tree.v
-    k = 2 * v + 1
-    counts = np.asarray(counts, np.int64)
-    boundaries = np.zeros(k + 1, np.int64)
-    np.cumsum(counts, out=boundaries[1:])
-    delta = np.zeros(k, np.int64)
-    delta[1::2] = WORD_CHARS
-    if v > 1:
-        inner = np.arange(2, 2 * v, 2)
-        delta[inner] = tree.splitter_lcp[inner // 2]
-    finished = np.zeros(k, np.bool_)
-    finished[1::2] = tree.terminated
-    return BucketLayout(counts, boundaries, delta, finished)

@@ -141,6 +141,10 @@ Layout make_layout(uint64_t n, const Cfg& c) {
     // ceil(size/64K) <= 296 rows of k <= size/4 counters (see choose_d)
     L.tree_cap = n / 4 + uint64_t(L.cap[WIDE]) * (2 + kLutWords) + 16;
     L.hist_cap = n + n / 2 + 3 * uint64_t(L.cap[WIDE]) + 65536;
+    if (const char* e = getenv("S5_TEST_POOL_WORDS")) {  // tests: force the overflow path
+        L.tree_cap = std::min<uint64_t>(L.tree_cap, strtoull(e, nullptr, 10));
+        L.hist_cap = std::min<uint64_t>(L.hist_cap, strtoull(e, nullptr, 10));
+    }
     L.tree_pool = take(L.tree_cap * 8);
     L.hist_pool = take(L.hist_cap * 4);
     L.hints = take(n * sizeof(uint2));
@@ -206,22 +210,45 @@ int init_attributes() {
 // host spin on seq instead of a copy + stream synchronisation
 struct Pinned {
     Ctl* ctl = nullptr;
-    long long* ll = nullptr;
     uint32_t* seq = nullptr;
     uint32_t next = 0;
+    ~Pinned() {  // thread exit (the mapped block is per thread)
+        if (ctl) cudaFreeHost(ctl);
+        if (seq) cudaFreeHost(seq);
+    }
 };
 
 Pinned& pinned() {
     thread_local Pinned p;
-    if (!p.ctl) {
+    if (!p.ctl || !p.seq) {
         const unsigned fl = cudaHostAllocMapped | cudaHostAllocPortable;
-        if (cudaHostAlloc(&p.ctl, sizeof(Ctl), fl) != cudaSuccess) p.ctl = nullptr;
-        if (cudaHostAlloc(&p.seq, 64, fl) != cudaSuccess) p.seq = nullptr;
-        cudaHostAlloc(&p.ll, 64, cudaHostAllocDefault);
+        if (!p.ctl && cudaHostAlloc(&p.ctl, sizeof(Ctl), fl) != cudaSuccess) p.ctl = nullptr;
+        if (!p.seq && cudaHostAlloc(&p.seq, 64, fl) != cudaSuccess) p.seq = nullptr;
         if (p.seq) *p.seq = 0;
     }
     return p;
 }
+
+// Serialises sorts on one device: the side streams and their fork/join
+// events (Side) are shared by every caller on the device, so one sort's
+// enqueue sequence must not interleave with another's.
+struct DevSortLock {
+    std::mutex mu;
+};
+
+// Error-path cleanup of sort_impl: timing events destroyed on every return;
+// on an error return the caller's stream is drained first, so no kernel of
+// the failed call is still reading the workspace when the caller reuses it.
+struct SortScope {
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool ok = false;
+    ~SortScope() {
+        if (!ok) cudaStreamSynchronize(st);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+};
 
 // copy of the device control block into mapped host memory, then the
 // sequence number (system-scope fence between them)
@@ -358,6 +385,12 @@ struct Prof {
         recs.clear();
     }
     size_t recs_total = 0;
+    ~Prof() {  // error returns: events of unfinished records
+        for (auto& r : recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+    }
 };
 
 }  // namespace
@@ -368,6 +401,7 @@ namespace {
 // chunk would cost more than the copies themselves).
 class Pool {
     std::vector<std::thread> th_;
+    std::mutex job_mu_;  // one job at a time: callers on other devices queue here
     std::mutex mu_;
     std::condition_variable go_, done_;
     std::function<void(unsigned)> job_;
@@ -417,6 +451,10 @@ public:
             f(0, n);
             return;
         }
+        // the job slot (job_, left_, gen_) belongs to one caller until every
+        // worker has finished its part: concurrent callers (threads driving
+        // different GPUs through the host paths) wait for it
+        std::lock_guard<std::mutex> job(job_mu_);
         auto part = [&, T](unsigned i) { f(n * i / T, n * (i + 1) / T); };
         {
             std::lock_guard<std::mutex> g(mu_);
@@ -715,12 +753,18 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     Pinned& hp = pinned();
     if (!hp.ctl || !hp.seq) return fail(S5_E_CUDA, "pinned host allocation failed");
 
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // one sort at a time per device (shared side streams); events and the
+    // stream drain of an error return handled by the scope
+    DevSortLock& dsl = per_device<DevSortLock>();
+    std::lock_guard<std::mutex> dev_lock(dsl.mu);
+    SortScope scope;
+    scope.st = st;
     if (stats) {
-        S5_CUDA(cudaEventCreate(&ev0));
-        S5_CUDA(cudaEventCreate(&ev1));
-        S5_CUDA(cudaEventRecord(ev0, st));
+        S5_CUDA(cudaEventCreate(&scope.ev0));
+        S5_CUDA(cudaEventCreate(&scope.ev1));
+        S5_CUDA(cudaEventRecord(scope.ev0, st));
     }
+    cudaEvent_t ev0 = scope.ev0, ev1 = scope.ev1;
 
     SortArgs A{};
     A.arena = d_arena;
@@ -776,10 +820,14 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     // kernel; otherwise a separate gather pass
     A.arena_len = arena_len;
     const bool fuse_root = !audit && !c.classifier && n > c.narrow_max && !(c.flags & 64);
+    // flags bit9: the input is n u32 offsets in the first 4n bytes of d_handles
+    // (the multi-GPU exchange payload); every level-0 read of it (tree sample,
+    // fused count or k_gather) completes before the first handle is written
+    const uint32_t* in32 = (c.flags & 512) ? reinterpret_cast<const uint32_t*>(d_handles) : nullptr;
     if (!fuse_root) {
         prof.begin(S5_K_GATHER, n);
-        k_gather<<<grid_for(n, 256), 256, 0, st>>>(d_handles, static_cast<uint32_t>(n), depth,
-                                                    arena_len, A);
+        k_gather<<<grid_for(n, 256), 256, 0, st>>>(d_handles, in32, static_cast<uint32_t>(n),
+                                                    depth, arena_len, A);
         prof.end();
     }
     prof.begin(S5_K_INIT);
@@ -791,7 +839,8 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     uint32_t level = 0;
     for (;; ++level) {
         prof.level = level;
-        A.root = level == 0 && fuse_root ? d_handles : nullptr;
+        A.root = level == 0 && fuse_root && !in32 ? d_handles : nullptr;
+        A.root32 = level == 0 && fuse_root ? in32 : nullptr;
         const uint32_t tag = ++hp.next;
         k_publish<<<1, 32, 0, st>>>(A.ctl, hp.ctl, hp.seq, tag);
         ++prof.launches;
@@ -811,6 +860,10 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         A.k2_stage = !fuse_root ? 0u : level == 0 ? 1u : (level == 1 && h.k2) ? 2u : 0u;
         if (h.err & ERR_RANGE) return fail(S5_E_RANGE, "handle outside the arena");
         if (h.err & ERR_LIST) return fail(S5_E_INTERNAL, "segment list overflow");
+        // plan_err is sticky and must be checked before the `!live` break: the
+        // plan of this level's wide segments ran before the host read the
+        // block, and when it overflowed (wide_ctas = 0) every wide kernel of
+        // the level skipped its work -- the sort must fail, not finish early
         if ((h.err | h.plan_err) & ERR_POOL) return fail(S5_E_INTERNAL, "wide pool overflow");
         fetches_total = h.fetches;
         hints_total = h.hints;
@@ -983,9 +1036,8 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         stats->boundary_lcps = hints_total;
     }
     prof.finish(stats);
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
     if (stats) stats->n_launch_recs = static_cast<uint32_t>(std::min<size_t>(prof.recs_total, S5_MAX_LAUNCH_RECS));
+    scope.ok = true;
     return 0;
 }
 
@@ -1398,6 +1450,15 @@ int s5_host_markov_text(const double* cdf, const double* u, uint64_t n, uint32_t
         a = b;
         b = s;
     }
+    return 0;
+}
+
+int s5_host_copy_pieces(uint8_t* dst, const int64_t* dst_start, const int64_t* src_start,
+                        const int64_t* lengths, const uint8_t* blob, uint64_t m) {
+    Pool::get().par_for(m, [&](uint64_t a, uint64_t b) {
+        for (uint64_t i = a; i < b; ++i)
+            memcpy(dst + dst_start[i], blob + src_start[i], static_cast<size_t>(lengths[i]));
+    });
     return 0;
 }
 

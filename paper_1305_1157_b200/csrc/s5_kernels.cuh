@@ -68,6 +68,7 @@ struct SortArgs {
     uint32_t flags;        // s5_config flags (bit2: no common-prefix skip)
     uint64_t seed;
     const int64_t* root;   // level 0 only: the caller's handles (gather fused into the count)
+    const uint32_t* root32; // ... or, with cfg flags bit9, the caller's handles as u32 offsets
     uint64_t arena_len;
     // Second key words (string bytes depth+8..depth+15), gathered by the root
     // count while its reads are in arena order and carried to level 1, whose
@@ -397,14 +398,20 @@ __device__ __forceinline__ uint32_t k2_mode(const SortArgs& A, const Seg& s) {
     return s.depth == A.k2_depth ? 2u : 0u;
 }
 
+// level-0 input handle i of the caller's array (int64, or u32 offsets with
+// cfg flags bit9 -- the multi-GPU exchange's payload), streamed once
+__device__ __forceinline__ int64_t root_handle(const SortArgs& A, uint32_t i) {
+    return A.root32 ? static_cast<int64_t>(__ldcs(A.root32 + i)) : __ldcs(A.root + i);
+}
+
 // ---------------------------------------------------------------------------
 // level 0: gather keys at the common depth (pack_keys, strings.py:176-182)
 
-__global__ void k_gather(const int64_t* __restrict__ handles, uint32_t n, uint64_t depth,
-                         uint64_t arena_len, SortArgs A) {
+__global__ void k_gather(const int64_t* __restrict__ handles, const uint32_t* __restrict__ h32,
+                         uint32_t n, uint64_t depth, uint64_t arena_len, SortArgs A) {
     uint32_t stride = gridDim.x * blockDim.x;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-        int64_t h = handles[i];
+        int64_t h = h32 ? static_cast<int64_t>(h32[i]) : handles[i];
         if (h < 0 || static_cast<uint64_t>(h) + depth >= arena_len) {
             atomicOr(&A.ctl->err, ERR_RANGE);
             h = 0;
@@ -1606,8 +1613,8 @@ __global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P) {
         uint64_t x = ~0ull;
         if (t < m) {
             const uint32_t idx = sample_index(sseed, t, s.size);
-            if (A.root) {  // level 0: keys are not gathered yet
-                const int64_t h = A.root[s.begin + idx];
+            if (A.root || A.root32) {  // level 0: keys are not gathered yet
+                const int64_t h = root_handle(A, s.begin + idx);
                 x = (h >= 0 && static_cast<uint64_t>(h) + s.depth < A.arena_len)
                         ? load_key(A.arena, static_cast<uint64_t>(h) + s.depth) : 0;
             } else {
@@ -1677,7 +1684,7 @@ __device__ __forceinline__ void root_gather_count(const SortArgs& A, const Seg& 
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             const uint32_t i = base + j * kWideThreads + threadIdx.x;
-            hh[j] = i < hi ? __ldcs(A.root + s.begin + i) : 0;
+            hh[j] = i < hi ? root_handle(A, s.begin + i) : 0;
         }
 #pragma unroll
         for (int j = 0; j < R; ++j) {
@@ -1741,7 +1748,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
         T.v = g.v;
         T.pf = tsrc[2 * g.v + 1 + kLutTabWords];
         T.lb = static_cast<uint32_t>(tsrc[2 * g.v + 1 + kLutTabWords + 1]);
-        if (A.root) {  // level 0: handle -> (offset, key) gather fused with the count
+        if (A.root || A.root32) {  // level 0: handle -> (offset, key) gather fused with the count
             if (A.k2_stage == 1 && A.ctl->k2) {
                 root_gather_count<true>(A, s, lo, hi, T, hist, bkt);
             } else {
@@ -1753,7 +1760,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
 #pragma unroll
                     for (int j = 0; j < R; ++j) {
                         const uint32_t i = base + j * kWideThreads + threadIdx.x;
-                        hh[j] = i < hi ? __ldcs(A.root + s.begin + i) : 0;
+                        hh[j] = i < hi ? root_handle(A, s.begin + i) : 0;
                     }
 #pragma unroll
                     for (int j = 0; j < R; ++j) {

@@ -144,6 +144,11 @@ def gen_config3(n: int = 1 << 24, seed: int = 3):
 
 def _scatter_pieces(data, dst_start, src_start, lengths, blob, chunk=1 << 22):
     """data[dst_start[i] + j] = blob[src_start[i] + j] for j < lengths[i]."""
+    try:
+        from . import _native
+        return _native.copy_pieces(data, dst_start, src_start, lengths, blob)
+    except ImportError:  # library not built: the numpy restatement
+        pass
     m = lengths.size
     for a in range(0, m, chunk):
         b = min(m, a + chunk)

@@ -16,10 +16,12 @@ contiguous slices of the global sorted order:
    grouped by destination -- one library call (``s5_partition``: a counting
    kernel with the splitters' keys in shared memory, a column scan, a
    scatter);
-4. ``all_to_all_single`` of the per-destination counts, then of the
-   handles (NCCL over NVLink on GPUs; gloo in the CPU tests);
-5. each rank sorts its received strings with the single-GPU sorter and
-   emits their LCP array;
+4. ``all_gather`` of the per-destination counts (every rank learns the
+   G x G matrix: its receive sizes and all slice sizes), then one
+   ``all_to_all_single`` of the handles as u32 offsets (NCCL over NVLink on
+   GPUs; gloo in the CPU tests);
+5. each rank sorts its received strings with the single-GPU sorter (which
+   reads the u32 payload in place) and emits their LCP array;
 6. the LCP across each rank boundary is one string comparison (the next
    rank's first handle is all-gathered).
 
@@ -129,6 +131,29 @@ class GpuBackend:
         _lib.check(rc, "s5_download")
         return hh, hl
 
+    def sort_u32(self, buf, n: int):
+        """Sort n u32 offsets packed into the first 4n bytes of the int64
+        tensor ``buf`` (the exchange payload); the sorted int64 handles land
+        in ``buf`` itself (s5_sort flags bit9).  Returns (handles, lcp)."""
+        import dataclasses
+
+        import torch
+        from . import _lib
+        from .samplesort import SampleSortConfig, gpu_sort
+        lcp = torch.empty(max(n - 1, 0), dtype=torch.int64, device=buf.device)
+        if getattr(self, "keep_input", False):  # bench.py's profiled re-run of the local sort
+            self.last_input = buf.view(torch.int32)[:n].to(torch.int64) & 0xFFFFFFFF
+        if n == 1:
+            buf.copy_(buf.view(torch.int32)[:1].to(torch.int64) & 0xFFFFFFFF)
+        if n > 1:
+            cfg = dataclasses.replace(self.cfg or SampleSortConfig())
+            cfg.flags |= 512
+            st = _lib.S5Stats()
+            gpu_sort(self.arena, buf, 0, cfg, lcp, stats=st)
+            self.launches += int(st.launches)
+            self.last_stats = st
+        return buf, lcp
+
     def sort(self, handles):
         """Sort a device int64 tensor in place; returns (handles, lcp)."""
         import torch
@@ -195,6 +220,13 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
     entry (absent on the last nonempty rank) is the LCP of slice[-1] and
     the next rank's first string, so concatenating all ranks' ``lcp``
     gives the global LCP array of length n-1.
+
+    Host round trips: the partition's group sizes (one small D2H inside
+    ``s5_partition``) and the G x G count matrix (one all-gather read on the
+    host, which sizes the receive buffer and gives every rank all slice
+    sizes); everything else stays on the device.  Handles cross the
+    interconnect as u32 offsets (arena < 4 GiB) and the local sort reads
+    them in place (``s5_sort`` flags bit9).
     """
     import torch
     import torch.distributed as dist
@@ -216,11 +248,10 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
         samp = torch.full((s,), -1, dtype=torch.int64, device=dev)
     allsamp = torch.empty(G * s, dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(allsamp, samp, group=group)
-    top = allsamp.max()
-    if int(top.item()) < 0:  # no strings on any rank
-        allsamp = allsamp[:0]
-    else:  # empty ranks' slots repeat a drawn handle (splitters stay strings)
-        allsamp = torch.where(allsamp >= 0, allsamp, top)
+    # empty ranks' slots repeat a drawn handle, so the splitters stay strings
+    # (no strings anywhere: handle 0, and every partition below is empty)
+    top = allsamp.max().clamp(min=0)
+    allsamp = torch.where(allsamp >= 0, allsamp, top)
 
     t = _mark("sample", t)
     # 2. identical splitters on every rank: sort by (string, handle)
@@ -228,44 +259,47 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
     t = _mark("splitters", t)
 
     # 3. destination of every local string, handles grouped by destination
-    if G == 1 or splitters.numel() == 0:  # one rank, or no strings on any rank
-        send, counts = h, [0] * (G - 1) + [n_local]
+    if G == 1:
+        send, counts = h, [n_local]
     else:
         send, counts = be.partition(h, splitters)
-    send_counts = torch.tensor(counts, dtype=torch.int64, device=dev)
     t = _mark("partition", t)
 
-    # 4. exchange counts, then handles
-    recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts, group=group)
-    recv = torch.empty(int(recv_counts.sum().item()), dtype=torch.int64, device=dev)
-    dist.all_to_all_single(recv, send, output_split_sizes=recv_counts.tolist(),
-                           input_split_sizes=send_counts.tolist(), group=group)
-
+    # 4. the G x G count matrix on every rank (row = source, column =
+    #    destination), then one exchange of u32 offsets
+    mine = torch.tensor(counts, dtype=torch.int64, device=dev)
+    allc = torch.empty(G * G, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allc, mine, group=group)
+    M = allc.view(G, G).tolist()
+    recv_sizes = [int(M[src][rank]) for src in range(G)]
+    slice_sizes = [sum(int(M[src][d]) for src in range(G)) for d in range(G)]
+    n_recv = slice_sizes[rank]
+    recv = torch.empty(n_recv, dtype=torch.int64, device=dev)
+    recv32 = recv.view(torch.int32)[:n_recv]  # the first 4 n_recv bytes
+    send32 = send.to(torch.int32)  # u32 offsets (bit pattern kept)
+    if G == 1:
+        recv32.copy_(send32)
+    else:
+        dist.all_to_all_single(recv32, send32, output_split_sizes=recv_sizes,
+                               input_split_sizes=[int(c) for c in counts], group=group)
     t = _mark("exchange", t)
-    # 5. local sort + LCP
-    recv, lcp = be.sort(recv)
+
+    # 5. local sort of the received u32 offsets (in place) + LCP
+    recv, lcp = be.sort_u32(recv, n_recv)
     t = _mark("local_sort", t)
 
-    # 6. boundary LCPs and global offsets: one all-gather of (size, first handle)
-    mine = torch.tensor([recv.numel(), -1], dtype=torch.int64, device=dev)
-    if recv.numel():
-        mine[1:] = recv[:1]
-    allm = torch.empty(2 * G, dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(allm, mine, group=group)
-    meta = allm.view(G, 2).tolist()
-    counts = [int(m[0]) for m in meta]
-    nxt = None
-    for r in range(rank + 1, G):
-        if counts[r]:
-            nxt = int(meta[r][1])
-            break
-    if recv.numel() and nxt is not None:
-        pair = torch.cat([recv[-1:], torch.tensor([nxt], dtype=torch.int64, device=dev)])
+    # 6. boundary LCP: the next nonempty rank's first handle (one all-gather;
+    #    which rank that is, every rank already knows from the count matrix)
+    first = recv[:1] if n_recv else torch.full((1,), -1, dtype=torch.int64, device=dev)
+    firsts = torch.empty(G, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(firsts, first.contiguous(), group=group)
+    nxt = next((r for r in range(rank + 1, G) if slice_sizes[r]), None)
+    if n_recv and nxt is not None:
+        pair = torch.cat([recv[-1:], firsts[nxt:nxt + 1]])
         lcp = torch.cat([lcp, be.lcp_pair(pair)])
-    offset = sum(counts[:rank])
+    offset = sum(slice_sizes[:rank])
     _mark("boundary", t)
-    return ShardResult(recv, lcp, offset, counts)
+    return ShardResult(recv, lcp, offset, slice_sizes)
 
 
 def _pick_splitters(be, samples, G: int):

@@ -78,9 +78,17 @@ _ws_cache: dict = {}
 
 
 def _workspace(nbytes: int, device):
+    """Cached device workspace per (device, calling thread): a sort's last
+    kernels may still be in flight on its stream when the call returns, so
+    concurrent callers (threads driving several GPUs, or several streams of
+    one GPU) never share a buffer."""
     import torch
-    key = str(device)
+    key = (str(device), threading.get_ident())
     with _ws_lock:
+        if len(_ws_cache) > 1:  # buffers of threads that have exited
+            alive = {t.ident for t in threading.enumerate()}
+            for k in [k for k in _ws_cache if k[1] not in alive]:
+                del _ws_cache[k]
         buf = _ws_cache.get(key)
         if buf is None or buf.numel() < nbytes:
             _ws_cache.pop(key, None)
@@ -216,8 +224,39 @@ def sample_sort(arena: StringArena, handles, depth: int = 0, cfg: SampleSortConf
 
 def parallel_sample_sort(arena: StringArena, handles, workers: int = 1,
                          cfg: SampleSortConfig | None = None, counters: Counters | None = None,
-                         audit=None, lcp_out=None):
-    """Fully parallel string sample sort (samplesort.py:437-444) on one B200."""
+                         audit=None, lcp_out=None, devices=None):
+    """Fully parallel string sample sort (samplesort.py:437-444).
+
+    ``workers`` is the number of GPUs (the reference's worker threads): with
+    ``workers > 1`` and several visible devices the sort runs on
+    ``min(workers, device_count)`` of them from this process (sample-sort
+    partitioning + peer copies, ``multi.multi_gpu_sort``); ``devices`` names
+    them explicitly (a device may repeat: several shards on one GPU).  One
+    GPU otherwise.  ``audit`` runs single-GPU."""
+    import torch
+    if devices is None and workers > 1 and torch.cuda.is_available():
+        devices = list(range(min(int(workers), torch.cuda.device_count())))
+    n = int(len(handles))
+    if audit is None and devices is not None and len(devices) > 1 and n > 1:
+        from .multi import multi_gpu_sort
+        on_device = isinstance(handles, torch.Tensor) and handles.is_cuda
+        if not on_device and (not isinstance(handles, np.ndarray) or handles.dtype != np.int64):
+            raise TypeError("handles must be a numpy int64 array or a CUDA int64 tensor")
+        if arena.size > 0xFFFFFFFF:
+            raise ValueError(f"arena of {arena.size} bytes: offsets are 32-bit (< 4 GiB)")
+        h = handles if on_device or (handles.flags.c_contiguous and handles.flags.writeable) \
+            else np.ascontiguousarray(handles)
+        lo = lcp_out
+        if lcp_out is not None and not on_device and not (
+                isinstance(lcp_out, np.ndarray) and lcp_out.dtype == np.int64
+                and lcp_out.flags.c_contiguous):
+            lo = np.empty(n - 1, np.int64)
+        multi_gpu_sort(arena, h, devices, cfg, lo, counters=counters)
+        if h is not handles:
+            handles[:] = h
+        if lo is not lcp_out:
+            lcp_out[: n - 1] = lo
+        return handles
     return _sort(arena, handles, 0, cfg, counters, audit, lcp_out)
 
 

@@ -74,3 +74,26 @@ def test_product_has_no_oracle_dependency():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "s5_oracle" not in src and "libs5oracle" not in src, f
+
+
+def test_copy_pieces_helper_matches_numpy():
+    import numpy as np
+    from paper_1305_1157_b200 import _native, datasets
+    rng = np.random.default_rng(1)
+    blob = rng.integers(0, 256, 5000, dtype=np.uint8)
+    m = 200_000  # above the helper's threading threshold
+    ln = rng.integers(0, 9, m)
+    src = rng.integers(0, blob.size - 8, m)
+    dst = np.concatenate([[0], np.cumsum(ln)[:-1]])
+    got = np.zeros(int(ln.sum()) + 1, np.uint8)
+    _native.copy_pieces(got, dst, src, ln, blob)
+    want = np.zeros_like(got)
+    rep = np.repeat(np.arange(m), ln)
+    within = np.arange(int(ln.sum())) - np.repeat(np.cumsum(ln) - ln, ln)
+    want[dst[rep] + within] = blob[src[rep] + within]
+    assert np.array_equal(got, want)
+    with pytest.raises(ValueError):
+        _native.copy_pieces(got, dst + got.size, src, ln, blob)
+    # config 3's generator through the helper still reproduces SURVEY's N
+    arena, h = datasets.generate(3, 1 << 12)
+    assert h.size == 1 << 12 and arena.data[-1] == 0

@@ -51,6 +51,11 @@ class OracleBackend:
     def lcp_pair(self, pair):
         return torch.from_numpy(O.adjacent_lcps(self.arena, pair.numpy()))
 
+    def sort_u32(self, buf, n):
+        h = buf.view(torch.int32)[:n].numpy().view(np.uint32).astype(np.int64)
+        buf[:n] = torch.from_numpy(h)
+        return self.sort(buf[:n])
+
     def sort(self, handles):
         h = handles.numpy().copy()
         O.parallel_sample_sort(self.arena, h, 1)
