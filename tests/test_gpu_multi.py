@@ -100,7 +100,7 @@ def test_workers_config5_handle_digest():
     dig, first = datasets.HANDLE_DIGESTS[5]
     assert hashlib.sha256(h.tobytes()).hexdigest()[:16] == dig
     assert h[:5].tolist() == first
-    assert O.digest_lcp(lcp) == datasets.DIGESTS[5][1]
+    assert O.digest_lcp(lcp)[:16] == datasets.DIGESTS[5][1]
 
 
 def _nccl_world1(fn):
