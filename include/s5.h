@@ -50,7 +50,7 @@ typedef struct {
     uint32_t alpha;       /* oversampling factor (default 4; the reference's 2)  */
     uint32_t classifier;  /* 0 = "unroll", 1 = "equal" (samplesort.py:43)      */
     uint32_t small_max;   /* segments <= small_max: warp base case (<= 32)      */
-    uint32_t narrow_max;  /* segments <= narrow_max: one-CTA S^5 step (<=16384; 0: 4096 = off) */
+    uint32_t narrow_max;  /* segments <= narrow_max: one-CTA S^5 step (<= 2^20; 0: 4096 = off) */
     uint32_t flags;       /* bit0: skip the LCP fix-up (debug); bit1: per-kernel timing;
                            * bit2: no common-prefix skip; bit3: also skip partial prefixes
                            * of >= 4 bytes; bit4: bitonic local sort (power-of-two network);

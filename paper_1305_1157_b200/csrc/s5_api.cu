@@ -69,13 +69,19 @@ constexpr uint32_t kLocalSThreads = 128;  // <= 1024
 using LocalSCfg = LocalSmem<kLocalSThreads>;
 constexpr uint32_t kLocalMThreads = 256;  // <= 2048
 using LocalMCfg = LocalSmem<kLocalMThreads>;
+#ifndef S5_NARROW_DEFAULT
+#define S5_NARROW_DEFAULT 4096
+#endif
+// segments of (local_max, kNarrowDefault] strings take the one-CTA S^5 step
+// (off by default: measured slower than the wide pipeline at level 1, DESIGN 8)
+constexpr uint32_t kNarrowDefault = S5_NARROW_DEFAULT;
 
 int resolve(const s5_config* c, Cfg* o) {
     o->v = c && c->v ? c->v : 8191;
     o->alpha = c && c->alpha ? c->alpha : 4;
     o->classifier = c ? c->classifier : 0;
     o->small_max = c && c->small_max ? c->small_max : 32;
-    o->narrow_max = c && c->narrow_max ? c->narrow_max : 4096;  // narrow tier off by default
+    o->narrow_max = c && c->narrow_max ? c->narrow_max : kNarrowDefault;
     o->local_max = c && c->local_max ? c->local_max : LocalCfg::maxn;
     uint32_t wv = c && c->wide_v ? c->wide_v : 511;
     uint32_t wd = 0;
@@ -313,7 +319,7 @@ int grid_for(uint64_t n, int threads, int max_blocks = 148 * 16) {
 // with the level's wide step (fork/join by events; the per-kernel profiling
 // mode keeps everything on the caller's stream).
 struct Side {
-    static constexpr int kLanes = 6;
+    static constexpr int kLanes = 7;
     cudaStream_t s[kLanes] = {};
     cudaEvent_t fork = nullptr, join[kLanes] = {};
     bool ok = false;
@@ -971,9 +977,9 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         if (m[NARROW]) {
             prof.begin(S5_K_NARROW, h.elems[NARROW]);
             if (c.classifier)
-                k_narrow<true><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
+                k_narrow<true><<<m[NARROW], kNarrowThreads, NarrowSmem::total, lane(6)>>>(A, segs[NARROW]);
             else
-                k_narrow<false><<<m[NARROW], kNarrowThreads, NarrowSmem::total, st>>>(A, segs[NARROW]);
+                k_narrow<false><<<m[NARROW], kNarrowThreads, NarrowSmem::total, lane(6)>>>(A, segs[NARROW]);
             prof.end();
         }
         if (m[LOCAL_W]) {

@@ -242,4 +242,45 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
+// ---------------------------------------------------------------------------
+// bulk-copy engine (cp.async.bulk global -> shared, completion on an mbarrier)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 16-byte aligned superset of [src, src + bytes) into dst; returns the
+// element shift of src inside the copy
+template <typename T>
+__device__ __forceinline__ uint32_t bulk_in(T* dst, const T* src, uint32_t count, uint64_t* bar,
+                                            uint32_t& tx) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    const uintptr_t a16 = a & ~static_cast<uintptr_t>(15);
+    const uint32_t bytes = static_cast<uint32_t>(((a + count * sizeof(T) + 15) & ~static_cast<uintptr_t>(15)) - a16);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        :: "r"(smem_u32(dst)), "l"(a16), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+    tx += bytes;
+    return static_cast<uint32_t>((a - a16) / sizeof(T));
+}
+
+__device__ __forceinline__ uint32_t elem_shift(const void* src, uint32_t size) {
+    return static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) & 15) / size);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t tx) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                 :: "r"(smem_u32(bar)), "r"(tx) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n W%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra W%=;\n}\n" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
 }  // namespace s5

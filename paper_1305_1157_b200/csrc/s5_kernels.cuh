@@ -82,9 +82,9 @@ struct SortArgs {
 };
 
 constexpr uint32_t kNarrowThreads = 512;
-constexpr uint32_t kNarrowDMax = 10;          // v <= 1023, k <= 2047
-constexpr uint32_t kNarrowMaxSize = 16384;    // tags fit 14-bit ranks
-constexpr uint32_t kNarrowSampleCap = 8192;
+constexpr uint32_t kNarrowDMax = 8;           // v <= 255, k <= 511
+constexpr uint32_t kNarrowMaxSize = 1u << 20;  // no per-string shared memory
+constexpr uint32_t kNarrowSampleCap = 2048;
 constexpr uint32_t kWideThreads = 512;
 constexpr uint32_t kWideDMax = 10;            // v <= 1023, k <= 2047
 constexpr uint32_t kWideTile = 4096;          // scatter tile staged in shared memory
@@ -426,89 +426,6 @@ __global__ void k_init_root(SortArgs A, uint32_t n, uint32_t depth) {
         emit_child(A, 0, n, depth, 0);
         A.ctl->fetches += n;
     }
-}
-
-// ---------------------------------------------------------------------------
-// narrow tier: one fused CTA per segment (sample, tree, classify+count with
-// warp-aggregated shared-memory histogram, scan, emit, scatter)
-
-struct NarrowSmem {
-    static constexpr uint32_t tree_bytes = (1u << kNarrowDMax) * 8;                  // 8 KB
-    static constexpr uint32_t big_bytes =                                              // 64 KB
-        (kNarrowSampleCap * 8 > kNarrowMaxSize * 4) ? kNarrowSampleCap * 8 : kNarrowMaxSize * 4;
-    static constexpr uint32_t node_bytes = (1u << kNarrowDMax) * 12;                  // 12 KB
-    static constexpr uint32_t hist_bytes = ((2u << kNarrowDMax) + 2) * 4;             // 8 KB
-    static constexpr uint32_t aux_bytes = node_bytes > hist_bytes ? node_bytes : hist_bytes;
-    static constexpr uint32_t total = tree_bytes + big_bytes + aux_bytes + 64 * 4;
-};
-
-template <bool EQUAL>
-__global__ void __launch_bounds__(kNarrowThreads, 2)
-k_narrow(SortArgs A, const Seg* __restrict__ segs) {
-    extern __shared__ __align__(16) uint8_t sm[];
-    uint64_t* tree = reinterpret_cast<uint64_t*>(sm);
-    uint8_t* big = sm + NarrowSmem::tree_bytes;
-    uint64_t* sample = reinterpret_cast<uint64_t*>(big);
-    uint32_t* tags = reinterpret_cast<uint32_t*>(big);
-    uint8_t* aux = big + NarrowSmem::big_bytes;
-    int32_t* na = reinterpret_cast<int32_t*>(aux);
-    int32_t* nb = na + (1u << kNarrowDMax);
-    uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << kNarrowDMax));
-    uint32_t* hist = reinterpret_cast<uint32_t*>(aux);
-    uint32_t* warp_sums = reinterpret_cast<uint32_t*>(aux + NarrowSmem::aux_bytes);
-
-    const Seg s = segs[blockIdx.x];
-    const uint32_t d = choose_d(s.size, A.dmax < kNarrowDMax ? A.dmax : kNarrowDMax);
-    const uint32_t v = (1u << d) - 1, k = 2 * v + 1;
-    uint32_t m = A.alpha * v;
-    if (m > kNarrowSampleCap) m = kNarrowSampleCap;
-    uint32_t M = 1;
-    while (M < m) M <<= 1;
-    const uint32_t* __restrict__ off = A.off[s.side] + s.begin;
-    const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
-
-    // stage 1: sample (classifier.py:76-82) and splitter tree
-    const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
-    for (uint32_t t = threadIdx.x; t < M; t += kNarrowThreads)
-        sample[t] = t < m ? key[sample_index(sseed, t, s.size)] : ~0ull;
-    __syncthreads();
-    bitonic_sort_smem<kNarrowThreads>(sample, M);
-    build_tree_levels<kNarrowThreads>(sample, m, d, tree, na, nb, nf);
-    for (uint32_t b = threadIdx.x; b <= k; b += kNarrowThreads) hist[b] = 0;
-    __syncthreads();
-
-    // stage 2: classify + count; tag = bucket | rank-in-bucket << 11
-    const uint32_t lane = threadIdx.x & 31;
-    for (uint32_t base = 0; base < s.size; base += kNarrowThreads) {
-        uint32_t i = base + threadIdx.x;
-        bool act = i < s.size;
-        uint32_t b = act ? classify<EQUAL>(key[i], tree, d) : 0xFFFFFFFFu;
-        uint32_t peers = __match_any_sync(0xffffffffu, b);
-        uint32_t leader = __ffs(peers) - 1;
-        uint32_t r = 0;
-        if (act && lane == leader) r = atomicAdd(&hist[b], __popc(peers));
-        r = __shfl_sync(0xffffffffu, r, leader) + __popc(peers & lanemask_lt());
-        if (act) tags[i] = b | (r << 11);
-    }
-    __syncthreads();
-
-    // stage 3: bucket boundaries (bucket_layout) and children
-    block_exclusive_scan<kNarrowThreads>(hist, k, warp_sums);
-    __shared__ EmitScratch es;
-    emit_block<kNarrowThreads>(A, s, hist, k, tree, d, &es);
-
-    // stage 4: out-of-place distribution (samplesort.py:146-152)
-    unsigned long long fetches = 0;
-    for (uint32_t i = threadIdx.x; i < s.size; i += kNarrowThreads) {
-        uint32_t tg = tags[i];
-        uint32_t b = tg & 2047u, r = tg >> 11;
-        uint32_t start = hist[b], end = hist[b + 1];
-        uint64_t kk = key[i];
-        bool fin = (end - start == 1) || ((b & 1) && has_zero_byte(kk));
-        place(A, s, b, fin, start + r, end, off[i], kk, fetches);
-    }
-    for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
-    if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
 }
 
 // ---------------------------------------------------------------------------
@@ -1475,6 +1392,215 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
 }
 
 // ---------------------------------------------------------------------------
+// narrow tier: the whole S^5 step of one segment in one CTA (the reference's
+// sequential step, samplesort.py:213-238, at the fan-out of the wide tier):
+// sample + splitter tree in shared memory, a counting pass over the keys
+// (shared histogram), the bucket starts and children (bucket_layout), then a
+// distribution pass that classifies every key again and takes its slot from
+// a per-bucket cursor (warp-aggregated shared atomics; order inside a bucket
+// is free, the reference's distribution is not stable either).  Both passes
+// stream the segment through a ring of shared-memory tiles filled by the
+// bulk-copy engine, so the loads of the next tiles are in flight while one
+// is classified.  No per-string shared memory: the segment size is not
+// bounded by it.  Replaces the six-kernel wide pipeline (tree, count, column
+// scan, bucket scan, scatter + the u16 bucket array in HBM) for the segments
+// below the root.  A segment whose sample is one unterminated key is checked
+// in full and, when every key is equal, its keys are refetched 8 bytes deeper
+// in place (the equality-bucket chain of a long shared prefix without a
+// level per 8 bytes, as in k_local).
+
+constexpr uint32_t kNarrowTile = 2048;
+constexpr uint32_t kNarrowStages = 3;
+
+struct NarrowStage {
+    uint64_t key[kNarrowTile + 2];
+    uint32_t off[kNarrowTile + 4];
+};
+
+struct NarrowSmem {
+    static constexpr uint32_t ring_bytes = kNarrowStages * sizeof(NarrowStage);  // 72 KB
+    static constexpr uint32_t sample_bytes = kNarrowSampleCap * 8;                // aliases the ring
+    static constexpr uint32_t big_bytes = ring_bytes > sample_bytes ? ring_bytes : sample_bytes;
+    static constexpr uint32_t tree_bytes = (1u << kNarrowDMax) * 8;
+    static constexpr uint32_t node_bytes = (1u << kNarrowDMax) * 12;
+    static constexpr uint32_t hist_words = (2u << kNarrowDMax) + 2;  // k + 1
+    // in-order splitters + the classification table (lut_build)
+    static constexpr uint32_t lut_bytes = (1u << kNarrowDMax) * 8 + (kLutCells + 1 + 7) / 8 * 16;
+    static constexpr uint32_t total = big_bytes + tree_bytes + node_bytes + 2 * hist_words * 4 + 8 * kNarrowStages +
+                                      lut_bytes;
+};
+
+template <bool EQUAL>
+__global__ void __launch_bounds__(kNarrowThreads, 2)
+k_narrow(SortArgs A, const Seg* __restrict__ segs) {
+    constexpr uint32_t T = kNarrowThreads, TILE = kNarrowTile, NS = kNarrowStages;
+    constexpr uint32_t IT = TILE / T;  // keys per thread and tile
+    extern __shared__ __align__(16) uint8_t sm[];
+    NarrowStage* ring = reinterpret_cast<NarrowStage*>(sm);
+    uint64_t* sample = reinterpret_cast<uint64_t*>(sm);
+    uint64_t* tree = reinterpret_cast<uint64_t*>(sm + NarrowSmem::big_bytes);
+    int32_t* na = reinterpret_cast<int32_t*>(sm + NarrowSmem::big_bytes + NarrowSmem::tree_bytes);
+    int32_t* nb = na + (1u << kNarrowDMax);
+    uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << kNarrowDMax));
+    uint32_t* hist = nf + (1u << kNarrowDMax);
+    uint32_t* cur = hist + NarrowSmem::hist_words;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(cur + NarrowSmem::hist_words);
+    uint64_t* spl = bar + kNarrowStages;  // in-order splitters, then the table
+    __shared__ uint32_t warp_sums[32];
+    __shared__ uint64_t red[2][32];
+    __shared__ EmitScratch es;
+
+    Seg s = segs[blockIdx.x];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t* off = A.off[s.side] + s.begin;
+    uint64_t* key = A.key[s.side] + s.begin;  // rewritten in place by the prefix skip
+    uint32_t dw = A.dmax < kNarrowDMax ? A.dmax : kNarrowDMax;
+    uint32_t d = ceil_log2((s.size + A.wide_target - 1) / A.wide_target);
+    d = d < 1 ? 1 : (d > dw ? dw : d);
+    const uint32_t v = (1u << d) - 1, k = 2 * v + 1;
+    uint32_t m = A.alpha * v;
+    if (m > kNarrowSampleCap) m = kNarrowSampleCap;
+    uint32_t M = 64;
+    while (M < m) M <<= 1;
+    unsigned long long fetches = 0;
+
+    // stage 1: sample (classifier.py:76-82), sorted; the common-prefix skip
+    for (;;) {
+        const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
+        for (uint32_t t = threadIdx.x; t < M; t += T)
+            sample[t] = t < m ? __ldcg(key + sample_index(sseed, t, s.size)) : ~0ull;
+        __syncthreads();
+        sort_sample<T>(sample, M);
+        const uint64_t s0 = sample[0];
+        if (s0 != sample[m - 1] || has_zero_byte(s0) || (A.flags & 4)) break;
+        // the sample is one unterminated key: is every key equal?
+        uint64_t mn = ~0ull, mx = 0;
+        for (uint32_t i = threadIdx.x; i < s.size; i += T) {
+            const uint64_t x = __ldcg(key + i);
+            mn = x < mn ? x : mn;
+            mx = x > mx ? x : mx;
+        }
+        block_minmax<T>(mn, mx, red);
+        if (mn != mx) break;  // no: an ordinary step (one dominant equality bucket)
+        s.depth += 8;
+        for (uint32_t i = threadIdx.x; i < s.size; i += T) {
+            key[i] = load_key(A.arena, static_cast<uint64_t>(off[i]) + s.depth);
+            ++fetches;
+        }
+        // generic-proxy writes, read next by the sample and the bulk copies
+        asm volatile("fence.proxy.async;\n" ::: "memory");
+        __syncthreads();
+    }
+    build_tree_levels<T>(sample, m, d, tree, na, nb, nf);  // ends with a barrier
+    // classification table: ~3 shared loads per key instead of d dependent
+    // ones (same buckets as the tree descent, classify_lut)
+    const LutTree LT = lut_build<T>(tree, d, spl, reinterpret_cast<uint16_t*>(spl + v));
+    for (uint32_t b = threadIdx.x; b <= k; b += T) hist[b] = 0;
+    if (threadIdx.x == 0) {
+        for (uint32_t q = 0; q < NS; ++q) mbar_init(&bar[q], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();  // the sample's shared memory is the ring from here on
+
+    // one ring sequence over both passes: tile q of the segment's pass A
+    // (keys), then of pass B (keys + offsets); slot q % NS, parity (q / NS) & 1
+    const uint32_t ntiles = (s.size + TILE - 1) / TILE;
+    auto issue = [&](uint32_t q) {
+        const bool pass_b = q >= ntiles;
+        const uint32_t base = (pass_b ? q - ntiles : q) * TILE;
+        const uint32_t cnt = min(TILE, s.size - base);
+        NarrowStage& S = ring[q % NS];
+        uint32_t tx = 0;
+        bulk_in(S.key, key + base, cnt, &bar[q % NS], tx);
+        if (pass_b) bulk_in(S.off, off + base, cnt, &bar[q % NS], tx);
+        mbar_expect_tx(&bar[q % NS], tx);
+    };
+    if (threadIdx.x == 0)
+        for (uint32_t q = 0; q < NS && q < 2 * ntiles; ++q) issue(q);
+
+    // stage 2: classify + count (samplesort.py:51-113), tile by tile
+    for (uint32_t q = 0; q < ntiles; ++q) {
+        const uint32_t base = q * TILE, cnt = min(TILE, s.size - base);
+        const uint32_t shk = elem_shift(key + base, 8);
+        mbar_wait(&bar[q % NS], (q / NS) & 1u);
+        const NarrowStage& S = ring[q % NS];
+        uint64_t kk[IT];
+        uint32_t bb[IT];
+#pragma unroll
+        for (uint32_t j = 0; j < IT; ++j) {
+            const uint32_t e = j * T + threadIdx.x;
+            kk[j] = e < cnt ? S.key[e + shk] : 0;
+        }
+        if (EQUAL) {
+            classify_iw<true, IT>(kk, tree, d, bb);
+        } else {
+#pragma unroll
+            for (uint32_t j = 0; j < IT; ++j) bb[j] = classify_lut(kk[j], LT);
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < IT; ++j)
+            if (j * T + threadIdx.x < cnt) atomicAdd(&hist[bb[j]], 1u);
+        __syncthreads();  // every read of this slot is done: refill it
+        if (threadIdx.x == 0 && q + NS < 2 * ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(q + NS);
+        }
+    }
+
+    // stage 3: bucket starts and children (bucket_layout, classifier.py:284-304)
+    block_exclusive_scan<T>(hist, k, warp_sums);
+    for (uint32_t b = threadIdx.x; b <= k; b += T) cur[b] = hist[b];
+    emit_block<T>(A, s, hist, k, tree, d, &es);
+    __syncthreads();
+
+    // stage 4: distribution (samplesort.py:146-152): classify again, slot
+    // from the bucket's cursor
+    const uint32_t k2m = k2_mode(A, s);
+    for (uint32_t t = 0; t < ntiles; ++t) {
+        const uint32_t q = ntiles + t;
+        const uint32_t base = t * TILE, cnt = min(TILE, s.size - base);
+        const uint32_t shk = elem_shift(key + base, 8), sho = elem_shift(off + base, 4);
+        mbar_wait(&bar[q % NS], (q / NS) & 1u);
+        const NarrowStage& S = ring[q % NS];
+        uint64_t kk[IT];
+        uint32_t oo[IT], bb[IT];
+#pragma unroll
+        for (uint32_t j = 0; j < IT; ++j) {
+            const uint32_t e = j * T + threadIdx.x;
+            kk[j] = e < cnt ? S.key[e + shk] : 0;
+            oo[j] = e < cnt ? S.off[e + sho] : 0;
+        }
+        if (EQUAL) {
+            classify_iw<true, IT>(kk, tree, d, bb);
+        } else {
+#pragma unroll
+            for (uint32_t j = 0; j < IT; ++j) bb[j] = classify_lut(kk[j], LT);
+        }
+        uint32_t rr[IT];
+#pragma unroll
+        for (uint32_t j = 0; j < IT; ++j)
+            rr[j] = j * T + threadIdx.x < cnt ? atomicAdd(&cur[bb[j]], 1u) : 0u;
+#pragma unroll
+        for (uint32_t j = 0; j < IT; ++j) {
+            const uint32_t e = j * T + threadIdx.x;
+            const uint32_t b = bb[j], r = rr[j];
+            if (e < cnt) {
+                const uint32_t st = hist[b], end = hist[b + 1];
+                const bool fin = end - st == 1 || ((b & 1) && has_zero_byte(kk[j]));
+                place_k2(A, s, b, fin, r, end, oo[j], kk[j], k2m, s.begin + base + e, fetches);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && q + NS < 2 * ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            issue(q + NS);
+        }
+    }
+    for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
+    if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
+}
+
+// ---------------------------------------------------------------------------
 // wide tier (segments > narrow_max): the fully parallel step of
 // samplesort.py:369-434 with CTAs as workers.
 
@@ -1641,9 +1767,9 @@ __global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P) {
             for (uint32_t q = 0; q < 8; ++q) c += __popc(bytemask[j][q]);
             est *= c ? c : 1;
         }
-        // (and only when the root's children will be wide steps themselves)
+        // (and only when the root's children will be S^5 steps themselves)
         A.ctl->k2 = (A.flags & 256) == 0 && static_cast<double>(s.size) > 16.0 * est &&
-                    s.size / (g.v + 1) > A.narrow_max;
+                    s.size / (g.v + 1) > A.local_max;
     }
     sort_sample<TT>(sample, M);
     uint64_t* tree = P.tree_pool + P.tree_off[blockIdx.x];
@@ -2076,29 +2202,6 @@ struct WideTmaSmem {
                (3 * (2u << dcap) + 8) * 4 + 64 * 4 + 8 * NS;
     }
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-// 16-byte aligned superset of [src, src + bytes) into dst; returns the
-// element shift of src inside the copy
-template <typename T>
-__device__ __forceinline__ uint32_t bulk_in(T* dst, const T* src, uint32_t count, uint64_t* bar,
-                                            uint32_t& tx) {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
-    const uintptr_t a16 = a & ~static_cast<uintptr_t>(15);
-    const uint32_t bytes = static_cast<uint32_t>(((a + count * sizeof(T) + 15) & ~static_cast<uintptr_t>(15)) - a16);
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-        :: "r"(smem_u32(dst)), "l"(a16), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-    tx += bytes;
-    return static_cast<uint32_t>((a - a16) / sizeof(T));
-}
-
-__device__ __forceinline__ uint32_t elem_shift(const void* src, uint32_t size) {
-    return static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) & 15) / size);
-}
 
 template <uint32_t THREADS, uint32_t TILE, uint32_t NS = 2>
 __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePlan P) {

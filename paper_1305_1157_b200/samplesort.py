@@ -40,8 +40,9 @@ class SampleSortConfig:
     """samplesort.py:37-45 plus the GPU tiering knobs.
 
     ``t_m``/``t_i``/``interleave`` are kept for signature compatibility; the
-    GPU tiers are ``narrow_max`` (one-CTA S^5 step, <= 16384 strings) and
-    ``small_max`` (warp base case, <= 32 strings).  ``alpha`` defaults to 4
+    GPU tiers are ``narrow_max`` (segments up to it take the one-CTA S^5
+    step; 0 = the library default, 4096 = off), ``local_max`` (one-CTA base case,
+    <= 4096) and ``small_max`` (warp base case, <= 32 strings).  ``alpha`` defaults to 4
     (the reference's 2 is accepted): the wide steps' samples are cheap on the
     device and better balanced buckets pay (measured 1-2 %); splitters only
     move the order of identical strings, never the output.
@@ -54,7 +55,7 @@ class SampleSortConfig:
     interleave: int = 3
     seed: int = 1
     small_max: int = 32
-    narrow_max: int = 4096
+    narrow_max: int = 0
     local_max: int = 4096
     wide_v: int = 511
     wide_target: int = 512

@@ -10,13 +10,14 @@ REP=/tmp/ncu_$TAG; mkdir -p $REP
 for C in $CFGS; do
   python profiles/profile_one.py --config $C > /dev/null || exit 1
   timeout 900 ncu --set full --import-source on --clock-control none -f \
-      -k regex:"k_local|k_wide_scatter|k_wide_count|k_small" --launch-count 48 \
+      -k regex:"k_local|k_wide_scatter|k_wide_count|k_small|k_narrow" --launch-count 48 \
       -o $REP/full_cfg$C python profiles/profile_one.py --config $C \
       > gpurun_out/${TAG}_ncu_cfg$C.log 2>&1
   echo "cfg $C rc=$?"
   python profiles/ncu_summary.py $REP/full_cfg$C.ncu-rep --json gpurun_out/${TAG}_ncu_cfg$C.json \
       > gpurun_out/${TAG}_ncu_cfg$C.txt 2>&1
-  for K in "k_local_w" "k_local<64" "k_local<128" "k_local<256" "k_local<512" "k_wide_scatter" "k_wide_count"; do
+  for K in "k_local_w" "k_local<[^>]*64>" "k_local<[^>]*128>" "k_local<[^>]*256>" "k_local<[^>]*512>" \
+           "k_wide_scatter" "k_wide_count" "k_narrow"; do
     echo "== $K" >> gpurun_out/${TAG}_stalls_cfg$C.txt
     timeout 300 python profiles/stall_by_line.py $REP/full_cfg$C.ncu-rep "$K" 0 \
         >> gpurun_out/${TAG}_stalls_cfg$C.txt 2>&1

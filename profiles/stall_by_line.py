@@ -17,7 +17,8 @@ import tempfile
 
 
 def sass_samples(rep, kregex, skip):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv",
+                          "--kernel-name-base", "demangled", "--kernel-name",
                           f"regex:{kregex}", "--launch-skip", str(skip), "--launch-count", "1"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))

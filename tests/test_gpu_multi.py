@@ -230,7 +230,7 @@ def test_wide_pool_overflow_is_reported(monkeypatch):
     monkeypatch.setenv("S5_TEST_POOL_WORDS", "1000")
     arena, h0 = datasets.generate(2, 1 << 18)
     with pytest.raises(RuntimeError, match="wide pool overflow"):
-        sort_with_lcp(arena, h0.copy(), cfg=SampleSortConfig())
+        sort_with_lcp(arena, h0.copy(), cfg=SampleSortConfig(narrow_max=4096))
     monkeypatch.delenv("S5_TEST_POOL_WORDS")
     h, lcp = sort_with_lcp(arena, h0.copy())
     assert O.first_unsorted(arena, h) == -1
