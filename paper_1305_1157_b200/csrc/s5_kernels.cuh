@@ -893,6 +893,24 @@ __device__ __forceinline__ void block_minmax(uint64_t& mn, uint64_t& mx, uint64_
     __syncthreads();
 }
 
+// block-wide OR of one u64 per thread (all threads call): one redux per
+// 32-bit half and warp, then the warps' words through shared memory
+template <uint32_t THREADS>
+__device__ __forceinline__ uint64_t block_or64(uint64_t x, uint64_t (*red)[32]) {
+    const uint32_t lo = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(x));
+    const uint32_t hi = __reduce_or_sync(0xffffffffu, static_cast<uint32_t>(x >> 32));
+    x = (static_cast<uint64_t>(hi) << 32) | lo;
+    if (THREADS == 32) return x;
+    const uint32_t w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) red[0][w] = x;
+    __syncthreads();
+    x = 0;
+#pragma unroll
+    for (uint32_t q = 0; q < THREADS / 32; ++q) x |= red[0][q];
+    __syncthreads();
+    return x;
+}
+
 // run boundaries: bit p of the bitmap marks the first position of a run
 __device__ __forceinline__ uint32_t run_end(const uint32_t* bits, uint32_t p) {
     uint32_t q = p + 1, wi = q >> 5;
@@ -966,26 +984,26 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     // depth in-CTA (the equality-bucket chain of long shared prefixes,
     // classifier.py:297-303, without a level per 8 bytes); all-identical
     // terminated keys finish here
+    // (the common prefix of all keys = that of every key with the first one:
+    // the leading zeros of the OR of the XORs, one redux per warp)
     unsigned long long fetches = 0;
     uint32_t L;
+    const uint32_t o0 = goff[0];
+    uint64_t k0 = gkey[0];
     for (;;) {
-        uint64_t mn = ~0ull, mx = 0;
+        uint64_t x = 0;
 #pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) {
-            if (t + j * THREADS < s.size) {
-                mn = rk[j] < mn ? rk[j] : mn;
-                mx = rk[j] > mx ? rk[j] : mx;
-            }
-        }
-        block_minmax<THREADS>(mn, mx, red);
-        if (mn == mx) {
-            if (has_zero_byte(mn)) {  // identical strings: any order, lcp = |s|
+        for (uint32_t j = 0; j < 8; ++j)
+            if (t + j * THREADS < s.size) x |= rk[j] ^ k0;
+        x = block_or64<THREADS>(x, red);
+        if (x == 0) {
+            if (has_zero_byte(k0)) {  // identical strings: any order, lcp = |s|
 #pragma unroll
                 for (uint32_t j = 0; j < 8; ++j) {
                     uint32_t i = t + j * THREADS;
                     if (i < s.size) {
                         A.out[s.begin + i] = ro[j];
-                        if (A.lcp && i + 1 < s.size) A.lcp[s.begin + i] = s.depth + zero_index(mn);
+                        if (A.lcp && i + 1 < s.size) A.lcp[s.begin + i] = s.depth + zero_index(k0);
                     }
                 }
                 for (uint32_t x = 16; x > 0; x >>= 1)
@@ -995,7 +1013,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
             }
             L = 8;
         } else {
-            L = diff_bytes(mn, mx);
+            L = static_cast<uint32_t>(__clzll(static_cast<long long>(x))) >> 3;
         }
         // default: skip whole equal words only; flags bit3 also skips a partial
         // common prefix of >= 4 bytes; bit2 disables the skip
@@ -1009,6 +1027,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
                 ++fetches;
             }
         }
+        k0 = load_key(A.arena, static_cast<uint64_t>(o0) + s.depth);
     }
     if (L > 7) L = 7;  // all keys equal (skip disabled): one run either way
     // sort words: key bytes after the common prefix, slot in the low 12 bits.
@@ -1224,29 +1243,21 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
     }
     unsigned long long fetches = 0;
     uint32_t L;
-    for (;;) {  // common-prefix skip, as in k_local
-        uint64_t mn = ~0ull, mx = 0;
+    uint64_t k0 = __shfl_sync(0xffffffffu, rk[0], 0);
+    for (;;) {  // common-prefix skip, as in k_local (OR of the XORs with the first key)
+        uint64_t x = 0;
 #pragma unroll
-        for (uint32_t j = 0; j < 8; ++j) {
-            if (lane + 32 * j < s.size) {
-                mn = rk[j] < mn ? rk[j] : mn;
-                mx = rk[j] > mx ? rk[j] : mx;
-            }
-        }
-        for (uint32_t x = 16; x > 0; x >>= 1) {
-            const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, x);
-            const uint64_t b = __shfl_xor_sync(0xffffffffu, mx, x);
-            mn = a < mn ? a : mn;
-            mx = b > mx ? b : mx;
-        }
-        if (mn == mx) {
-            if (has_zero_byte(mn)) {  // identical strings
+        for (uint32_t j = 0; j < 8; ++j)
+            if (lane + 32 * j < s.size) x |= rk[j] ^ k0;
+        x = block_or64<32>(x, nullptr);
+        if (x == 0) {
+            if (has_zero_byte(k0)) {  // identical strings
 #pragma unroll
                 for (uint32_t j = 0; j < 8; ++j) {
                     const uint32_t i = lane + 32 * j;
                     if (i < s.size) {
                         A.out[s.begin + i] = ro[j];
-                        if (A.lcp && i + 1 < s.size) A.lcp[s.begin + i] = s.depth + zero_index(mn);
+                        if (A.lcp && i + 1 < s.size) A.lcp[s.begin + i] = s.depth + zero_index(k0);
                     }
                 }
                 L = 9;  // done
@@ -1254,7 +1265,7 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
             }
             L = 8;
         } else {
-            L = diff_bytes(mn, mx);
+            L = static_cast<uint32_t>(__clzll(static_cast<long long>(x))) >> 3;
         }
         if ((A.flags & 4) || L < ((A.flags & 8) ? 4u : 8u)) break;
         s.depth += L;
@@ -1265,6 +1276,7 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
                 ++fetches;
             }
         }
+        k0 = __shfl_sync(0xffffffffu, rk[0], 0);
     }
     if (L <= 8) {
         if (L > 7) L = 7;
