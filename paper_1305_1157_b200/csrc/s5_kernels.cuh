@@ -785,10 +785,14 @@ __device__ __forceinline__ void block_merge_sort8(uint64_t (&w)[8], uint64_t* sb
 // bytes) with refills 16 bytes deeper while pairs stay unresolved (the mkqs
 // equal-partition refill, basesort.py:146-150, as warp rounds); writes the
 // pair LCPs, the order and the final handles.
-__device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uint32_t gs,
-                                            uint32_t g, const uint32_t* off1, uint16_t* perm,
-                                            uint64_t depth, uint32_t lane,
-                                            unsigned long long& fetches) {
+// Plain pointers, not the SortArgs: a reference to the kernel's parameter
+// block makes every thread copy it to local memory (measured: ~19 B of DRAM
+// writes per string on the local tier).  Returns this lane's arena fetches.
+__device__ __noinline__ uint32_t tie_group_warp(const uint8_t* __restrict__ arena, int64_t* out,
+                                                int64_t* lcp, uint32_t begin, uint32_t gs,
+                                                uint32_t g, const uint32_t* off1, uint16_t* perm,
+                                                uint64_t depth, uint32_t lane) {
+    uint32_t fetches = 0;
     const bool valid = lane < g;
     const bool pair_valid = lane + 1 < g;
     uint32_t e = valid ? perm[gs + lane] : 0u;
@@ -799,7 +803,7 @@ __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uin
     const uint32_t P = g <= 2 ? 2u : 1u << (32 - __clz(g - 1));
     for (;; depth += 16) {  // 16 string bytes per round
         if (active) {
-            load_key2(A.arena, static_cast<uint64_t>(off1[e]) + depth, k0, k1);
+            load_key2(arena, static_cast<uint64_t>(off1[e]) + depth, k0, k1);
             ++fetches;
         }
         // bitonic sort of (run, k0, k1), payload e -- skipped when every
@@ -831,7 +835,7 @@ __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uin
             else if (has_zero_byte(k0)) { l = depth + zero_index(k0); resolved = true; }
             else if (k1 != n1) { l = depth + 8 + diff_bytes(k1, n1); resolved = true; }
             else if (has_zero_byte(k1)) { l = depth + 8 + zero_index(k1); resolved = true; }
-            if (resolved && A.lcp) A.lcp[s.begin + gs + lane] = l;
+            if (resolved && lcp) lcp[begin + gs + lane] = l;
         }
         uint32_t unres = __ballot_sync(0xffffffffu, pair_valid && !resolved);
         if (!unres) break;
@@ -843,13 +847,14 @@ __device__ __noinline__ void tie_group_warp(const SortArgs& A, const Seg& s, uin
     }
     if (valid) {
         perm[gs + lane] = static_cast<uint16_t>(e);
-        A.out[s.begin + gs + lane] = off1[e];
+        out[begin + gs + lane] = off1[e];
     }
+    return fetches;
 }
 
 // strings.py:64-74 (_compare_from) + :56-61 (_lcp_pair) in one walk from a
 // depth both strings are known to share, 16 bytes per step.
-__device__ __noinline__ int walk_compare(const uint8_t* __restrict__ arena, uint64_t a,
+__device__ __forceinline__ int walk_compare(const uint8_t* __restrict__ arena, uint64_t a,
                                          uint64_t b, uint64_t depth, uint64_t* lcp_out,
                                          unsigned long long& fetches) {
 #pragma unroll 1
@@ -1167,7 +1172,8 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     const uint32_t nt = nties, nk = nkids;
     for (uint32_t q = t >> 5; q < nt; q += THREADS / 32) {
         const uint32_t x = ties[q];
-        tie_group_warp(A, s, x & 0x1FFFu, x >> 13, off1, perm, depth + 8, lane, fetches);
+        fetches += tie_group_warp(A.arena, A.out, A.lcp, s.begin, x & 0x1FFFu, x >> 13, off1, perm,
+                                  depth + 8, lane);
     }
     // children: one list reservation per size class per CTA
     if (nk) {
@@ -1396,7 +1402,8 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
         const uint32_t nt = W.nties;
         for (uint32_t q = 0; q < nt; ++q) {
             const uint32_t x = W.ties[q];
-            tie_group_warp(A, s, x & 0x1FFFu, x >> 13, W.off1, W.perm, depth + 8, lane, fetches);
+            fetches += tie_group_warp(A.arena, A.out, A.lcp, s.begin, x & 0x1FFFu, x >> 13, W.off1,
+                                      W.perm, depth + 8, lane);
         }
     }
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
