@@ -646,7 +646,7 @@ int host_upload(HostPath& H, const int64_t* h_handles, uint64_t n, uint64_t aren
         S5_CUDA(cudaMemcpyAsync(d32 + off, s32, len * 4, cudaMemcpyHostToDevice, st));
         S5_CUDA(cudaEventRecord(H.ev[b], st));
     }
-    k_widen32<<<grid_for(n, 256), 256, 0, st>>>(d32, dh, n);
+    if (dh) k_widen32<<<grid_for(n, 256), 256, 0, st>>>(d32, dh, n);
     S5_CUDA(cudaStreamSynchronize(st));
     if (bad.load()) return fail(S5_E_RANGE, "handle outside the arena");
     return 0;
@@ -1102,10 +1102,17 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
     void* dn = base + 2 * align_up(n * 8) + align_up(n * 4);
     void* dws = base + 2 * align_up(n * 8) + 2 * align_up(n * 4);
 
+    // the u32 offsets land in the first 4n bytes of dh and the sort reads them
+    // in place (flags bit9: no widening pass, half the root's handle reads)
+    s5_config cc{};
+    if (cfg) cc = *cfg;
+    else cc.seed = 1;
+    cc.flags |= 512;
     auto t0 = std::chrono::steady_clock::now();
-    if (int rc = host_upload(H, h_handles, n, arena_len, d32, dh, st)) return rc;
+    if (int rc = host_upload(H, h_handles, n, arena_len, reinterpret_cast<uint32_t*>(dh), nullptr, st))
+        return rc;
     auto t1 = std::chrono::steady_clock::now();
-    int rc = s5_sort(d_arena, arena_len, dh, n, depth, h_lcp ? dl : nullptr, cfg, dws, ws,
+    int rc = s5_sort(d_arena, arena_len, dh, n, depth, h_lcp ? dl : nullptr, &cc, dws, ws,
                      stream_, stats);
     if (rc) return rc;
     S5_CUDA(cudaStreamSynchronize(st));

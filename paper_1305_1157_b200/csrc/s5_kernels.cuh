@@ -297,7 +297,7 @@ __device__ __forceinline__ void reserve_hints(const SortArgs& A, EmitScratch* es
 // KEEP_SMALL: buckets of <= small_max strings are finished by the calling CTA
 // itself (k_local) instead of becoming children.
 template <uint32_t THREADS, bool KEEP_SMALL = false>
-__device__ __noinline__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* starts, uint32_t k,
+__device__ __forceinline__ void emit_block(const SortArgs& A, const Seg& s, const uint32_t* starts, uint32_t k,
                            const uint64_t* tree, uint32_t d, EmitScratch* es) {
     if (threadIdx.x < NCLS) {
         es->cnt[threadIdx.x] = 0;
@@ -854,6 +854,9 @@ __device__ __noinline__ uint32_t tie_group_warp(const uint8_t* __restrict__ aren
 
 // strings.py:64-74 (_compare_from) + :56-61 (_lcp_pair) in one walk from a
 // depth both strings are known to share, 16 bytes per step.
+// strings.py:64-74 (_compare_from) + :56-61 (_lcp_pair) in one walk from a
+// depth both strings are known to share, 16 bytes per step.  (Rounds of 16,
+// 32, then 64 bytes were measured slower: config 4 +7 %.)
 __device__ __forceinline__ int walk_compare(const uint8_t* __restrict__ arena, uint64_t a,
                                          uint64_t b, uint64_t depth, uint64_t* lcp_out,
                                          unsigned long long& fetches) {
