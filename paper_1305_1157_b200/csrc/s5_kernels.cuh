@@ -254,6 +254,54 @@ __device__ __noinline__ void block_exclusive_scan(uint32_t* h, uint32_t k, uint3
     __syncthreads();
 }
 
+// block_exclusive_scan of a tile's bucket counts fused with the per-CTA
+// cursor step of the distribution: gb[b] = cur[b] (the tile's global base of
+// bucket b), cur[b] += count of b.  All threads call; ends with a barrier.
+template <uint32_t THREADS>
+__device__ __forceinline__ void tile_scan(uint32_t* h, uint32_t k, uint32_t* cur, uint32_t* gb,
+                                          uint32_t* warp_sums) {
+    const uint32_t per = (k + THREADS) / THREADS;  // covers k+1 slots
+    const uint32_t lo = threadIdx.x * per;
+    uint32_t sum = 0;
+    for (uint32_t j = 0; j < per; ++j) {
+        const uint32_t idx = lo + j;
+        if (idx < k) sum += h[idx];
+    }
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = sum;
+    for (uint32_t o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_sums[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        constexpr uint32_t NW = THREADS / 32;
+        uint32_t x = lane < NW ? warp_sums[lane] : 0;
+        for (uint32_t o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane < NW) warp_sums[lane] = x;  // inclusive
+    }
+    __syncthreads();
+    uint32_t run = incl - sum + (w ? warp_sums[w - 1] : 0);
+    for (uint32_t j = 0; j < per; ++j) {
+        const uint32_t idx = lo + j;
+        if (idx < k) {
+            const uint32_t c = h[idx];
+            h[idx] = run;
+            run += c;
+            const uint32_t r = cur[idx];
+            gb[idx] = r;
+            cur[idx] = r + c;
+        } else if (idx == k) {
+            h[idx] = run;
+        }
+    }
+    __syncthreads();
+}
+
 struct EmitScratch {
     uint32_t cnt[NCLS];
     uint32_t base[NCLS];
@@ -2164,13 +2212,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
             if (i < hi) br[j] |= atomicAdd(&cnt[br[j]], 1u) << 16;
         }
         __syncthreads();
-        for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) {
-            uint32_t r = cur[b];
-            gb[b] = r;
-            cur[b] = r + cnt[b];
-        }
-        __syncthreads();
-        block_exclusive_scan<kWideThreads>(cnt, g.k, warp_sums);
+        tile_scan<kWideThreads>(cnt, g.k, cur, gb, warp_sums);
 #pragma unroll
         for (uint32_t j = 0; j < IT; ++j) {
             uint32_t i = base + j * kWideThreads + threadIdx.x;
@@ -2302,13 +2344,7 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
             }
         }
         __syncthreads();
-        for (uint32_t b = threadIdx.x; b < g.k; b += kTmaThreads) {
-            uint32_t r = cur[b];
-            gb[b] = r;
-            cur[b] = r + cnt[b];
-        }
-        __syncthreads();
-        block_exclusive_scan<kTmaThreads>(cnt, g.k, warp_sums);
+        tile_scan<kTmaThreads>(cnt, g.k, cur, gb, warp_sums);
 #pragma unroll
         for (uint32_t j = 0; j < IT; ++j) {
             const uint32_t e = threadIdx.x + j * kTmaThreads;
