@@ -146,7 +146,7 @@ Layout make_layout(uint64_t n, const Cfg& c) {
     // wide segments have > narrow_max strings; v+1 <= size/8, and at most
     // ceil(size/64K) <= 296 rows of k <= size/4 counters (see choose_d)
     L.tree_cap = n / 4 + uint64_t(L.cap[WIDE]) * (2 + kLutWords) + 16;
-    L.hist_cap = n + n / 2 + 3 * uint64_t(L.cap[WIDE]) + 65536;
+    L.hist_cap = n + n / 2 + 4 * uint64_t(L.cap[WIDE]) + 65536;
     if (const char* e = getenv("S5_TEST_POOL_WORDS")) {  // tests: force the overflow path
         L.tree_cap = std::min<uint64_t>(L.tree_cap, strtoull(e, nullptr, 10));
         L.hist_cap = std::min<uint64_t>(L.hist_cap, strtoull(e, nullptr, 10));

@@ -1725,7 +1725,7 @@ __global__ void __launch_bounds__(1024) k_wide_plan(SortArgs A, WidePlan P) {
             WideGeom g = wide_geom(P.segs[i], A);
             x[0] = g.C;
             x[1] = 2 * g.v + 1 + kLutWords;
-            x[2] = static_cast<unsigned long long>(g.C) * g.k + g.k + 1;
+            x[2] = static_cast<unsigned long long>(g.C) * g.k + g.k + 2;  // + the solo flag
         }
         unsigned long long incl[3];
         for (int q = 0; q < 3; ++q) {
@@ -2134,8 +2134,43 @@ __global__ void __launch_bounds__(256) k_wide_bscan(SortArgs A, WidePlan P) {
     uint32_t* starts = P.hist_pool + P.hist_off[si] + static_cast<uint64_t>(g.C) * g.k;
     block_exclusive_scan<256>(starts, g.k, warp_sums);
     const uint64_t* tree = P.tree_pool + P.tree_off[si];
+    // one equality bucket of an unterminated splitter holding the whole
+    // segment: every key is equal, so the segment stays where it is and only
+    // its keys advance 8 bytes (the scatter does that in place, reading the
+    // flag starts[k + 1] = bucket + 1) -- the equality-bucket chain of a
+    // shared prefix (classifier.py:297-303) without moving a string
+    __shared__ uint32_t solo;
+    if (threadIdx.x == 0) solo = 0;
+    __syncthreads();
+    for (uint32_t b = 1 + 2 * threadIdx.x; b < g.k; b += 2 * 256)
+        if (starts[b + 1] - starts[b] == s.size && !has_zero_byte(tree[node_of_rank(b >> 1, g.d)]))
+            solo = b + 1;
+    __syncthreads();
+    if (threadIdx.x == 0) starts[g.k + 1] = solo;
+    if (solo) {
+        if (threadIdx.x == 0) emit_child(A, s.begin, s.size, s.depth + 8, s.side);
+        return;
+    }
     __shared__ EmitScratch es;
     emit_block<256>(A, s, starts, g.k, tree, g.d, &es);
+}
+
+// The scatter of a segment whose keys are all equal (k_wide_bscan's solo
+// flag): keys advance 8 bytes in place -- the carried second words when the
+// root gathered them, else one arena fetch per string.
+__device__ __forceinline__ void advance_keys(const SortArgs& A, const Seg& s, uint32_t lo, uint32_t hi,
+                                             uint32_t threads, unsigned long long& fetches) {
+    const uint32_t k2m = k2_mode(A, s);
+    const uint32_t* __restrict__ off = A.off[s.side] + s.begin;
+    uint64_t* key = A.key[s.side] + s.begin;
+    for (uint32_t i = lo + threadIdx.x; i < hi; i += threads) {
+        if (k2m) {
+            key[i] = __ldcs(A.key2[k2m - 1] + s.begin + i);
+        } else {
+            key[i] = load_key(A.arena, static_cast<uint64_t>(__ldcs(off + i)) + s.depth + 8);
+            ++fetches;
+        }
+    }
 }
 
 // Out-of-place distribution with per-CTA cursors (stage 4, samplesort.py:412-417).
@@ -2175,6 +2210,13 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
     const uint64_t* tree = P.tree_pool + P.tree_off[si];
     const uint32_t* rows = P.hist_pool + P.hist_off[si];
     const uint32_t* starts = rows + static_cast<uint64_t>(g.C) * g.k;
+    if (starts[g.k + 1]) {  // all keys equal: advance them in place
+        unsigned long long fetches = 0;
+        advance_keys(A, s, lo, hi, kWideThreads, fetches);
+        for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
+        if ((threadIdx.x & 31) == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
+        return;
+    }
     for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) {
         uint32_t st = starts[b], n_b = starts[b + 1] - st;
         bool fin = n_b == 1 || ((b & 1) && has_zero_byte(tree[node_of_rank(b >> 1, g.d)]));
@@ -2292,6 +2334,13 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
     const uint64_t* tree = P.tree_pool + P.tree_off[si];
     const uint32_t* rows = P.hist_pool + P.hist_off[si];
     const uint32_t* starts = rows + static_cast<uint64_t>(g.C) * g.k;
+    if (starts[g.k + 1]) {  // all keys equal: advance them in place
+        unsigned long long fetches = 0;
+        advance_keys(A, s, lo, hi, kTmaThreads, fetches);
+        for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
+        if ((threadIdx.x & 31) == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
+        return;
+    }
     const uint32_t* __restrict__ off = A.off[s.side] + s.begin;
     const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
     const uint16_t* __restrict__ bkt = P.bkt + s.begin;
