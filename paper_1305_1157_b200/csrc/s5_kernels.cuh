@@ -695,7 +695,8 @@ __device__ __forceinline__ void block_sort8(uint64_t (&w)[8], uint64_t* sb) {
 
 // Ascending sort of the 8 words of one thread (bitonic network, 24
 // compare-exchanges with compile-time directions).
-__device__ __forceinline__ void sort8_regs(uint64_t (&w)[8]) {
+template <typename T>
+__device__ __forceinline__ void sort8_regs(T (&w)[8]) {
 #pragma unroll
     for (uint32_t K = 2; K <= 8; K <<= 1) {
 #pragma unroll
@@ -704,7 +705,7 @@ __device__ __forceinline__ void sort8_regs(uint64_t (&w)[8]) {
             for (uint32_t j = 0; j < 8; ++j) {
                 if (j & J) continue;
                 const bool asc = (j & K) == 0 || K == 8;
-                const uint64_t a = w[j], b = w[j | J];
+                const T a = w[j], b = w[j | J];
                 const bool x = (a > b) == asc;
                 w[j] = x ? b : a;
                 w[j | J] = x ? a : b;
@@ -737,11 +738,12 @@ __device__ __forceinline__ void load8(const uint64_t* sb, uint32_t my, uint64_t 
 // position p with the block's mirror position (partner lane l ^ (g-1),
 // element 7-j), so both runs stay ascending; then half-cleaners by shuffle
 // and inside the thread.  No shared memory, no barriers.
-__device__ __forceinline__ void warp_merge256(uint64_t (&w)[8], uint32_t lane) {
+template <typename T>
+__device__ __forceinline__ void warp_merge256(T (&w)[8], uint32_t lane) {
 #pragma unroll 1
     for (uint32_t g = 2; g <= 32; g <<= 1) {  // lanes per merged run
         {
-            uint64_t o[8];
+            T o[8];
 #pragma unroll
             for (uint32_t j = 0; j < 8; ++j) o[j] = __shfl_xor_sync(0xffffffffu, w[7 - j], g - 1);
             const bool lo_half = (lane & (g >> 1)) == 0;
@@ -756,7 +758,7 @@ __device__ __forceinline__ void warp_merge256(uint64_t (&w)[8], uint32_t lane) {
             const bool keep_min = (lane & m) == 0;
 #pragma unroll
             for (uint32_t j = 0; j < 8; ++j) {
-                const uint64_t o = __shfl_xor_sync(0xffffffffu, w[j], m);
+                const T o = __shfl_xor_sync(0xffffffffu, w[j], m);
                 if ((o < w[j]) == keep_min) w[j] = o;
             }
         }
@@ -765,7 +767,7 @@ __device__ __forceinline__ void warp_merge256(uint64_t (&w)[8], uint32_t lane) {
 #pragma unroll
             for (uint32_t j = 0; j < 8; ++j) {
                 if (j & J) continue;
-                const uint64_t a = w[j], b = w[j | J];
+                const T a = w[j], b = w[j | J];
                 const bool x = a > b;
                 w[j] = x ? b : a;
                 w[j | J] = x ? a : b;
@@ -1337,28 +1339,35 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
     }
     if (L <= 8) {
         if (L > 7) L = 7;
-        const bool exact = L >= 2;
-        uint64_t w[8];
+        // 32-bit sort words: the 3 key bytes after the common prefix, the
+        // slot in the low 8 bits (min/max compare-exchanges and one shuffle
+        // per word instead of 64-bit compares, four selects and two
+        // shuffles).  The words hold the whole key when L >= 5; otherwise
+        // equal words are candidate runs, ranked by the full cached keys
+        // below -- skipped when the sort left none.
+        bool exact = L >= 5;
+        uint32_t w[8];
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j) {
             const uint32_t i = lane + 32 * j;
             W.key1[i] = rk[j];
             W.off1[i] = ro[j];
-            w[j] = i < s.size ? (((rk[j] << (8 * L)) & ~0xFFFull) | i) : ~0ull;
+            w[j] = i < s.size ? ((static_cast<uint32_t>((rk[j] << (8 * L)) >> 40) << 8) | i) : ~0u;
         }
         sort8_regs(w);
         warp_merge256(w, lane);
         // run starts of the sorted words (lane l holds positions 8l..8l+7)
-        const uint64_t prev = __shfl_up_sync(0xffffffffu, w[7], 1);
+        const uint32_t prev = __shfl_up_sync(0xffffffffu, w[7], 1);
         uint32_t fl = 0;
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j) {
             const uint32_t p = 8 * lane + j;
-            const uint64_t pw = j ? w[j - 1] : prev;
-            const bool st = p == 0 || p >= s.size || (w[j] >> 12) != (pw >> 12);
+            const uint32_t pw = j ? w[j - 1] : prev;
+            const bool st = p == 0 || p >= s.size || (w[j] >> 8) != (pw >> 8);
             fl |= (st ? 1u : 0u) << j;
-            if (p < s.size) W.perm[p] = static_cast<uint16_t>(w[j] & 0xFFFu);
+            if (p < s.size) W.perm[p] = static_cast<uint16_t>(w[j] & 0xFFu);
         }
+        if (!exact && !__any_sync(0xffffffffu, fl != 0xFFu)) exact = true;  // every run is one string
         uint32_t word = fl << (8 * (lane & 3));
         word |= __shfl_xor_sync(0xffffffffu, word, 1);
         word |= __shfl_xor_sync(0xffffffffu, word, 2);
@@ -1417,7 +1426,9 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
             const uint32_t o = W.off1[slot];
             const uint32_t r0 = run_begin(rb, p), r1 = run_end(rb, p);
             const uint32_t g = r1 - r0;
-            const bool rexact = exact || g <= kTruncFix || zero_index(k) < L + 6;  // as in k_local
+            // (the words kept key bytes [L, L+3) whole: a terminator there
+            // makes the run's strings identical)
+            const bool rexact = exact || g <= kTruncFix || zero_index(k) < L + 3;
             const uint32_t dst = s.begin + p;
             if (A.lcp && p + 1 == r1 && r1 < s.size)
                 A.lcp[dst] = depth + diff_bytes(k, W.key1[W.perm[r1]]);
