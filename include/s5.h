@@ -60,7 +60,9 @@ typedef struct {
                            * to level 1 (otherwise chosen from the root sample); bit9: the
                            * input handles are n u32 offsets packed into the first 4n bytes
                            * of d_handles (the multi-GPU exchange payload); the output is
-                           * still n int64 handles in d_handles (n >= 2) */
+                           * still n int64 handles in d_handles (n >= 2); bit11: never
+                           * use 32-bit sort words in the one-CTA local tiers (otherwise
+                           * chosen from the root sample's key entropy) */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
     uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (511)  */

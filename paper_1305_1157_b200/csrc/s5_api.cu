@@ -206,6 +206,8 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_local<kLocalThreads>, LocalCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalSThreads>, LocalSCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalXSThreads>, LocalXSCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalXSThreads, true>, LocalXSCfg::total);
+        if (!rc) rc = set_smem(k_local<kLocalSThreads, true>, LocalSCfg::total);
         if (!rc) rc = set_smem(k_local<kLocalMThreads>, LocalMCfg::total);
     });
     return rc;
@@ -990,14 +992,22 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         }
         if (m[LOCAL_XS]) {
             prof.begin(S5_K_LOCAL_XS, h.elems[LOCAL_XS]);
-            k_local<kLocalXSThreads>
-                <<<m[LOCAL_XS], kLocalXSThreads, LocalXSCfg::total, lane(0)>>>(A, segs[LOCAL_XS]);
+            if (h.w32)  // high-entropy keys (root sample): 32-bit sort words
+                k_local<kLocalXSThreads, true>
+                    <<<m[LOCAL_XS], kLocalXSThreads, LocalXSCfg::total, lane(0)>>>(A, segs[LOCAL_XS]);
+            else
+                k_local<kLocalXSThreads>
+                    <<<m[LOCAL_XS], kLocalXSThreads, LocalXSCfg::total, lane(0)>>>(A, segs[LOCAL_XS]);
             prof.end();
         }
         if (m[LOCAL_S]) {
             prof.begin(S5_K_LOCAL_S, h.elems[LOCAL_S]);
-            k_local<kLocalSThreads>
-                <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, lane(1)>>>(A, segs[LOCAL_S]);
+            if (h.w32)
+                k_local<kLocalSThreads, true>
+                    <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, lane(1)>>>(A, segs[LOCAL_S]);
+            else
+                k_local<kLocalSThreads>
+                    <<<m[LOCAL_S], kLocalSThreads, LocalSCfg::total, lane(1)>>>(A, segs[LOCAL_S]);
             prof.end();
         }
         if (m[LOCAL_M]) {

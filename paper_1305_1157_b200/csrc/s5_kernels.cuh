@@ -37,9 +37,9 @@ struct Ctl {
     unsigned long long hints;     // boundary LCP hints appended to the hint list
     uint32_t wide_ctas;           // plan: CTAs of the current wide launch
     uint32_t k2;                  // root tree: carry second key words to level 1
+    uint32_t w32;                 // root tree: high-entropy keys, 32-bit local sort words
     unsigned long long tree_words, hist_words;  // plan: pool use of the current level
     uint32_t plan_err;            // plan: ERR_POOL (sticky; the plan runs before the level's reset)
-    uint32_t pad_;
 };
 
 enum : uint32_t { ERR_RANGE = 1, ERR_LIST = 2, ERR_POOL = 4 };
@@ -784,9 +784,8 @@ __device__ __forceinline__ void warp_merge256(T (&w)[8], uint32_t lane) {
 // search and merges them serially (one shared load per output, no
 // divergence).  O(n log n) work, no padding to a power of two; positions
 // >= n_live are never touched.
-template <uint32_t THREADS>
-__device__ __forceinline__ void block_merge_sort8(uint64_t (&w)[8], uint64_t* sb,
-                                                  uint32_t n_live) {
+template <uint32_t THREADS, typename T = uint64_t>
+__device__ __forceinline__ void block_merge_sort8(T (&w)[8], T* sb, uint32_t n_live) {
     const uint32_t my = 8 * threadIdx.x;
     const bool live = my < n_live;
     if (8 * (threadIdx.x & ~31u) < n_live) {  // warp holds live words: runs of 256 in registers
@@ -812,8 +811,8 @@ __device__ __forceinline__ void block_merge_sort8(uint64_t (&w)[8], uint64_t* sb
                 else hi = mid;
             }
             uint32_t ia = a0 + lo, ib = a1 + diag - lo;
-            uint64_t va = ia < a1 ? sb[swz(ia)] : ~0ull;
-            uint64_t vb = ib < b1 ? sb[swz(ib)] : ~0ull;
+            T va = ia < a1 ? sb[swz(ia)] : static_cast<T>(~T(0));
+            T vb = ib < b1 ? sb[swz(ib)] : static_cast<T>(~T(0));
 #pragma unroll
             for (uint32_t j = 0; j < 8; ++j) {
                 const bool pa = va <= vb;  // an exhausted side holds ~0 (live words are smaller)
@@ -821,7 +820,7 @@ __device__ __forceinline__ void block_merge_sort8(uint64_t (&w)[8], uint64_t* sb
                 ia += pa;
                 ib += !pa;
                 const uint32_t nx = pa ? ia : ib;
-                const uint64_t nv = (pa ? ia < a1 : ib < b1) ? sb[swz(nx)] : ~0ull;
+                const T nv = (pa ? ia < a1 : ib < b1) ? sb[swz(nx)] : static_cast<T>(~T(0));
                 va = pa ? nv : va;
                 vb = pa ? vb : nv;
             }
@@ -998,7 +997,7 @@ struct LocalSmem {
 // the cached full keys in shared memory
 constexpr uint32_t kTruncFix = 64;
 
-template <uint32_t THREADS>
+template <uint32_t THREADS, bool W32 = false>
 __global__ void __launch_bounds__(THREADS, (THREADS >= 512 ? 2 : THREADS >= 256 ? 4 : THREADS >= 128 ? 8 : 16))
 k_local(SortArgs A, const Seg* __restrict__ segs) {
     using LS = LocalSmem<THREADS>;
@@ -1092,7 +1091,53 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     // With L >= 2 the word holds the whole key (exact); with L < 2 the key's
     // last 12 (L = 0) or 4 (L = 1) bits are dropped, so runs of equal words
     // are only candidate ties, resolved from the segment depth
-    const bool exact = L >= 2;
+    // Sort words: the key bytes after the common prefix with the slot in the
+    // low bits.  W32 (CTAs of <= 128 threads, launched when the root sample
+    // found high-entropy keys, ctl->w32): 32-bit words of SB slot bits and
+    // the next KB = 32 - SB key bits -- single-instruction compare-exchanges;
+    // the words hold the whole key when L >= 6, else equal words are
+    // candidate runs ranked by the full keys below, skipped when the sort
+    // left none.  Otherwise 64-bit words (52 key bits, the whole key when
+    // L >= 2).
+    static_assert(!W32 || THREADS <= 128, "32-bit words need <= 1024 strings");
+    constexpr uint32_t SB = THREADS == 128 ? 10u : THREADS == 64 ? 9u : 12u;
+    constexpr uint32_t KB = 32u - SB;  // key bits in a 32-bit word
+    constexpr bool use32 = W32;
+    bool cand_any = true;  // use32: the sort left candidate runs
+    if (use32 && !(A.flags & 16)) {
+        uint32_t* sb32 = reinterpret_cast<uint32_t*>(sb);
+        uint32_t w[8];
+        {
+            uint64_t kk[8];
+            load8(key1, 8 * t, kk);  // key1 published by the last prefix barrier
+#pragma unroll
+            for (uint32_t j = 0; j < 8; ++j) {
+                const uint32_t i = 8 * t + j;
+                w[j] = i < s.size ? ((static_cast<uint32_t>((kk[j] << (8 * L)) >> (64 - KB)) << SB) | i) : ~0u;
+            }
+        }
+        block_merge_sort8<THREADS, uint32_t>(w, sb32, (s.size + 7) & ~7u);
+        *reinterpret_cast<uint4*>(sb32 + 8 * t) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(sb32 + 8 * t + 4) = make_uint4(w[4], w[5], w[6], w[7]);
+        __syncthreads();
+        if (t == 0) {
+            bits[N / 32] = 1u;
+            nties = 0;
+            nkids = 0;
+            npairs = 0;
+        }
+        bool cand = false;
+#pragma unroll 1
+        for (uint32_t p = t; p < N; p += THREADS) {
+            const uint32_t wp = sb32[p];
+            const bool st = p == 0 || p >= s.size || (wp >> SB) != (sb32[p - 1] >> SB);
+            cand |= !st;
+            const uint32_t b = __ballot_sync(0xffffffffu, st);
+            if (lane == 0) bits[p >> 5] = b;
+            if (p < s.size) perm[p] = static_cast<uint16_t>(wp & ((1u << SB) - 1u));
+        }
+        cand_any = __syncthreads_or(cand);
+    } else {
     uint64_t w[8];
     if (A.flags & 16) {  // power-of-two bitonic network over the whole CTA
 #pragma unroll
@@ -1129,6 +1174,11 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         if (p < s.size) perm[p] = static_cast<uint16_t>(wp & 0xFFFu);
     }
     __syncthreads();
+    }
+    // key bytes after the prefix the words hold whole; whole keys in the
+    // words, or no candidate run (every run is one string)
+    const uint32_t kept = use32 ? KB / 8 : 6u;
+    const bool exact = use32 ? (8 * (8 - L) <= KB || !cand_any) : L >= 2;
     const uint32_t* rb = bits;
     if (!exact) {
         // truncated words: candidate runs of <= kTruncFix strings are put in
@@ -1187,7 +1237,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         // keys of the run are equal: exact words, a re-ranked short run, or a
         // terminator inside the bytes the truncated words kept whole ([0, L+6):
         // the run's strings are then identical -- short duplicates finish here)
-        const bool rexact = exact || g <= kTruncFix || zero_index(k) < L + 6;
+        const bool rexact = exact || g <= kTruncFix || zero_index(k) < L + kept;
         const uint32_t dst = s.begin + p;
         if (A.lcp && p + 1 == r1 && r1 < s.size)
             A.lcp[dst] = depth + diff_bytes(k, key1[(perm[r1])]);
@@ -1853,6 +1903,22 @@ __global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P) {
                     s.size / (g.v + 1) > A.local_max;
     }
     sort_sample<TT>(sample, M);
+    if (A.k2_stage == 1) {
+        // the keys' entropy from the root sample: when nearly every sampled
+        // key has its own leading 3-byte window, the one-CTA local tiers sort
+        // on 32-bit words (a window + the slot) -- low-entropy data (DNA,
+        // Markov text, URLs) would only turn them into candidate runs
+        uint32_t same = 0;
+        for (uint32_t t = 1 + threadIdx.x; t < m; t += TT)
+            same += (sample[t] >> 40) == (sample[t - 1] >> 40);
+        same = __reduce_add_sync(0xffffffffu, same);
+        __shared__ uint32_t s_same;
+        if (threadIdx.x == 0) s_same = 0;
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) atomicAdd(&s_same, same);
+        __syncthreads();
+        if (threadIdx.x == 0) A.ctl->w32 = (A.flags & 2048) == 0 && m >= 256 && s_same * 64 <= m;
+    }
     uint64_t* tree = P.tree_pool + P.tree_off[blockIdx.x];
     build_tree_levels<TT>(sample, m, g.d, tree, na, nb, nf);
     // classification table for k_wide_count, once per segment
