@@ -37,7 +37,7 @@ def audited_sort(arena, handles, depth, cfg, counters, audit, lcp_out):
             s1 = np.ctypeslib.as_array(side1, shape=(nn,)).astype(np.int64)
             for i in range(nsegs):
                 sg = segs[i]
-                audit(s1 if sg.side else s0, int(sg.begin), int(sg.begin + sg.size), int(sg.depth))
+                audit(s1 if sg.side & 1 else s0, int(sg.begin), int(sg.begin + sg.size), int(sg.depth))
         except Exception as e:  # surface after the C call returns
             errors.append(e)
 

@@ -782,6 +782,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         A.key2[s] = reinterpret_cast<uint64_t*>(ws + L.key2[s]);
     }
     A.k2_depth = static_cast<uint32_t>(depth);
+    A.k2_cap = n > c.narrow_max;  // the key2 arrays exist (make_layout)
     A.out = d_handles;
     A.lcp = d_lcp;
     A.hint_list = reinterpret_cast<uint2*>(ws + L.hints);
@@ -973,7 +974,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
                 k_wide_scatter_tma<512, 2048>
                     <<<ub, 512, WideTmaSmem<2048>::bytes(c.wide_dcap), st>>>(A, P);
             else
-                k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::bytes(c.wide_dcap, A.k2_stage != 0), st>>>(A, P);
+                k_wide_scatter<<<ub, kWideThreads, WideScatterSmem::bytes(c.wide_dcap, A.k2_cap != 0), st>>>(A, P);
             prof.end();
         }
         if (m[NARROW]) {

@@ -79,7 +79,40 @@ struct SortArgs {
     uint64_t* key2[2];
     uint32_t k2_stage;
     uint32_t k2_depth;
+    // Below the root the same arrays carry an equality bucket's second word
+    // one level: a segment with Seg.side bit 1 set ("k2-valid") has in
+    // key2[side & 1] the string bytes [depth+8, depth+16).  The wide scatter
+    // fetches 16 bytes for the strings of an equality bucket (one random
+    // access, like the 8-byte refetch) and flags the child; the child's own
+    // equality buckets then take their next key from key2 instead of the
+    // arena -- every other level of a shared-prefix chain without a random
+    // fetch.  k2_cap: the arrays exist (n > narrow_max).
+    uint32_t k2_cap;
 };
+
+// ping-pong side of a segment, and its second-key-word flag (see SortArgs)
+__device__ __forceinline__ uint32_t sd(const Seg& s) { return s.side & 1u; }
+__device__ __forceinline__ bool k2v(const Seg& s) { return (s.side & 2u) != 0; }
+
+// second key words of the root (k2_stage 1: gathered by the count, carried by
+// the scatter) and of level 1 (k2_stage 2, segments still at the root depth)
+__device__ __forceinline__ uint32_t k2_mode(const SortArgs& A, const Seg& s) {
+    if (!A.k2_stage || !A.ctl->k2) return 0;
+    if (A.k2_stage == 1) return 1;
+    return s.depth == A.k2_depth ? 2u : 0u;
+}
+
+// What a distribution step does with second key words: 1 / 2 the root's
+// carry (k2_mode), 3 = the segment is k2-valid (equality buckets read their
+// next key from key2), 4 = fetch 16 bytes for equality buckets and flag the
+// children k2-valid, 0 = plain 8-byte refetch.
+enum : uint32_t { K2_NONE = 0, K2_ROOT = 1, K2_LEVEL1 = 2, K2_USE = 3, K2_MAKE = 4 };
+__device__ __forceinline__ uint32_t k2_kind(const SortArgs& A, const Seg& s) {
+    const uint32_t m = k2_mode(A, s);
+    if (m) return m;
+    if (k2v(s)) return K2_USE;
+    return A.k2_cap ? K2_MAKE : K2_NONE;
+}
 
 constexpr uint32_t kNarrowThreads = 512;
 constexpr uint32_t kNarrowDMax = 8;           // v <= 255, k <= 511
@@ -352,6 +385,7 @@ __device__ __forceinline__ void emit_block(const SortArgs& A, const Seg& s, cons
         es->elems[threadIdx.x] = 0;
     }
     if (threadIdx.x == 0) es->hints = 0;
+    const bool make2 = k2_kind(A, s) == K2_MAKE;  // the scatter fetches 16 bytes for them
     __syncthreads();
     uint32_t my_hints = 0;
     uint32_t my_elems[NCLS] = {};
@@ -392,7 +426,8 @@ __device__ __forceinline__ void emit_block(const SortArgs& A, const Seg& s, cons
         int cls = size_class(A, cnt);
         uint32_t slot = es->base[cls] + atomicAdd(&es->cnt[cls], 1u);
         if (slot < A.cap[cls])
-            A.next[cls][slot] = Seg{s.begin + st, cnt, s.depth + (odd ? 8u : 0u), s.side ^ 1u};
+            A.next[cls][slot] = Seg{s.begin + st, cnt, s.depth + (odd ? 8u : 0u),
+                                    (sd(s) ^ 1u) | (odd && make2 ? 2u : 0u)};
     }
 }
 
@@ -400,33 +435,44 @@ __device__ __forceinline__ void emit_block(const SortArgs& A, const Seg& s, cons
 // LCP), refetched key at depth+8 for equality buckets, plain move otherwise.
 __device__ __forceinline__ void place(const SortArgs& A, const Seg& s, uint32_t b, bool fin,
                                       uint32_t p, uint32_t bucket_end, uint32_t o, uint64_t k,
-                                      unsigned long long& fetches) {
+                                      unsigned long long& fetches, uint32_t kind = K2_NONE,
+                                      uint32_t src = 0) {
     uint32_t dst = s.begin + p;
-    uint32_t ns = s.side ^ 1u;
+    uint32_t ns = sd(s) ^ 1u;
     if (fin) {
         A.out[dst] = o;
         if ((b & 1) && A.lcp && p + 1 < bucket_end) A.lcp[dst] = s.depth + zero_index(k);
     } else if (b & 1) {
         A.off[ns][dst] = o;
-        A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + s.depth + 8);
-        ++fetches;
+        if (kind == K2_USE) {  // the carried word (src = the string's index on this side)
+            A.key[ns][dst] = A.key2[sd(s)][src];
+        } else if (kind == K2_MAKE) {  // 16 bytes: the next key and the one after
+            uint64_t k0, k1;
+            load_key2(A.arena, static_cast<uint64_t>(o) + s.depth + 8, k0, k1);
+            A.key[ns][dst] = k0;
+            A.key2[ns][dst] = k1;
+            ++fetches;
+        } else {
+            A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + s.depth + 8);
+            ++fetches;
+        }
     } else {
         A.off[ns][dst] = o;
         A.key[ns][dst] = k;
     }
 }
 
-// place() of the root and level-1 scatters when second key words are live
-// (mode 1: root, mode 2: level 1; src = the string's absolute source index)
+// place() with second key words (mode = k2_kind; 1: root, 2: level 1, else
+// place()'s own kinds; src = the string's absolute source index)
 __device__ __forceinline__ void place_k2(const SortArgs& A, const Seg& s, uint32_t b, bool fin,
                                          uint32_t p, uint32_t bucket_end, uint32_t o, uint64_t k,
                                          uint32_t mode, uint32_t src, unsigned long long& fetches) {
-    if (!mode) {
-        place(A, s, b, fin, p, bucket_end, o, k, fetches);
+    if (mode != K2_ROOT && mode != K2_LEVEL1) {
+        place(A, s, b, fin, p, bucket_end, o, k, fetches, mode, src);
         return;
     }
     const uint32_t dst = s.begin + p;
-    const uint32_t ns = s.side ^ 1u;
+    const uint32_t ns = sd(s) ^ 1u;
     if (fin) {
         A.out[dst] = o;
         if ((b & 1) && A.lcp && p + 1 < bucket_end) A.lcp[dst] = s.depth + zero_index(k);
@@ -440,11 +486,6 @@ __device__ __forceinline__ void place_k2(const SortArgs& A, const Seg& s, uint32
     }
 }
 
-__device__ __forceinline__ uint32_t k2_mode(const SortArgs& A, const Seg& s) {
-    if (!A.k2_stage || !A.ctl->k2) return 0;
-    if (A.k2_stage == 1) return 1;
-    return s.depth == A.k2_depth ? 2u : 0u;
-}
 
 // level-0 input handle i of the caller's array (int64, or u32 offsets with
 // cfg flags bit9 -- the multi-GPU exchange's payload), streamed once
@@ -519,8 +560,8 @@ __global__ void __launch_bounds__(256) k_small(SortArgs A, const Seg* __restrict
     const Seg s = segs[warp];
     const bool valid = lane < s.size;
     const bool pair_valid = lane + 1 < s.size;
-    uint32_t o = valid ? A.off[s.side][s.begin + lane] : 0u;
-    uint64_t k = valid ? A.key[s.side][s.begin + lane] : ~0ull;
+    uint32_t o = valid ? A.off[sd(s)][s.begin + lane] : 0u;
+    uint64_t k = valid ? A.key[sd(s)][s.begin + lane] : ~0ull;
     uint32_t run = valid ? 0u : 0xFFFFFFFFu;
     uint64_t depth = s.depth;
     bool resolved = false;
@@ -1017,9 +1058,10 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     __shared__ uint32_t nties, nkids, npairs;
 
     Seg s = segs[blockIdx.x];
+    const uint32_t depth0 = s.depth;  // the carried second words hold [depth0+8, depth0+16)
     const uint32_t t = threadIdx.x, lane = t & 31;
-    const uint32_t* __restrict__ goff = A.off[s.side] + s.begin;
-    const uint64_t* __restrict__ gkey = A.key[s.side] + s.begin;
+    const uint32_t* __restrict__ goff = A.off[sd(s)] + s.begin;
+    const uint64_t* __restrict__ gkey = A.key[sd(s)] + s.begin;
 
     // the segment in registers (coalesced)
     uint64_t rk[8];
@@ -1225,7 +1267,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     // per position: finished strings go out, children to the other side,
     // LCPs at run boundaries and inside identical runs; ties are listed
     const uint32_t tmax = A.small_max;
-    const uint32_t ns = s.side ^ 1u;
+    const uint32_t ns = sd(s) ^ 1u;
     const uint64_t depth = s.depth;
 #pragma unroll 1
     for (uint32_t p = t; p < s.size; p += THREADS) {
@@ -1246,7 +1288,9 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
             if (A.lcp && p + 1 < r1) A.lcp[dst] = depth + zero_index(k);
         } else if (g > 2 && g > tmax) {
             A.off[ns][dst] = o;
-            if (rexact) {
+            if (rexact && k2v(s) && depth == depth0) {  // the carried word (slot = input index)
+                A.key[ns][dst] = A.key2[sd(s)][s.begin + slot];
+            } else if (rexact) {
                 A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + depth + 8);
                 ++fetches;
             } else {
@@ -1340,8 +1384,9 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
     if (si >= nsegs) return;  // warp scope only: no block barriers below
     WarpLocalSmem& W = wsm[wid];
     Seg s = segs[si];
-    const uint32_t* __restrict__ goff = A.off[s.side] + s.begin;
-    const uint64_t* __restrict__ gkey = A.key[s.side] + s.begin;
+    const uint32_t depth0 = s.depth;
+    const uint32_t* __restrict__ goff = A.off[sd(s)] + s.begin;
+    const uint64_t* __restrict__ gkey = A.key[sd(s)] + s.begin;
     uint64_t rk[8];
     uint32_t ro[8];
 #pragma unroll
@@ -1467,7 +1512,7 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
         }
         // per position, as in k_local; children are emitted one by one
         const uint32_t tmax = A.small_max;
-        const uint32_t ns = s.side ^ 1u;
+        const uint32_t ns = sd(s) ^ 1u;
         const uint64_t depth = s.depth;
 #pragma unroll 1
         for (uint32_t p = lane; p < s.size; p += 32) {
@@ -1487,7 +1532,9 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
                 if (A.lcp && p + 1 < r1) A.lcp[dst] = depth + zero_index(k);
             } else if (g > 2 && g > tmax) {
                 A.off[ns][dst] = o;
-                if (rexact) {
+                if (rexact && k2v(s) && depth == depth0) {  // the carried word
+                    A.key[ns][dst] = A.key2[sd(s)][s.begin + slot];
+                } else if (rexact) {
                     A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + depth + 8);
                     ++fetches;
                 } else {
@@ -1583,8 +1630,8 @@ k_narrow(SortArgs A, const Seg* __restrict__ segs) {
 
     Seg s = segs[blockIdx.x];
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t* off = A.off[s.side] + s.begin;
-    uint64_t* key = A.key[s.side] + s.begin;  // rewritten in place by the prefix skip
+    const uint32_t* off = A.off[sd(s)] + s.begin;
+    uint64_t* key = A.key[sd(s)] + s.begin;  // rewritten in place by the prefix skip
     uint32_t dw = A.dmax < kNarrowDMax ? A.dmax : kNarrowDMax;
     uint32_t d = ceil_log2((s.size + A.wide_target - 1) / A.wide_target);
     d = d < 1 ? 1 : (d > dw ? dw : d);
@@ -1686,7 +1733,7 @@ k_narrow(SortArgs A, const Seg* __restrict__ segs) {
 
     // stage 4: distribution (samplesort.py:146-152): classify again, slot
     // from the bucket's cursor
-    const uint32_t k2m = k2_mode(A, s);
+    const uint32_t k2m = k2_kind(A, s);
     for (uint32_t t = 0; t < ntiles; ++t) {
         const uint32_t q = ntiles + t;
         const uint32_t base = t * TILE, cnt = min(TILE, s.size - base);
@@ -1861,7 +1908,7 @@ __global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P) {
     if (m > kWideSampleCap) m = kWideSampleCap;
     uint32_t M = 64;
     while (M < m) M <<= 1;
-    const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
+    const uint64_t* __restrict__ key = A.key[sd(s)] + s.begin;
     const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
     __shared__ uint32_t bytemask[8][8];  // root: byte values seen per key position
     if (threadIdx.x < 64) bytemask[threadIdx.x >> 3][threadIdx.x & 7] = 0;
@@ -2012,7 +2059,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
     }
     for (uint32_t b = threadIdx.x; b < g.k; b += kWideThreads) hist[b] = 0;
     __syncthreads();
-    const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
+    const uint64_t* __restrict__ key = A.key[sd(s)] + s.begin;
     uint16_t* __restrict__ bkt = P.bkt + s.begin;
     if (!EQUAL) {  // table classification (same buckets, fewer dependent loads)
         LutTree T;
@@ -2225,7 +2272,8 @@ __global__ void __launch_bounds__(256) k_wide_bscan(SortArgs A, WidePlan P) {
     __syncthreads();
     if (threadIdx.x == 0) starts[g.k + 1] = solo;
     if (solo) {
-        if (threadIdx.x == 0) emit_child(A, s.begin, s.size, s.depth + 8, s.side);
+        if (threadIdx.x == 0)
+            emit_child(A, s.begin, s.size, s.depth + 8, sd(s) | (k2_kind(A, s) == K2_MAKE ? 2u : 0u));
         return;
     }
     __shared__ EmitScratch es;
@@ -2237,12 +2285,21 @@ __global__ void __launch_bounds__(256) k_wide_bscan(SortArgs A, WidePlan P) {
 // root gathered them, else one arena fetch per string.
 __device__ __forceinline__ void advance_keys(const SortArgs& A, const Seg& s, uint32_t lo, uint32_t hi,
                                              uint32_t threads, unsigned long long& fetches) {
-    const uint32_t k2m = k2_mode(A, s);
-    const uint32_t* __restrict__ off = A.off[s.side] + s.begin;
-    uint64_t* key = A.key[s.side] + s.begin;
+    const uint32_t k2m = k2_kind(A, s);
+    const uint32_t* __restrict__ off = A.off[sd(s)] + s.begin;
+    uint64_t* key = A.key[sd(s)] + s.begin;
+    uint64_t* key2 = A.key2[sd(s)] + s.begin;
     for (uint32_t i = lo + threadIdx.x; i < hi; i += threads) {
-        if (k2m) {
+        if (k2m == K2_ROOT || k2m == K2_LEVEL1) {
             key[i] = __ldcs(A.key2[k2m - 1] + s.begin + i);
+        } else if (k2m == K2_USE) {
+            key[i] = __ldcs(key2 + i);
+        } else if (k2m == K2_MAKE) {  // the child (this range, k2-valid) keeps the word after
+            uint64_t k0, k1;
+            load_key2(A.arena, static_cast<uint64_t>(__ldcs(off + i)) + s.depth + 8, k0, k1);
+            key[i] = k0;
+            key2[i] = k1;
+            ++fetches;
         } else {
             key[i] = load_key(A.arena, static_cast<uint64_t>(__ldcs(off + i)) + s.depth + 8);
             ++fetches;
@@ -2273,7 +2330,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
     uint16_t* sb = reinterpret_cast<uint16_t*>(so + kWideTile);
     uint16_t* sx = sb + kWideTile;  // tile-relative source index (second key words)
     const uint32_t kc = 2u << A.wide_dcap;
-    uint32_t* cur = reinterpret_cast<uint32_t*>(A.k2_stage ? sx + kWideTile : sx);
+    uint32_t* cur = reinterpret_cast<uint32_t*>(A.k2_cap ? sx + kWideTile : sx);
     uint32_t* cnt = cur + kc;
     uint32_t* gb = cnt + kc + 4;
     uint32_t* warp_sums = gb + kc + 4;
@@ -2299,12 +2356,13 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
         bool fin = n_b == 1 || ((b & 1) && has_zero_byte(tree[node_of_rank(b >> 1, g.d)]));
         cur[b] = (st + rows[static_cast<uint64_t>(c) * g.k + b]) | (fin ? 0x80000000u : 0u);
     }
-    const uint32_t* __restrict__ off = A.off[s.side] + s.begin;
-    const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
+    const uint32_t* __restrict__ off = A.off[sd(s)] + s.begin;
+    const uint64_t* __restrict__ key = A.key[sd(s)] + s.begin;
     const uint16_t* __restrict__ bkt = P.bkt + s.begin;
     const uint32_t lane = threadIdx.x & 31;
     unsigned long long fetches = 0;
-    const uint32_t k2m = k2_mode(A, s);
+    const uint32_t k2m = k2_kind(A, s);
+    const bool need_src = k2m != K2_NONE && k2m != K2_MAKE;  // sx: the source index of a slot
     constexpr uint32_t IT = kWideTile / kWideThreads;
     uint64_t kk[IT];
     uint32_t oo[IT], br[IT];  // bucket | rank-in-tile << 16
@@ -2341,7 +2399,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
                 sk[p] = kk[j];
                 so[p] = oo[j];
                 sb[p] = static_cast<uint16_t>(b);
-                if (k2m) sx[p] = static_cast<uint16_t>(j * kWideThreads + threadIdx.x);
+                if (need_src) sx[p] = static_cast<uint16_t>(j * kWideThreads + threadIdx.x);
             }
         }
         if (base + kWideTile < hi) load_tile(base + kWideTile);
@@ -2354,7 +2412,8 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
             uint32_t p = (r & 0x7FFFFFFFu) + (t - cnt[b]);
             uint32_t end = fin && (b & 1) ? starts[b + 1] : 0;
             if (k2m)
-                place_k2(A, s, b, fin, p, end, so[t], sk[t], k2m, s.begin + base + sx[t], fetches);
+                place_k2(A, s, b, fin, p, end, so[t], sk[t], k2m, need_src ? s.begin + base + sx[t] : 0u,
+                         fetches);
             else
                 place(A, s, b, fin, p, end, so[t], sk[t], fetches);
         }
@@ -2418,8 +2477,8 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
         if ((threadIdx.x & 31) == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
         return;
     }
-    const uint32_t* __restrict__ off = A.off[s.side] + s.begin;
-    const uint64_t* __restrict__ key = A.key[s.side] + s.begin;
+    const uint32_t* __restrict__ off = A.off[sd(s)] + s.begin;
+    const uint64_t* __restrict__ key = A.key[sd(s)] + s.begin;
     const uint16_t* __restrict__ bkt = P.bkt + s.begin;
     auto issue = [&](uint32_t base, uint32_t buf) {
         const uint32_t m = min(kTmaTile, hi - base);
@@ -2446,7 +2505,7 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
             if (lo + q * kTmaTile < hi) issue(lo + q * kTmaTile, q);
     constexpr uint32_t IT = kTmaTile / kTmaThreads;
     unsigned long long fetches = 0;
-    const uint32_t k2m = k2_mode(A, s);
+    const uint32_t k2m = k2_kind(A, s);
     uint32_t t = 0, buf = 0, phase = 0;
 #pragma unroll 1
     for (uint32_t base = lo; base < hi; base += kTmaTile, ++t) {
