@@ -475,6 +475,27 @@ public:
         std::unique_lock<std::mutex> lk(mu_);
         done_.wait(lk, [&] { return left_ == 0; });
     }
+    unsigned threads() const { return T_; }
+    // f(tid, T) once on every pool thread (tid 0 = the caller)
+    void run_all(const std::function<void(unsigned, unsigned)>& f) {
+        if (T_ == 1) {
+            f(0, 1);
+            return;
+        }
+        std::lock_guard<std::mutex> job(job_mu_);
+        const unsigned T = T_;
+        auto part = [&, T](unsigned i) { f(i, T); };
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            job_ = part;
+            left_ = T_ - 1;
+            ++gen_;
+        }
+        go_.notify_all();
+        part(0);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return left_ == 0; });
+    }
 };
 
 // Host staging kernels.  The output streams are written once and not read
@@ -485,7 +506,10 @@ bool has_avx2() {
     return v;
 }
 
-// int64 handles -> u32 offsets with the range check; true if any is outside [0, lim)
+// int64 handles -> u32 offsets with the range check; true if any is outside [0, lim).
+// NT: non-temporal stores (a staging buffer larger than the host cache);
+// otherwise plain stores, so a small staging slot stays cached for the DMA read
+template <bool NT = true>
 __attribute__((target("avx2"))) bool narrow_u32_avx2(const int64_t* src, uint32_t* dst, uint64_t n,
                                                      uint64_t lim) {
     uint64_t i = 0, bad = 0;
@@ -504,13 +528,14 @@ __attribute__((target("avx2"))) bool narrow_u32_avx2(const int64_t* src, uint32_
         badv = _mm256_or_si256(badv, _mm256_or_si256(_mm256_cmpgt_epi64(zero, b), _mm256_cmpgt_epi64(b, top)));
         const __m128i la = _mm256_castsi256_si128(_mm256_permutevar8x32_epi32(a, lows));
         const __m128i lb = _mm256_castsi256_si128(_mm256_permutevar8x32_epi32(b, lows));
-        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), _mm256_set_m128i(lb, la));
+        if (NT) _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), _mm256_set_m128i(lb, la));
+        else _mm256_store_si256(reinterpret_cast<__m256i*>(dst + i), _mm256_set_m128i(lb, la));
     }
     for (; i < n; ++i) {
         bad |= static_cast<uint64_t>(src[i]) >= lim;
         dst[i] = static_cast<uint32_t>(src[i]);
     }
-    _mm_sfence();
+    if (NT) _mm_sfence();
     return bad || !_mm256_testz_si256(badv, badv);
 }
 
@@ -535,8 +560,9 @@ __attribute__((target("avx2"))) void widen_avx2(const T* src, int64_t* dst, uint
     _mm_sfence();
 }
 
+template <bool NT = true>
 bool narrow_u32(const int64_t* src, uint32_t* dst, uint64_t n, uint64_t lim) {
-    if (has_avx2()) return narrow_u32_avx2(src, dst, n, lim);
+    if (has_avx2()) return narrow_u32_avx2<NT>(src, dst, n, lim);
     uint64_t bad = 0;
     for (uint64_t i = 0; i < n; ++i) {
         bad |= static_cast<uint64_t>(src[i]) >= lim;
@@ -592,6 +618,19 @@ struct HostPath {
     void* xbuf = nullptr;  // narrowing scratch of the standalone transfer entries
     uint64_t xbytes = 0;
     static constexpr uint64_t kChunk = 32ull << 20;  // bytes per staging buffer
+    // staging ring (S5_HOST_RING, default: both directions): R pinned slots of
+    // P bytes (default 48 x 2 MiB); the copy engine and the host workers each
+    // run ahead on their own pieces -- no barrier per piece as in the
+    // three-stage path (config 2 e2e 12.5-13.3 -> 11.2-11.4 ms, same box,
+    // profiles/e2e_ring.py)
+    static constexpr int kRingMax = 64;
+    int ring = -1;  // -1: not configured yet
+    char* rbuf = nullptr;
+    uint64_t rP = 0;
+    int rR = 0;
+    cudaEvent_t rev[kRingMax] = {};
+    std::atomic<int64_t> rready[kRingMax];
+    std::atomic<int64_t> rfreed[kRingMax];
 };
 
 HostPath& host_path() { return per_device<HostPath>(); }
@@ -614,7 +653,169 @@ int host_path_init(HostPath& H) {
     }
     S5_CUDA(cudaMalloc(&H.dmax, sizeof(unsigned long long)));
     S5_CUDA(cudaHostAlloc(&H.hmax, sizeof(unsigned long long), cudaHostAllocDefault));
+    // bit 0: downloads through the ring, bit 1: uploads too, bit 2: plain
+    // (cached) narrowing stores into the ring instead of non-temporal ones
+    const char* r = getenv("S5_HOST_RING");
+    H.ring = Pool::get().threads() >= 2 ? (r ? atoi(r) : 3) : 0;  // a scheduler + at least one worker
+    if (H.ring) {
+        const char* p = getenv("S5_RING_PIECE");
+        const char* q = getenv("S5_RING_SLOTS");
+        H.rP = p ? strtoull(p, nullptr, 10) : (2ull << 20);
+        H.rP = std::max<uint64_t>(64 << 10, std::min<uint64_t>(H.rP, 16ull << 20)) & ~uint64_t(255);
+        H.rR = q ? atoi(q) : 48;
+        H.rR = std::max(2, std::min(H.rR, HostPath::kRingMax));
+        S5_CUDA(cudaHostAlloc(&H.rbuf, H.rP * H.rR, cudaHostAllocDefault));
+        for (int i = 0; i < H.rR; ++i) S5_CUDA(cudaEventCreateWithFlags(&H.rev[i], cudaEventDisableTiming));
+    }
     return 0;
+}
+
+// The staging ring.  The caller's thread (pool thread 0) schedules the DMA
+// in piece order on the caller's stream and retires finished copies by
+// event queries; the other pool threads claim pieces in order and narrow
+// (H2D) or widen (D2H) them.  Slot s holds pieces s, s + R, ...; per slot
+// `rready` is the last piece made ready for the other side and `rfreed` the
+// last piece whose slot use is over.  A worker never waits for the others,
+// only for its own piece's slot or copy.
+struct RingPiece {
+    const char* d;   // device source (D2H)
+    int64_t* h;      // host destination (D2H)
+    uint64_t count;
+    uint32_t w;
+};
+
+template <typename Sched, typename Work>
+int ring_run(HostPath& H, uint64_t K, Sched&& sched_step, Work&& work) {
+    const int R = H.rR;
+    for (int s = 0; s < R; ++s) {
+        H.rready[s].store(static_cast<int64_t>(s) - R, std::memory_order_relaxed);
+        H.rfreed[s].store(static_cast<int64_t>(s) - R, std::memory_order_relaxed);
+    }
+    std::atomic<uint64_t> next{0};
+    std::atomic<int> abort{0};
+    std::atomic<int> err{0};
+    Pool::get().run_all([&](unsigned tid, unsigned) {
+        if (tid == 0) {
+            if (int e = sched_step(abort)) {
+                err.store(e);
+                abort.store(1);
+            }
+            return;
+        }
+        for (;;) {
+            const uint64_t k = next.fetch_add(1, std::memory_order_relaxed);
+            if (k >= K) return;
+            if (!work(k, abort)) return;
+        }
+    });
+    return err.load();
+}
+
+int host_upload_ring(HostPath& H, const int64_t* h_handles, uint64_t n, uint64_t arena_len,
+                     uint32_t* d32, cudaStream_t st) {
+    const int R = H.rR;
+    const uint64_t E = H.rP / 4;
+    const uint64_t K = (n + E - 1) / E;
+    std::atomic<bool> bad{false};
+    auto sched = [&](std::atomic<int>& abort) -> int {
+        uint64_t issued = 0, retired = 0;
+        while (retired < K) {
+            bool progress = false;
+            if (issued < K) {
+                const int s = static_cast<int>(issued % R);
+                if (H.rready[s].load(std::memory_order_acquire) == static_cast<int64_t>(issued)) {
+                    const uint64_t len = std::min(E, n - issued * E);
+                    S5_CUDA(cudaMemcpyAsync(d32 + issued * E, H.rbuf + uint64_t(s) * H.rP, len * 4,
+                                            cudaMemcpyHostToDevice, st));
+                    S5_CUDA(cudaEventRecord(H.rev[s], st));
+                    ++issued;
+                    progress = true;
+                }
+            }
+            if (retired < issued) {
+                const int s = static_cast<int>(retired % R);
+                const cudaError_t q = cudaEventQuery(H.rev[s]);
+                if (q == cudaSuccess) {
+                    H.rfreed[s].store(static_cast<int64_t>(retired), std::memory_order_release);
+                    ++retired;
+                    progress = true;
+                } else if (q != cudaErrorNotReady) {
+                    return fail(S5_E_CUDA, "staging DMA failed: %s", cudaGetErrorString(q));
+                }
+            }
+            if (!progress) _mm_pause();
+            if (abort.load(std::memory_order_relaxed)) return 0;
+        }
+        return 0;
+    };
+    auto work = [&](uint64_t k, std::atomic<int>& abort) -> bool {
+        const int s = static_cast<int>(k % R);
+        const int64_t want = static_cast<int64_t>(k) - R;
+        while (H.rfreed[s].load(std::memory_order_acquire) != want)
+            if (abort.load(std::memory_order_relaxed)) return false; else _mm_pause();
+        const uint64_t len = std::min(E, n - k * E);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(H.rbuf + uint64_t(s) * H.rP);
+        if ((H.ring & 4) ? narrow_u32<false>(h_handles + k * E, dst, len, arena_len)
+                         : narrow_u32<true>(h_handles + k * E, dst, len, arena_len))
+            bad.store(true, std::memory_order_relaxed);
+        H.rready[s].store(static_cast<int64_t>(k), std::memory_order_release);
+        return true;
+    };
+    if (int e = ring_run(H, K, sched, work)) return e;
+    if (bad.load()) return fail(S5_E_RANGE, "handle outside the arena");
+    return 0;
+}
+
+int host_download_ring(HostPath& H, const std::vector<RingPiece>& pieces, cudaStream_t st) {
+    const int R = H.rR;
+    const uint64_t K = pieces.size();
+    auto sched = [&](std::atomic<int>& abort) -> int {
+        uint64_t issued = 0, retired = 0;
+        while (retired < K) {
+            bool progress = false;
+            if (issued < K) {
+                const int s = static_cast<int>(issued % R);
+                if (H.rfreed[s].load(std::memory_order_acquire) == static_cast<int64_t>(issued) - R) {
+                    const RingPiece& P = pieces[issued];
+                    S5_CUDA(cudaMemcpyAsync(H.rbuf + uint64_t(s) * H.rP, P.d, P.count * P.w,
+                                            cudaMemcpyDeviceToHost, st));
+                    S5_CUDA(cudaEventRecord(H.rev[s], st));
+                    ++issued;
+                    progress = true;
+                }
+            }
+            if (retired < issued) {
+                const int s = static_cast<int>(retired % R);
+                const cudaError_t q = cudaEventQuery(H.rev[s]);
+                if (q == cudaSuccess) {
+                    H.rready[s].store(static_cast<int64_t>(retired), std::memory_order_release);
+                    ++retired;
+                    progress = true;
+                } else if (q != cudaErrorNotReady) {
+                    return fail(S5_E_CUDA, "staging DMA failed: %s", cudaGetErrorString(q));
+                }
+            }
+            if (!progress) _mm_pause();
+            if (abort.load(std::memory_order_relaxed)) return 0;
+        }
+        return 0;
+    };
+    auto work = [&](uint64_t k, std::atomic<int>& abort) -> bool {
+        const int s = static_cast<int>(k % R);
+        while (H.rready[s].load(std::memory_order_acquire) != static_cast<int64_t>(k))
+            if (abort.load(std::memory_order_relaxed)) return false; else _mm_pause();
+        const RingPiece& P = pieces[k];
+        const char* sp = H.rbuf + uint64_t(s) * H.rP;
+        switch (P.w) {
+            case 1: widen(reinterpret_cast<const uint8_t*>(sp), P.h, P.count); break;
+            case 2: widen(reinterpret_cast<const uint16_t*>(sp), P.h, P.count); break;
+            case 4: widen(reinterpret_cast<const uint32_t*>(sp), P.h, P.count); break;
+            default: memcpy(P.h, sp, P.count * 8);
+        }
+        H.rfreed[s].store(static_cast<int64_t>(k), std::memory_order_release);
+        return true;
+    };
+    return ring_run(H, K, sched, work);
 }
 
 int host_scratch(HostPath& H, uint64_t bytes) {
@@ -631,6 +832,15 @@ int host_scratch(HostPath& H, uint64_t bytes) {
 // on the device; chunk i is narrowed while chunk i-1 is in flight
 int host_upload(HostPath& H, const int64_t* h_handles, uint64_t n, uint64_t arena_len,
                 uint32_t* d32, int64_t* dh, cudaStream_t st) {
+    if (H.ring & 2) {
+        if (int e = host_upload_ring(H, h_handles, n, arena_len, d32, st)) {
+            cudaStreamSynchronize(st);
+            return e;
+        }
+        if (dh) k_widen32<<<grid_for(n, 256), 256, 0, st>>>(d32, dh, n);
+        S5_CUDA(cudaStreamSynchronize(st));
+        return 0;
+    }
     Pool& pool = Pool::get();
     const uint64_t per = H.piece;
     constexpr int NS = HostPath::kStages;
@@ -678,6 +888,23 @@ int host_download(HostPath& H, const int64_t* dh, uint64_t n, const int64_t* dl,
         if (w == 4) k_shrink<uint32_t><<<g, 256, 0, st>>>(dl, static_cast<uint32_t*>(dn), nl);
     }
     S5_CUDA(cudaGetLastError());
+    if (H.ring & 1) {
+        std::vector<RingPiece> rp;
+        const uint64_t e4 = H.rP / 4;
+        for (uint64_t off = 0; off < n; off += e4)
+            rp.push_back({reinterpret_cast<const char*>(d32 + off), h_handles + off, std::min(e4, n - off), 4});
+        if (dl && h_lcp && nl) {
+            const char* src = w == 8 ? reinterpret_cast<const char*>(dl) : static_cast<const char*>(dn);
+            const uint64_t ew = H.rP / w;
+            for (uint64_t off = 0; off < nl; off += ew)
+                rp.push_back({src + off * w, h_lcp + off, std::min(ew, nl - off), w});
+        }
+        *bytes = n * 4 + (dl && h_lcp ? nl * w : 0);
+        if (rp.empty()) return 0;
+        const int e = host_download_ring(H, rp, st);
+        S5_CUDA(cudaStreamSynchronize(st));
+        return e;
+    }
     struct Piece { const char* d; int64_t* h; uint64_t count; uint32_t w; };
     std::vector<Piece> pieces;
     for (uint64_t off = 0; off < n; off += per)
