@@ -38,7 +38,7 @@ enum {
     S5_E_INVALID = -1,   /* bad argument: unterminated arena, bad v, ... (ValueError) */
     S5_E_CUDA = -2,      /* CUDA runtime error (RuntimeError)                          */
     S5_E_WORKSPACE = -3, /* workspace too small                                        */
-    S5_E_RANGE = -4,     /* handle outside the arena / arena >= 4 GiB / n >= 2^31      */
+    S5_E_RANGE = -4,     /* handle outside the arena / n >= 2^31                        */
     S5_E_INTERNAL = -5,  /* internal capacity exceeded (bug)                           */
     S5_E_NCCL = -6       /* NCCL error (multi-GPU entry points)                        */
 };
@@ -62,7 +62,11 @@ typedef struct {
                            * of d_handles (the multi-GPU exchange payload); the output is
                            * still n int64 handles in d_handles (n >= 2); bit11: never
                            * use 32-bit sort words in the one-CTA local tiers (otherwise
-                           * chosen from the root sample's key entropy) */
+                           * chosen from the root sample's key entropy); bit13: index
+                           * mode -- the u32 offset arrays hold string indices and an
+                           * int64 position table (8n more workspace bytes) maps them
+                           * to the arena; always on for arenas >= 4 GiB (the
+                           * reference's handles are int64 offsets, strings.py:3-7) */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
     uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (511)  */

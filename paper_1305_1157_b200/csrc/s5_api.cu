@@ -115,7 +115,7 @@ uint64_t align_up(uint64_t x, uint64_t a = 256) { return (x + a - 1) / a * a; }
 
 struct Layout {
     uint64_t off[2], key[2], key2[2], lists[2][NCLS], cta_start, tree_off, hist_off, tree_pool, hist_pool,
-        ctl, hints, bkt, total;
+        ctl, hints, bkt, pos, total;
     uint32_t cap[NCLS];
     uint64_t tree_cap, hist_cap;
 };
@@ -157,6 +157,8 @@ Layout make_layout(uint64_t n, const Cfg& c) {
     L.bkt = take(n * 2);
     L.ctl = take(sizeof(Ctl));
     for (int s = 0; s < 2; ++s) L.key2[s] = take(n > c.narrow_max ? n * 8 : 0);
+    // flags bit13 (arenas >= 4 GiB): the string-index -> arena-position table
+    L.pos = take((c.flags & 8192) ? n * 8 : 0);
     L.total = at;
     return L;
 }
@@ -197,6 +199,7 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_wide_tree<kTreeThreadsFew>, kWideTreeSmem);
         if (!rc) rc = set_smem(k_wide_count<false>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_count<true>, kWideSmem);
+        if (!rc) rc = set_smem(k_wide_count<false, true>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_scatter, WideScatterSmem::total);
         if (!rc) rc = set_smem(k_wide_scatter_tma<1024, 4096>, WideTmaSmem<4096>::bytes(kWideDMax));
         if (!rc) rc = set_smem(k_wide_scatter_tma<1024, 4096, kRootStages>,
@@ -955,9 +958,9 @@ int s5_version(void) { return 1; }
 const char* s5_last_error(void) { return g_err.c_str(); }
 
 uint64_t s5_workspace_bytes(uint64_t n, uint64_t arena_len, const s5_config* cfg) {
-    (void)arena_len;
     Cfg c;
     if (resolve(cfg, &c)) return 0;
+    if (arena_len >= (1ull << 32)) c.flags |= 8192;  // index mode: + the position table
     return make_layout(n, c).total;
 }
 
@@ -973,9 +976,13 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     if (reinterpret_cast<uintptr_t>(d_arena) % 8)
         return fail(S5_E_INVALID, "device arena must be 8-byte aligned");
     if (arena_len == 0) return fail(S5_E_INVALID, "empty arena with n > 1 handles");
-    if (arena_len >= (1ull << 32))
-        return fail(S5_E_RANGE, "arena of %llu bytes: offsets are 32-bit (< 4 GiB)",
-                    (unsigned long long)arena_len);
+    // arenas of >= 4 GiB (or flags bit13) sort string indices through a
+    // position table (SortArgs::pos, index mode)
+    if (arena_len >= (1ull << 32)) c.flags |= 8192;
+    const bool indexed = (c.flags & 8192) != 0;
+    if (indexed && audit) return fail(S5_E_INVALID, "the audit replay is not available in index mode");
+    if (arena_len >= (1ull << 32) && (c.flags & 512))
+        return fail(S5_E_INVALID, "u32 input offsets (flags bit9) cannot name an arena of >= 4 GiB");
     if (n >= (1ull << 31)) return fail(S5_E_RANGE, "n must be < 2^31");
     if (depth >= arena_len) return fail(S5_E_RANGE, "depth beyond arena");
     Layout L = make_layout(n, c);
@@ -1008,6 +1015,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         A.key[s] = reinterpret_cast<uint64_t*>(ws + L.key[s]);
         A.key2[s] = reinterpret_cast<uint64_t*>(ws + L.key2[s]);
     }
+    A.pos = indexed ? reinterpret_cast<int64_t*>(ws + L.pos) : nullptr;
     A.k2_depth = static_cast<uint32_t>(depth);
     A.k2_cap = n > c.narrow_max;  // the key2 arrays exist (make_layout)
     A.out = d_handles;
@@ -1174,6 +1182,8 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             prof.begin(S5_K_WIDE_COUNT, h.elems[WIDE]);
             if (c.classifier)
                 k_wide_count<true><<<ub, kWideThreads, wsm, st>>>(A, P);
+            else if (indexed && level == 0)  // fills the position table
+                k_wide_count<false, true><<<ub, kWideThreads, wsm, st>>>(A, P);
             else
                 k_wide_count<false><<<ub, kWideThreads, wsm, st>>>(A, P);
             prof.end();
@@ -1319,9 +1329,9 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
     }
     Cfg c;
     if (int rc = resolve(cfg, &c)) return rc;
-    if (arena_len > 0xFFFFFFFFull)
-        return fail(S5_E_RANGE, "arena of %llu bytes: offsets are 32-bit (< 4 GiB)",
-                    static_cast<unsigned long long>(arena_len));
+    // arenas of >= 4 GiB (or flags bit13): int64 handles both ways, index mode
+    const bool indexed = arena_len >= (1ull << 32) || (c.flags & 8192);
+    if (indexed) c.flags |= 8192;
     uint64_t ws = make_layout(n, c).total;
     uint64_t need = 2 * align_up(n * 8) + 2 * align_up(n * 4) + ws;
     if (need > H.dbytes) {
@@ -1345,10 +1355,15 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
     s5_config cc{};
     if (cfg) cc = *cfg;
     else cc.seed = 1;
-    cc.flags |= 512;
     auto t0 = std::chrono::steady_clock::now();
-    if (int rc = host_upload(H, h_handles, n, arena_len, reinterpret_cast<uint32_t*>(dh), nullptr, st))
-        return rc;
+    if (indexed) {
+        cc.flags |= 8192;
+        S5_CUDA(cudaMemcpyAsync(dh, h_handles, n * 8, cudaMemcpyHostToDevice, st));
+    } else {
+        cc.flags |= 512;
+        if (int rc = host_upload(H, h_handles, n, arena_len, reinterpret_cast<uint32_t*>(dh), nullptr, st))
+            return rc;
+    }
     auto t1 = std::chrono::steady_clock::now();
     int rc = s5_sort(d_arena, arena_len, dh, n, depth, h_lcp ? dl : nullptr, &cc, dws, ws,
                      stream_, stats);
@@ -1356,15 +1371,21 @@ int s5_sort_host(const uint8_t* d_arena, uint64_t arena_len, int64_t* h_handles,
     S5_CUDA(cudaStreamSynchronize(st));
     auto t2 = std::chrono::steady_clock::now();
     uint64_t d2h_bytes = 0;
-    if (int e = host_download(H, dh, n, h_lcp ? dl : nullptr, n - 1, d32, dn, h_handles, h_lcp, st,
-                              &d2h_bytes))
+    if (indexed) {
+        S5_CUDA(cudaMemcpyAsync(h_handles, dh, n * 8, cudaMemcpyDeviceToHost, st));
+        if (h_lcp) S5_CUDA(cudaMemcpyAsync(h_lcp, dl, (n - 1) * 8, cudaMemcpyDeviceToHost, st));
+        S5_CUDA(cudaStreamSynchronize(st));
+        d2h_bytes = n * 8 + (h_lcp ? (n - 1) * 8 : 0);
+    } else if (int e = host_download(H, dh, n, h_lcp ? dl : nullptr, n - 1, d32, dn, h_handles, h_lcp,
+                                     st, &d2h_bytes)) {
         return e;
+    }
     auto t3 = std::chrono::steady_clock::now();
     if (stats) {
         stats->host_h2d_ms = std::chrono::duration<float, std::milli>(t1 - t0).count();
         stats->host_sort_ms = std::chrono::duration<float, std::milli>(t2 - t1).count();
         stats->host_d2h_ms = std::chrono::duration<float, std::milli>(t3 - t2).count();
-        stats->host_h2d_bytes = n * 4;
+        stats->host_h2d_bytes = indexed ? n * 8 : n * 4;
         stats->host_d2h_bytes = d2h_bytes;
     }
     return 0;

@@ -88,7 +88,22 @@ struct SortArgs {
     // arena -- every other level of a shared-prefix chain without a random
     // fetch.  k2_cap: the arrays exist (n > narrow_max).
     uint32_t k2_cap;
+    // Arenas of >= 4 GiB (the reference's handles are int64 offsets,
+    // strings.py:3-7): the u32 offset arrays hold each string's index in the
+    // caller's array and `pos` (a copy of the handles, filled by level 0)
+    // maps it to the arena position -- one more load per key refetch, none
+    // on the key-only paths.  Null for arenas below 4 GiB.
+    int64_t* pos;
 };
+
+// arena position / final handle of the string an offset word names
+__device__ __forceinline__ uint64_t apos(const int64_t* pos, uint32_t o) {
+    return pos ? static_cast<uint64_t>(__ldg(pos + o)) : o;
+}
+__device__ __forceinline__ uint64_t apos(const SortArgs& A, uint32_t o) { return apos(A.pos, o); }
+__device__ __forceinline__ int64_t ahandle(const SortArgs& A, uint32_t o) {
+    return static_cast<int64_t>(apos(A.pos, o));
+}
 
 // ping-pong side of a segment, and its second-key-word flag (see SortArgs)
 __device__ __forceinline__ uint32_t sd(const Seg& s) { return s.side & 1u; }
@@ -440,7 +455,7 @@ __device__ __forceinline__ void place(const SortArgs& A, const Seg& s, uint32_t 
     uint32_t dst = s.begin + p;
     uint32_t ns = sd(s) ^ 1u;
     if (fin) {
-        A.out[dst] = o;
+        A.out[dst] = ahandle(A, o);
         if ((b & 1) && A.lcp && p + 1 < bucket_end) A.lcp[dst] = s.depth + zero_index(k);
     } else if (b & 1) {
         A.off[ns][dst] = o;
@@ -448,12 +463,12 @@ __device__ __forceinline__ void place(const SortArgs& A, const Seg& s, uint32_t 
             A.key[ns][dst] = A.key2[sd(s)][src];
         } else if (kind == K2_MAKE) {  // 16 bytes: the next key and the one after
             uint64_t k0, k1;
-            load_key2(A.arena, static_cast<uint64_t>(o) + s.depth + 8, k0, k1);
+            load_key2(A.arena, apos(A, o) + s.depth + 8, k0, k1);
             A.key[ns][dst] = k0;
             A.key2[ns][dst] = k1;
             ++fetches;
         } else {
-            A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + s.depth + 8);
+            A.key[ns][dst] = load_key(A.arena, apos(A, o) + s.depth + 8);
             ++fetches;
         }
     } else {
@@ -474,7 +489,7 @@ __device__ __forceinline__ void place_k2(const SortArgs& A, const Seg& s, uint32
     const uint32_t dst = s.begin + p;
     const uint32_t ns = sd(s) ^ 1u;
     if (fin) {
-        A.out[dst] = o;
+        A.out[dst] = ahandle(A, o);
         if ((b & 1) && A.lcp && p + 1 < bucket_end) A.lcp[dst] = s.depth + zero_index(k);
     } else if (b & 1) {  // equality bucket: its next key is the carried word
         A.off[ns][dst] = o;
@@ -505,7 +520,8 @@ __global__ void k_gather(const int64_t* __restrict__ handles, const uint32_t* __
             atomicOr(&A.ctl->err, ERR_RANGE);
             h = 0;
         }
-        A.off[0][i] = static_cast<uint32_t>(h);
+        if (A.pos) A.pos[i] = h;
+        A.off[0][i] = A.pos ? i : static_cast<uint32_t>(h);
         A.key[0][i] = load_key(A.arena, static_cast<uint64_t>(h) + depth);
     }
 }
@@ -589,12 +605,12 @@ __global__ void __launch_bounds__(256) k_small(SortArgs A, const Seg* __restrict
         bool active = ((unres >> lane) & 1u) || prev_unres;
         depth += 8;
         if (active) {
-            k = load_key(A.arena, static_cast<uint64_t>(o) + depth);
+            k = load_key(A.arena, apos(A, o) + depth);
             ++fetches;
         }
         run = valid ? run_start : 0xFFFFFFFFu;
     }
-    if (valid) A.out[s.begin + lane] = o;
+    if (valid) A.out[s.begin + lane] = ahandle(A, o);
     if (pair_valid && A.lcp) A.lcp[s.begin + lane] = static_cast<int64_t>(my_lcp);
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
     if (lane == 0 && fetches) atomicAdd(&A.ctl->fetches, fetches);
@@ -881,7 +897,8 @@ __device__ __forceinline__ void block_merge_sort8(T (&w)[8], T* sb, uint32_t n_l
 __device__ __noinline__ uint32_t tie_group_warp(const uint8_t* __restrict__ arena, int64_t* out,
                                                 int64_t* lcp, uint32_t begin, uint32_t gs,
                                                 uint32_t g, const uint32_t* off1, uint16_t* perm,
-                                                uint64_t depth, uint32_t lane) {
+                                                uint64_t depth, uint32_t lane,
+                                                const int64_t* __restrict__ pos) {
     uint32_t fetches = 0;
     const bool valid = lane < g;
     const bool pair_valid = lane + 1 < g;
@@ -893,7 +910,7 @@ __device__ __noinline__ uint32_t tie_group_warp(const uint8_t* __restrict__ aren
     const uint32_t P = g <= 2 ? 2u : 1u << (32 - __clz(g - 1));
     for (;; depth += 16) {  // 16 string bytes per round
         if (active) {
-            load_key2(arena, static_cast<uint64_t>(off1[e]) + depth, k0, k1);
+            load_key2(arena, apos(pos, off1[e]) + depth, k0, k1);
             ++fetches;
         }
         // bitonic sort of (run, k0, k1), payload e -- skipped when every
@@ -937,7 +954,7 @@ __device__ __noinline__ uint32_t tie_group_warp(const uint8_t* __restrict__ aren
     }
     if (valid) {
         perm[gs + lane] = static_cast<uint16_t>(e);
-        out[begin + gs + lane] = off1[e];
+        out[begin + gs + lane] = static_cast<int64_t>(apos(pos, off1[e]));
     }
     return fetches;
 }
@@ -1101,7 +1118,7 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
                 for (uint32_t j = 0; j < 8; ++j) {
                     uint32_t i = t + j * THREADS;
                     if (i < s.size) {
-                        A.out[s.begin + i] = ro[j];
+                        A.out[s.begin + i] = ahandle(A, ro[j]);
                         if (A.lcp && i + 1 < s.size) A.lcp[s.begin + i] = s.depth + zero_index(k0);
                     }
                 }
@@ -1121,12 +1138,12 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j) {
             if (t + j * THREADS < s.size) {
-                rk[j] = load_key(A.arena, static_cast<uint64_t>(ro[j]) + s.depth);
+                rk[j] = load_key(A.arena, apos(A, ro[j]) + s.depth);
                 key1[t + j * THREADS] = rk[j];
                 ++fetches;
             }
         }
-        k0 = load_key(A.arena, static_cast<uint64_t>(o0) + s.depth);
+        k0 = load_key(A.arena, apos(A, o0) + s.depth);
     }
     if (L > 7) L = 7;  // all keys equal (skip disabled): one run either way
     // sort words: key bytes after the common prefix, slot in the low 12 bits.
@@ -1284,14 +1301,14 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
         if (A.lcp && p + 1 == r1 && r1 < s.size)
             A.lcp[dst] = depth + diff_bytes(k, key1[(perm[r1])]);
         if (g == 1 || (rexact && has_zero_byte(k))) {
-            A.out[dst] = o;
+            A.out[dst] = ahandle(A, o);
             if (A.lcp && p + 1 < r1) A.lcp[dst] = depth + zero_index(k);
         } else if (g > 2 && g > tmax) {
             A.off[ns][dst] = o;
             if (rexact && k2v(s) && depth == depth0) {  // the carried word (slot = input index)
                 A.key[ns][dst] = A.key2[sd(s)][s.begin + slot];
             } else if (rexact) {
-                A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + depth + 8);
+                A.key[ns][dst] = load_key(A.arena, apos(A, o) + depth + 8);
                 ++fetches;
             } else {
                 A.key[ns][dst] = k;
@@ -1310,17 +1327,17 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     for (uint32_t q = t; q < np; q += THREADS) {
         const uint32_t p = pairs[q], sa = perm[p], sb2 = perm[p + 1];
         uint64_t l;
-        const int c = walk_compare(A.arena, off1[sa], off1[sb2], depth + 8, &l, fetches);
+        const int c = walk_compare(A.arena, apos(A, off1[sa]), apos(A, off1[sb2]), depth + 8, &l, fetches);
         if (A.lcp) A.lcp[s.begin + p] = l;
-        A.out[s.begin + p] = off1[c > 0 ? sb2 : sa];
-        A.out[s.begin + p + 1] = off1[c > 0 ? sa : sb2];
+        A.out[s.begin + p] = ahandle(A, off1[c > 0 ? sb2 : sa]);
+        A.out[s.begin + p + 1] = ahandle(A, off1[c > 0 ? sa : sb2]);
     }
     // runs of 3..small_max strings: one warp each
     const uint32_t nt = nties, nk = nkids;
     for (uint32_t q = t >> 5; q < nt; q += THREADS / 32) {
         const uint32_t x = ties[q];
         fetches += tie_group_warp(A.arena, A.out, A.lcp, s.begin, x & 0x1FFFu, x >> 13, off1, perm,
-                                  depth + 8, lane);
+                                  depth + 8, lane, A.pos);
     }
     // children: one list reservation per size class per CTA
     if (nk) {
@@ -1410,7 +1427,7 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
                 for (uint32_t j = 0; j < 8; ++j) {
                     const uint32_t i = lane + 32 * j;
                     if (i < s.size) {
-                        A.out[s.begin + i] = ro[j];
+                        A.out[s.begin + i] = ahandle(A, ro[j]);
                         if (A.lcp && i + 1 < s.size) A.lcp[s.begin + i] = s.depth + zero_index(k0);
                     }
                 }
@@ -1426,7 +1443,7 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
 #pragma unroll
         for (uint32_t j = 0; j < 8; ++j) {
             if (lane + 32 * j < s.size) {
-                rk[j] = load_key(A.arena, static_cast<uint64_t>(ro[j]) + s.depth);
+                rk[j] = load_key(A.arena, apos(A, ro[j]) + s.depth);
                 ++fetches;
             }
         }
@@ -1528,14 +1545,14 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
             if (A.lcp && p + 1 == r1 && r1 < s.size)
                 A.lcp[dst] = depth + diff_bytes(k, W.key1[W.perm[r1]]);
             if (g == 1 || (rexact && has_zero_byte(k))) {
-                A.out[dst] = o;
+                A.out[dst] = ahandle(A, o);
                 if (A.lcp && p + 1 < r1) A.lcp[dst] = depth + zero_index(k);
             } else if (g > 2 && g > tmax) {
                 A.off[ns][dst] = o;
                 if (rexact && k2v(s) && depth == depth0) {  // the carried word
                     A.key[ns][dst] = A.key2[sd(s)][s.begin + slot];
                 } else if (rexact) {
-                    A.key[ns][dst] = load_key(A.arena, static_cast<uint64_t>(o) + depth + 8);
+                    A.key[ns][dst] = load_key(A.arena, apos(A, o) + depth + 8);
                     ++fetches;
                 } else {
                     A.key[ns][dst] = k;
@@ -1553,16 +1570,16 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
         for (uint32_t q = lane; q < W.npairs; q += 32) {  // pairs spread over the lanes
             const uint32_t p = W.pairs[q], sa = W.perm[p], sb2 = W.perm[p + 1];
             uint64_t l;
-            const int c = walk_compare(A.arena, W.off1[sa], W.off1[sb2], depth + 8, &l, fetches);
+            const int c = walk_compare(A.arena, apos(A, W.off1[sa]), apos(A, W.off1[sb2]), depth + 8, &l, fetches);
             if (A.lcp) A.lcp[s.begin + p] = l;
-            A.out[s.begin + p] = W.off1[c > 0 ? sb2 : sa];
-            A.out[s.begin + p + 1] = W.off1[c > 0 ? sa : sb2];
+            A.out[s.begin + p] = ahandle(A, W.off1[c > 0 ? sb2 : sa]);
+            A.out[s.begin + p + 1] = ahandle(A, W.off1[c > 0 ? sa : sb2]);
         }
         const uint32_t nt = W.nties;
         for (uint32_t q = 0; q < nt; ++q) {
             const uint32_t x = W.ties[q];
             fetches += tie_group_warp(A.arena, A.out, A.lcp, s.begin, x & 0x1FFFu, x >> 13, W.off1,
-                                      W.perm, depth + 8, lane);
+                                      W.perm, depth + 8, lane, A.pos);
         }
     }
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
@@ -1662,7 +1679,7 @@ k_narrow(SortArgs A, const Seg* __restrict__ segs) {
         if (mn != mx) break;  // no: an ordinary step (one dominant equality bucket)
         s.depth += 8;
         for (uint32_t i = threadIdx.x; i < s.size; i += T) {
-            key[i] = load_key(A.arena, static_cast<uint64_t>(off[i]) + s.depth);
+            key[i] = load_key(A.arena, apos(A, off[i]) + s.depth);
             ++fetches;
         }
         // generic-proxy writes, read next by the sample and the bulk copies
@@ -1992,7 +2009,7 @@ __device__ __forceinline__ uint32_t find_seg(const uint32_t* cta_start, uint32_t
 // again.
 // Level 0 of k_wide_count with second key words: handle -> (offset, key,
 // next word) gather fused with the classification and the histogram.
-template <bool K2>
+template <bool K2, bool IDX = false>
 __device__ __forceinline__ void root_gather_count(const SortArgs& A, const Seg& s, uint32_t lo,
                                                   uint32_t hi, const LutTree& T, uint32_t* hist,
                                                   uint16_t* __restrict__ bkt) {
@@ -2023,7 +2040,12 @@ __device__ __forceinline__ void root_gather_count(const SortArgs& A, const Seg& 
         for (int j = 0; j < R; ++j) {
             const uint32_t i = base + j * kWideThreads + threadIdx.x;
             if (i < hi) {
-                A.off[0][s.begin + i] = static_cast<uint32_t>(hh[j]);
+                if (IDX) {  // index mode: the offset word names the string, pos its arena position
+                    A.pos[s.begin + i] = hh[j];
+                    A.off[0][s.begin + i] = s.begin + i;
+                } else {
+                    A.off[0][s.begin + i] = static_cast<uint32_t>(hh[j]);
+                }
                 A.key[0][s.begin + i] = kk[j];
                 if (K2) A.key2[0][s.begin + i] = k2w[j];
                 const uint32_t b = classify_lut(kk[j], T);
@@ -2034,7 +2056,9 @@ __device__ __forceinline__ void root_gather_count(const SortArgs& A, const Seg& 
     }
 }
 
-template <bool EQUAL>
+// IDX: the level-0 launch of index mode (its own instantiation: the position
+// table stores would cost the common kernel registers and a CTA per SM)
+template <bool EQUAL, bool IDX = false>
 __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePlan P) {
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t G = blockIdx.x;
@@ -2069,7 +2093,10 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
         T.pf = tsrc[2 * g.v + 1 + kLutTabWords];
         T.lb = static_cast<uint32_t>(tsrc[2 * g.v + 1 + kLutTabWords + 1]);
         if (A.root || A.root32) {  // level 0: handle -> (offset, key) gather fused with the count
-            if (A.k2_stage == 1 && A.ctl->k2) {
+            if (IDX) {  // index mode (arenas >= 4 GiB)
+                if (A.k2_stage == 1 && A.ctl->k2) root_gather_count<true, true>(A, s, lo, hi, T, hist, bkt);
+                else root_gather_count<false, true>(A, s, lo, hi, T, hist, bkt);
+            } else if (A.k2_stage == 1 && A.ctl->k2) {
                 root_gather_count<true>(A, s, lo, hi, T, hist, bkt);
             } else {
                 constexpr int R = 8;
@@ -2296,12 +2323,12 @@ __device__ __forceinline__ void advance_keys(const SortArgs& A, const Seg& s, ui
             key[i] = __ldcs(key2 + i);
         } else if (k2m == K2_MAKE) {  // the child (this range, k2-valid) keeps the word after
             uint64_t k0, k1;
-            load_key2(A.arena, static_cast<uint64_t>(__ldcs(off + i)) + s.depth + 8, k0, k1);
+            load_key2(A.arena, apos(A, __ldcs(off + i)) + s.depth + 8, k0, k1);
             key[i] = k0;
             key2[i] = k1;
             ++fetches;
         } else {
-            key[i] = load_key(A.arena, static_cast<uint64_t>(__ldcs(off + i)) + s.depth + 8);
+            key[i] = load_key(A.arena, apos(A, __ldcs(off + i)) + s.depth + 8);
             ++fetches;
         }
     }

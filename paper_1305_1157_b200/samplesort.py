@@ -238,13 +238,14 @@ def parallel_sample_sort(arena: StringArena, handles, workers: int = 1,
     if devices is None and workers > 1 and torch.cuda.is_available():
         devices = list(range(min(int(workers), torch.cuda.device_count())))
     n = int(len(handles))
-    if audit is None and devices is not None and len(devices) > 1 and n > 1:
+    # the multi-GPU exchange carries u32 offsets: an arena of >= 4 GiB sorts on
+    # one GPU (index mode, include/s5.h)
+    if audit is None and devices is not None and len(devices) > 1 and n > 1 \
+            and arena.size <= 0xFFFFFFFF:
         from .multi import multi_gpu_sort
         on_device = isinstance(handles, torch.Tensor) and handles.is_cuda
         if not on_device and (not isinstance(handles, np.ndarray) or handles.dtype != np.int64):
             raise TypeError("handles must be a numpy int64 array or a CUDA int64 tensor")
-        if arena.size > 0xFFFFFFFF:
-            raise ValueError(f"arena of {arena.size} bytes: offsets are 32-bit (< 4 GiB)")
         h = handles if on_device or (handles.flags.c_contiguous and handles.flags.writeable) \
             else np.ascontiguousarray(handles)
         lo = lcp_out

@@ -518,3 +518,101 @@ def test_duplicate_short_strings_in_truncated_segments(n_dup):
         h = h0.copy()
         _, lcp = sort_with_lcp(arena, h, cfg=cfg)
         _check_sorted(arena, h0, h, want, lcp, want_lcp, f"dup{n_dup}")
+
+
+# ---------------------------------------------------------------------------
+# index mode (cfg flags bit13; always on for arenas >= 4 GiB): the offset
+# arrays hold string indices and a position table maps them to the arena --
+# the reference's handles are int64 offsets (strings.py:3-7)
+
+INDEXED = 8192
+
+
+@pytest.mark.parametrize("cfg_name", ["default", "equal", "tiny_tiers", "wide_everywhere",
+                                      "wide_tma", "narrow_tier", "bitonic_gather"])
+def test_index_mode_matches_reference_golden(sort_cases, cfg_name):
+    import dataclasses
+    base = CONFIGS[cfg_name]
+    cfg = dataclasses.replace(base, flags=base.flags | INDEXED)
+    for name, c in sort_cases.items():
+        arena = StringArena(c["arena"])
+        h = c["handles"].copy()
+        _, lcp = sort_with_lcp(arena, h, cfg=cfg)
+        _check_sorted(arena, c["handles"], h, c["sorted"], lcp, c["lcp"], f"idx/{cfg_name}/{name}")
+
+
+@pytest.mark.parametrize("config,n", [(2, 1 << 20), (3, 1 << 19), (4, 1 << 19), (5, 1 << 20)])
+def test_index_mode_configs_vs_oracle(config, n):
+    import torch
+    arena, h0 = datasets.generate(config, n)
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, O.max_threads())
+    want_lcp = O.adjacent_lcps(arena, want)
+    # device-resident handles and the host path
+    d = torch.from_numpy(h0.copy()).cuda()
+    lcp = torch.empty(d.numel() - 1, dtype=torch.int64, device="cuda")
+    parallel_sample_sort(arena, d, cfg=SampleSortConfig(flags=INDEXED), lcp_out=lcp)
+    _check_sorted(arena, h0, d.cpu().numpy(), want, lcp.cpu().numpy(), want_lcp, f"idx/cfg{config}")
+    h = h0.copy()
+    _, hl = sort_with_lcp(arena, h, cfg=SampleSortConfig(flags=INDEXED, seed=4))
+    _check_sorted(arena, h0, h, want, hl, want_lcp, f"idx/host/cfg{config}")
+
+
+@pytest.mark.parametrize("shape", ["identical", "prefix1000", "nested"])
+def test_index_mode_adversarial_shapes(shape):
+    from paper_1305_1157_b200 import arena_from_strings
+    rng = np.random.default_rng(23)
+    n = 200_000
+    if shape == "identical":
+        strs = [b"the-same-string-repeated"] * n
+    elif shape == "prefix1000":
+        base = bytes(rng.integers(97, 123, 1000).tolist())
+        strs = [base + bytes(rng.integers(97, 99, rng.integers(0, 12)).tolist()) for _ in range(n // 10)]
+    else:
+        strs = [b"a" * int(k) for k in rng.integers(0, 300, n // 3)]
+    arena, h = arena_from_strings(strs)
+    want = h.copy()
+    O.parallel_sample_sort(arena, want, 8)
+    got, lcp = sort_with_lcp(arena, h.copy(), cfg=SampleSortConfig(flags=INDEXED))
+    _check_sorted(arena, h, got, want, lcp, O.adjacent_lcps(arena, want), "idx/" + shape)
+
+
+@pytest.mark.slow
+def test_arena_beyond_4gib():
+    """A 4.25 GiB arena: handles above 2^32, duplicated handles (identical
+    2 KB strings walked to their ends) and strings sharing long prefixes."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < 12 << 30:
+        pytest.skip("needs 12 GiB of free device memory")
+    rng = np.random.default_rng(41)
+    L = 2048                       # bytes per string slot, terminator included
+    n_slots = (17 << 28) // L      # 4.25 GiB
+    data = rng.integers(33, 127, size=n_slots * L, dtype=np.uint8)
+    data[L - 1::L] = 0
+    # slots 1.. copy a long prefix of slot 0 in a few places (deep LCPs high up)
+    for slot in (5, n_slots // 2, n_slots - 3, n_slots - 2):
+        keep = int(rng.integers(500, 1900))
+        data[slot * L: slot * L + keep] = data[:keep]
+    arena = StringArena(data)
+    h0 = np.arange(n_slots, dtype=np.int64) * L
+    # suffix handles (strings starting inside a slot) and duplicates
+    extra = h0[rng.integers(0, n_slots, 100_000)] + rng.integers(0, L - 1, 100_000)
+    dups = h0[rng.integers(n_slots - 50_000, n_slots, 60_000)]
+    h0 = np.concatenate([h0, extra, dups])
+    rng.shuffle(h0)
+    assert int(h0.max()) >= 1 << 32
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, O.max_threads())
+    want_lcp = O.adjacent_lcps(arena, want)
+    d = torch.from_numpy(h0.copy()).cuda()
+    lcp = torch.empty(d.numel() - 1, dtype=torch.int64, device="cuda")
+    parallel_sample_sort(arena, d, lcp_out=lcp)
+    _check_sorted(arena, h0, d.cpu().numpy(), want, lcp.cpu().numpy(), want_lcp, "4gib/device")
+    del d, lcp
+    h = h0.copy()
+    _, hl = sort_with_lcp(arena, h)     # host path: int64 handles both ways
+    _check_sorted(arena, h0, h, want, hl, want_lcp, "4gib/host")
+    from paper_1305_1157_b200 import samplesort as SS
+    arena.drop_device()
+    SS.release_workspace()
