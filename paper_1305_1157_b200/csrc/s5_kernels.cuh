@@ -886,28 +886,54 @@ __device__ __forceinline__ void block_merge_sort8(T (&w)[8], T* sb, uint32_t n_l
     }
 }
 
-// A run of g <= 32 strings at sorted positions gs..gs+g-1 whose keys agree
-// below `depth`, finished by one warp: bitonic sort of (run, 16 string
-// bytes) with refills 16 bytes deeper while pairs stay unresolved (the mkqs
-// equal-partition refill, basesort.py:146-150, as warp rounds); writes the
-// pair LCPs, the order and the final handles.
+// Runs of 3..32 strings whose keys agree below `depth` (the tie list of a
+// segment), finished by one warp, several runs per pass: the runs ties[q],
+// ties[q+1], ... are packed into the 32 lanes, each in an aligned block of
+// its size rounded up to a power of two, while they fit.  One bitonic sort
+// of (run, 16 string bytes) over the widest block then orders every packed
+// run at once, with refills 16 bytes deeper while pairs stay unresolved (the
+// mkqs equal-partition refill, basesort.py:146-150, as warp rounds); writes
+// the pair LCPs, the order and the final handles.  A pass costs one network
+// and one arena round trip per 16 bytes whatever it holds, so URL-like
+// segments (many runs of 3-8 strings) take a fraction of the passes.
+// Run ids are 2 x the run's first lane; lanes that hold no string (block
+// padding, alignment holes, the tail) carry 2 x lane + 1, so every tuple's
+// id grows with its lane and the sort leaves each run in its own lanes.
 // Plain pointers, not the SortArgs: a reference to the kernel's parameter
 // block makes every thread copy it to local memory (measured: ~19 B of DRAM
-// writes per string on the local tier).  Returns this lane's arena fetches.
-__device__ __noinline__ uint32_t tie_group_warp(const uint8_t* __restrict__ arena, int64_t* out,
-                                                int64_t* lcp, uint32_t begin, uint32_t gs,
-                                                uint32_t g, const uint32_t* off1, uint16_t* perm,
-                                                uint64_t depth, uint32_t lane,
-                                                const int64_t* __restrict__ pos) {
+// writes per string on the local tier).  Returns (this lane's arena fetches,
+// runs consumed).
+__device__ __noinline__ uint2 tie_batch_warp(const uint8_t* __restrict__ arena, int64_t* out,
+                                             int64_t* lcp, uint32_t begin, const uint32_t* ties,
+                                             uint32_t q, uint32_t qend, const uint32_t* off1,
+                                             uint16_t* perm, uint64_t depth, uint32_t lane,
+                                             const int64_t* __restrict__ pos) {
     uint32_t fetches = 0;
-    const bool valid = lane < g;
-    const bool pair_valid = lane + 1 < g;
-    uint32_t e = valid ? perm[gs + lane] : 0u;
-    uint32_t run = valid ? 0u : 0xFFFFFFFFu;
+    // packing (uniform over the warp: every lane walks the same list entries)
+    uint32_t used = 0, cursor = 0, P = 2;
+    uint32_t my_r0 = 0, my_start = 0, my_g = 0;
+#pragma unroll 1
+    while (q + used < qend) {
+        const uint32_t x = ties[q + used];
+        const uint32_t g = (x >> 13) & 0x3FFFu, B = g <= 2 ? 2u : 1u << (32 - __clz(g - 1));
+        const uint32_t st = (cursor + B - 1) & ~(B - 1);
+        if (st + B > 32) break;
+        if (lane >= st && lane < st + g) {
+            my_r0 = x & 0x1FFFu;
+            my_start = st;
+            my_g = g;
+        }
+        cursor = st + B;
+        P = B > P ? B : P;
+        ++used;
+    }
+    const bool valid = my_g != 0;
+    const bool pair_valid = valid && lane + 1 < my_start + my_g;
+    const uint32_t at = my_r0 + lane - my_start;  // sorted position of this lane (valid lanes)
+    uint32_t e = valid ? perm[at] : 0u;
+    uint32_t run = valid ? 2 * my_start : 2 * lane + 1;
     uint64_t k0 = ~0ull, k1 = ~0ull;
     bool resolved = false, active = valid;
-    // network width: the group's lanes [0, P) (the rest hold no string)
-    const uint32_t P = g <= 2 ? 2u : 1u << (32 - __clz(g - 1));
     for (;; depth += 16) {  // 16 string bytes per round
         if (active) {
             load_key2(arena, apos(pos, off1[e]) + depth, k0, k1);
@@ -915,7 +941,7 @@ __device__ __noinline__ uint32_t tie_group_warp(const uint8_t* __restrict__ aren
         }
         // bitonic sort of (run, k0, k1), payload e -- skipped when every
         // open run reads the same 16 bytes (identical strings so far)
-        const uint32_t lead = run & 31u;
+        const uint32_t lead = (run >> 1) & 31u;
         const uint64_t l0 = __shfl_sync(0xffffffffu, k0, lead);
         const uint64_t l1 = __shfl_sync(0xffffffffu, k1, lead);
         const bool same = !active || (k0 == l0 && k1 == l1);
@@ -929,7 +955,9 @@ __device__ __noinline__ uint32_t tie_group_warp(const uint8_t* __restrict__ aren
                 uint32_t oe = __shfl_xor_sync(0xffffffffu, e, J);
                 bool olt = orun < run || (orun == run && (o0 < k0 || (o0 == k0 && o1 < k1)));
                 bool mlt = run < orun || (run == orun && (k0 < o0 || (k0 == o0 && k1 < o1)));
-                bool take = (((lane & J) == 0) == ((lane & K) == 0)) ? olt : mlt;
+                // every P-block ends ascending (the last merge), blocks alternate before
+                const bool up = (lane & K) == 0 || K == P;
+                bool take = (((lane & J) == 0) == up) ? olt : mlt;
                 if (take) { run = orun; k0 = o0; k1 = o1; e = oe; }
             }
         }
@@ -942,7 +970,7 @@ __device__ __noinline__ uint32_t tie_group_warp(const uint8_t* __restrict__ aren
             else if (has_zero_byte(k0)) { l = depth + zero_index(k0); resolved = true; }
             else if (k1 != n1) { l = depth + 8 + diff_bytes(k1, n1); resolved = true; }
             else if (has_zero_byte(k1)) { l = depth + 8 + zero_index(k1); resolved = true; }
-            if (resolved && lcp) lcp[begin + gs + lane] = l;
+            if (resolved && lcp) lcp[begin + at] = l;
         }
         uint32_t unres = __ballot_sync(0xffffffffu, pair_valid && !resolved);
         if (!unres) break;
@@ -950,13 +978,13 @@ __device__ __noinline__ uint32_t tie_group_warp(const uint8_t* __restrict__ aren
         uint32_t starts = __ballot_sync(0xffffffffu, !prev_unres);
         uint32_t le = starts & (lane == 31 ? 0xffffffffu : ((2u << lane) - 1u));
         active = ((unres >> lane) & 1u) || prev_unres;
-        if (valid) run = 31u - __clz(le);
+        if (valid) run = 2 * (31u - __clz(le));
     }
     if (valid) {
-        perm[gs + lane] = static_cast<uint16_t>(e);
-        out[begin + gs + lane] = static_cast<int64_t>(apos(pos, off1[e]));
+        perm[at] = static_cast<uint16_t>(e);
+        out[begin + at] = static_cast<int64_t>(apos(pos, off1[e]));
     }
-    return fetches;
+    return make_uint2(fetches, used);
 }
 
 // strings.py:64-74 (_compare_from) + :56-61 (_lcp_pair) in one walk from a
@@ -1334,10 +1362,17 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
     }
     // runs of 3..small_max strings: one warp each
     const uint32_t nt = nties, nk = nkids;
-    for (uint32_t q = t >> 5; q < nt; q += THREADS / 32) {
-        const uint32_t x = ties[q];
-        fetches += tie_group_warp(A.arena, A.out, A.lcp, s.begin, x & 0x1FFFu, x >> 13, off1, perm,
-                                  depth + 8, lane, A.pos);
+    {  // each warp takes a contiguous share of the list, several runs per pass
+        constexpr uint32_t NWP = THREADS / 32;
+        const uint32_t share = (nt + NWP - 1) / NWP;
+        uint32_t q = (t >> 5) * share;
+        const uint32_t qend = min(nt, q + share);
+        while (q < qend) {
+            const uint2 r = tie_batch_warp(A.arena, A.out, A.lcp, s.begin, ties, q, qend, off1, perm,
+                                           depth + 8, lane, A.pos);
+            fetches += r.x;
+            q += r.y;
+        }
     }
     // children: one list reservation per size class per CTA
     if (nk) {
@@ -1576,10 +1611,11 @@ __global__ void __launch_bounds__(kWarpLocalWarps * 32) k_local_w(SortArgs A, co
             A.out[s.begin + p + 1] = ahandle(A, W.off1[c > 0 ? sa : sb2]);
         }
         const uint32_t nt = W.nties;
-        for (uint32_t q = 0; q < nt; ++q) {
-            const uint32_t x = W.ties[q];
-            fetches += tie_group_warp(A.arena, A.out, A.lcp, s.begin, x & 0x1FFFu, x >> 13, W.off1,
-                                      W.perm, depth + 8, lane, A.pos);
+        for (uint32_t q = 0; q < nt;) {  // several runs per pass
+            const uint2 r = tie_batch_warp(A.arena, A.out, A.lcp, s.begin, W.ties, q, nt, W.off1,
+                                           W.perm, depth + 8, lane, A.pos);
+            fetches += r.x;
+            q += r.y;
         }
     }
     for (uint32_t x = 16; x > 0; x >>= 1) fetches += __shfl_xor_sync(0xffffffffu, fetches, x);
