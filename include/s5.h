@@ -66,7 +66,10 @@ typedef struct {
                            * mode -- the u32 offset arrays hold string indices and an
                            * int64 position table (8n more workspace bytes) maps them
                            * to the arena; always on for arenas >= 4 GiB (the
-                           * reference's handles are int64 offsets, strings.py:3-7) */
+                           * reference's handles are int64 offsets, strings.py:3-7);
+                           * bit14: no root prefix skip (otherwise, when the root sample's
+                           * keys share 2..7 leading bytes, level 0 classifies the 8 bytes
+                           * behind them after checking every string against the prefix) */
     uint64_t seed;        /* sample seed (samplesort.py:45)                     */
     uint32_t local_max;   /* segments <= local_max: one CTA finishes them (<=4096)*/
     uint32_t wide_v;      /* splitters of multi-CTA steps, 2^d-1 <= 1023 (511)  */

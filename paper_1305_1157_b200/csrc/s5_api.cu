@@ -200,6 +200,8 @@ int init_attributes() {
         if (!rc) rc = set_smem(k_wide_count<false>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_count<true>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_count<false, true>, kWideSmem);
+        if (!rc) rc = set_smem(k_wide_count<false, false, true>, kWideSmem);
+        if (!rc) rc = set_smem(k_wide_count<false, true, true>, kWideSmem);
         if (!rc) rc = set_smem(k_wide_scatter, WideScatterSmem::total);
         if (!rc) rc = set_smem(k_wide_scatter_tma<1024, 4096>, WideTmaSmem<4096>::bytes(kWideDMax));
         if (!rc) rc = set_smem(k_wide_scatter_tma<1024, 4096, kRootStages>,
@@ -1016,7 +1018,6 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         A.key2[s] = reinterpret_cast<uint64_t*>(ws + L.key2[s]);
     }
     A.pos = indexed ? reinterpret_cast<int64_t*>(ws + L.pos) : nullptr;
-    A.k2_depth = static_cast<uint32_t>(depth);
     A.k2_cap = n > c.narrow_max;  // the key2 arrays exist (make_layout)
     A.out = d_handles;
     A.lcp = d_lcp;
@@ -1052,10 +1053,6 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     P.bkt = reinterpret_cast<uint16_t*>(ws + L.bkt);
     P.hist_cap = L.hist_cap;
 
-    // level 0: cached keys at the common depth, root segment
-    int cur = 0;
-    for (int q = 0; q < NCLS; ++q) A.next[q] = reinterpret_cast<Seg*>(ws + L.lists[cur][q]);
-    S5_CUDA(cudaMemsetAsync(A.ctl, 0, sizeof(Ctl), st));
     Prof prof;
     prof.on = stats && (c.flags & 2);
     prof.st = st;
@@ -1068,6 +1065,17 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     // (the multi-GPU exchange payload); every level-0 read of it (tree sample,
     // fused count or k_gather) completes before the first handle is written
     const uint32_t* in32 = (c.flags & 512) ? reinterpret_cast<const uint32_t*>(d_handles) : nullptr;
+    unsigned long long fetches_total = 0, hints_total = 0;
+    uint32_t level = 0;
+    // a second attempt only after a failed root prefix skip (Ctl::skip_fail: the
+    // sample's common prefix did not hold for every string; level 0 wrote nothing)
+    for (int attempt = 0;; ++attempt) {
+    bool retry = false;
+    // level 0: cached keys at the common depth, root segment
+    int cur = 0;
+    for (int q = 0; q < NCLS; ++q) A.next[q] = reinterpret_cast<Seg*>(ws + L.lists[cur][q]);
+    S5_CUDA(cudaMemsetAsync(A.ctl, 0, sizeof(Ctl), st));
+    A.k2_depth = static_cast<uint32_t>(depth);
     if (!fuse_root) {
         prof.begin(S5_K_GATHER, n);
         k_gather<<<grid_for(n, 256), 256, 0, st>>>(d_handles, in32, static_cast<uint32_t>(n),
@@ -1079,9 +1087,8 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     prof.end();
     S5_CUDA(cudaGetLastError());
 
-    unsigned long long fetches_total = 0, hints_total = 0;
-    uint32_t level = 0;
-    for (;; ++level) {
+    fetches_total = hints_total = 0;
+    for (level = 0;; ++level) {
         prof.level = level;
         A.root = level == 0 && fuse_root && !in32 ? d_handles : nullptr;
         A.root32 = level == 0 && fuse_root ? in32 : nullptr;
@@ -1102,6 +1109,12 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         // second key words: gathered at the root, read at level 1 when the root
         // tree chose to carry them (ctl->k2)
         A.k2_stage = !fuse_root ? 0u : level == 0 ? 1u : (level == 1 && h.k2) ? 2u : 0u;
+        if (level == 1 && h.skip_fail) {  // redo the sort without the root prefix skip
+            if (attempt) return fail(S5_E_INTERNAL, "root prefix skip failed twice");
+            retry = true;
+            break;
+        }
+        if (level == 1) A.k2_depth = static_cast<uint32_t>(depth) + h.skip;  // the root's depth
         if (h.err & ERR_RANGE) return fail(S5_E_RANGE, "handle outside the arena");
         if (h.err & ERR_LIST) return fail(S5_E_INTERNAL, "segment list overflow");
         // plan_err is sticky and must be checked before the `!live` break: the
@@ -1180,12 +1193,19 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
                 uint64_t(m[WIDE]) * kWideCtasMax, n / A.wide_chunk + m[WIDE]));
             const int wsm = wide_smem(c.wide_dcap);
             prof.begin(S5_K_WIDE_COUNT, h.elems[WIDE]);
-            if (c.classifier)
+            // level 0 of a fused root: the tree kernel may have moved the segment
+            // behind the sample's common prefix (Ctl::skip) -- the SKIP instantiation
+            // checks every string against it, the other one returns at once
+            const bool may_skip = level == 0 && fuse_root && !(c.flags & 16384);
+            if (c.classifier) {
                 k_wide_count<true><<<ub, kWideThreads, wsm, st>>>(A, P);
-            else if (indexed && level == 0)  // fills the position table
+            } else if (indexed && level == 0) {  // fills the position table
                 k_wide_count<false, true><<<ub, kWideThreads, wsm, st>>>(A, P);
-            else
+                if (may_skip) k_wide_count<false, true, true><<<ub, kWideThreads, wsm, st>>>(A, P);
+            } else {
                 k_wide_count<false><<<ub, kWideThreads, wsm, st>>>(A, P);
+                if (may_skip) k_wide_count<false, false, true><<<ub, kWideThreads, wsm, st>>>(A, P);
+            }
             prof.end();
             dim3 cg(m[WIDE], ((2u << std::min(c.dmax, c.wide_dcap)) + 31) / 32);
             prof.begin(S5_K_WIDE_COLSCAN);
@@ -1272,6 +1292,10 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             S5_CUDA(cudaStreamWaitEvent(st, sd->join[i], 0));
         }
         S5_CUDA(cudaGetLastError());
+    }
+    if (!retry) break;
+    c.flags |= 16384;
+    A.flags = c.flags;
     }
     if (d_lcp && !(c.flags & 1)) {
         prof.begin(S5_K_LCP_FIX, hints_total);

@@ -40,6 +40,14 @@ struct Ctl {
     uint32_t w32;                 // root tree: high-entropy keys, 32-bit local sort words
     unsigned long long tree_words, hist_words;  // plan: pool use of the current level
     uint32_t plan_err;            // plan: ERR_POOL (sticky; the plan runs before the level's reset)
+    // Root prefix skip: the root sample's keys share `skip` leading bytes
+    // (value skip_prefix, no terminator among them), so level 0 classifies
+    // the 8 bytes after them -- "http://" costs URL-like data no level of its
+    // own.  The level-0 count checks every string against the prefix; one
+    // mismatch sets skip_fail, the level-0 scatter then writes nothing and
+    // the host restarts the sort without the skip.
+    uint32_t skip, skip_fail;
+    unsigned long long skip_prefix;
 };
 
 enum : uint32_t { ERR_RANGE = 1, ERR_LIST = 2, ERR_POOL = 4 };
@@ -1964,30 +1972,54 @@ __global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P) {
     const uint64_t* __restrict__ key = A.key[sd(s)] + s.begin;
     const uint64_t sseed = segment_seed(A.seed, s.begin, s.size, s.depth);
     __shared__ uint32_t bytemask[8][8];  // root: byte values seen per key position
-    if (threadIdx.x < 64) bytemask[threadIdx.x >> 3][threadIdx.x & 7] = 0;
-    __syncthreads();
-    for (uint32_t t = threadIdx.x; t < M; t += TT) {
-        uint64_t x = ~0ull;
-        if (t < m) {
-            const uint32_t idx = sample_index(sseed, t, s.size);
-            if (A.root || A.root32) {  // level 0: keys are not gathered yet
-                const int64_t h = root_handle(A, s.begin + idx);
-                x = (h >= 0 && static_cast<uint64_t>(h) + s.depth < A.arena_len)
-                        ? load_key(A.arena, static_cast<uint64_t>(h) + s.depth) : 0;
-            } else {
-                x = key[idx];
-            }
-            if (A.k2_stage == 1 && t < 256) {  // 256 random samples suffice for the estimate
+    // level 0 may sample twice: when the first sample's keys share 2..7 whole
+    // bytes, the segment moves that many bytes deeper (Ctl::skip) and the
+    // splitters come from a second sample of the keys behind the prefix
+    uint32_t skip = 0;
+#pragma unroll 1
+    for (uint32_t pass = 0;; ++pass) {
+        if (threadIdx.x < 64) bytemask[threadIdx.x >> 3][threadIdx.x & 7] = 0;
+        __syncthreads();
+        for (uint32_t t = threadIdx.x; t < M; t += TT) {
+            uint64_t x = ~0ull;
+            if (t < m) {
+                const uint32_t idx = sample_index(sseed, t, s.size);
+                if (A.root || A.root32) {  // level 0: keys are not gathered yet
+                    const int64_t h = root_handle(A, s.begin + idx);
+                    x = (h >= 0 && static_cast<uint64_t>(h) + s.depth + skip < A.arena_len)
+                            ? load_key(A.arena, static_cast<uint64_t>(h) + s.depth + skip) : 0;
+                } else {
+                    x = key[idx];
+                }
+                if (A.k2_stage == 1 && t < 256) {  // 256 random samples suffice for the estimate
 #pragma unroll
-                for (uint32_t j = 0; j < 8; ++j) {
-                    const uint32_t v = static_cast<uint32_t>(x >> (56 - 8 * j)) & 0xFFu;
-                    atomicOr(&bytemask[j][v >> 5], 1u << (v & 31));
+                    for (uint32_t j = 0; j < 8; ++j) {
+                        const uint32_t v = static_cast<uint32_t>(x >> (56 - 8 * j)) & 0xFFu;
+                        atomicOr(&bytemask[j][v >> 5], 1u << (v & 31));
+                    }
                 }
             }
+            sample[t] = x;
         }
-        sample[t] = x;
+        __syncthreads();
+        if (pass == 1 || A.k2_stage != 1 || !(A.root || A.root32) || (A.flags & 16384)) break;
+        sort_sample<TT>(sample, M);
+        const uint64_t lo_k = sample[0], hi_k = sample[m - 1];
+        uint32_t L = lo_k == hi_k ? 8u : diff_bytes(lo_k, hi_k);
+        const uint32_t z = zero_index(lo_k);
+        L = L < z ? L : z;
+        __syncthreads();  // every thread has read the extremes: the sample may be redrawn
+        if (L < 2 || L > 7) {
+            skip = 0xFFFFFFFFu;  // sorted already, no skip
+            break;
+        }
+        skip = L;
+        if (threadIdx.x == 0) {
+            A.ctl->skip = L;
+            A.ctl->skip_prefix = lo_k >> (64 - 8 * L);
+            const_cast<Seg*>(P.segs)[blockIdx.x].depth = s.depth + L;
+        }
     }
-    __syncthreads();
     if (A.k2_stage == 1 && threadIdx.x == 0) {
         // distinct 8-byte keys <= product of the distinct byte values per
         // position; far fewer than the strings -> level 1 is dominated by
@@ -2002,7 +2034,7 @@ __global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P) {
         A.ctl->k2 = (A.flags & 256) == 0 && static_cast<double>(s.size) > 16.0 * est &&
                     s.size / (g.v + 1) > A.local_max;
     }
-    sort_sample<TT>(sample, M);
+    if (skip != 0xFFFFFFFFu) sort_sample<TT>(sample, M);
     if (A.k2_stage == 1) {
         // the keys' entropy from the root sample: when nearly every sampled
         // key has its own leading 3-byte window, the one-CTA local tiers sort
@@ -2045,11 +2077,16 @@ __device__ __forceinline__ uint32_t find_seg(const uint32_t* cta_start, uint32_t
 // again.
 // Level 0 of k_wide_count with second key words: handle -> (offset, key,
 // next word) gather fused with the classification and the histogram.
-template <bool K2, bool IDX = false>
+// SKIP: the segment sits Ctl::skip bytes behind the sort depth (root prefix
+// skip); every string's skipped bytes are checked against the prefix.
+template <bool K2, bool IDX = false, bool SKIP = false>
 __device__ __forceinline__ void root_gather_count(const SortArgs& A, const Seg& s, uint32_t lo,
                                                   uint32_t hi, const LutTree& T, uint32_t* hist,
                                                   uint16_t* __restrict__ bkt) {
     constexpr int R = 4;  // (8 would lift the whole count kernel's register budget)
+    const uint32_t skip = SKIP ? A.ctl->skip : 0u;
+    const uint64_t prefix = SKIP ? A.ctl->skip_prefix : 0ull;
+    bool mismatch = false;
 #pragma unroll 1
     for (uint32_t base = lo; base < hi; base += R * kWideThreads) {
         int64_t hh[R];
@@ -2062,12 +2099,15 @@ __device__ __forceinline__ void root_gather_count(const SortArgs& A, const Seg& 
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             const uint32_t i = base + j * kWideThreads + threadIdx.x;
-            if (i < hi && (hh[j] < 0 || static_cast<uint64_t>(hh[j]) + s.depth >= A.arena_len)) {
+            if (i < hi && (hh[j] < 0 || static_cast<uint64_t>(hh[j]) + s.depth - skip >= A.arena_len)) {
                 atomicOr(&A.ctl->err, ERR_RANGE);
                 hh[j] = 0;
             }
             kk[j] = k2w[j] = 0;
             if (i < hi) {
+                if (SKIP)  // a terminator inside the skipped bytes fails the check too
+                    mismatch |= (load_key(A.arena, static_cast<uint64_t>(hh[j]) + s.depth - skip) >>
+                                 (64 - 8 * skip)) != prefix;
                 if (K2) load_key2(A.arena, static_cast<uint64_t>(hh[j]) + s.depth, kk[j], k2w[j]);
                 else kk[j] = load_key(A.arena, static_cast<uint64_t>(hh[j]) + s.depth);
             }
@@ -2090,15 +2130,20 @@ __device__ __forceinline__ void root_gather_count(const SortArgs& A, const Seg& 
             }
         }
     }
+    if (SKIP && mismatch) atomicOr(&A.ctl->skip_fail, 1u);
 }
 
-// IDX: the level-0 launch of index mode (its own instantiation: the position
-// table stores would cost the common kernel registers and a CTA per SM)
-template <bool EQUAL, bool IDX = false>
+// IDX: the level-0 launch of index mode; SKIP: the level-0 launch behind a
+// root prefix skip.  Their own instantiations: the position table stores and
+// the prefix check would cost the common kernel registers and a CTA per SM.
+// The tree kernel decides the skip on the device right before, so level 0
+// launches both the plain and the SKIP kernel and the wrong one returns.
+template <bool EQUAL, bool IDX = false, bool SKIP = false>
 __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePlan P) {
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;
+    if (A.k2_stage == 1 && (A.ctl->skip != 0) != SKIP) return;
     uint64_t* tree = reinterpret_cast<uint64_t*>(sm);
     uint32_t* hist = reinterpret_cast<uint32_t*>(sm + (1u << A.wide_dcap) * 8);
     uint64_t* splitters = reinterpret_cast<uint64_t*>(hist + (2u << A.wide_dcap) + 2);
@@ -2129,9 +2174,9 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_count(SortArgs A, WidePla
         T.pf = tsrc[2 * g.v + 1 + kLutTabWords];
         T.lb = static_cast<uint32_t>(tsrc[2 * g.v + 1 + kLutTabWords + 1]);
         if (A.root || A.root32) {  // level 0: handle -> (offset, key) gather fused with the count
-            if (IDX) {  // index mode (arenas >= 4 GiB)
-                if (A.k2_stage == 1 && A.ctl->k2) root_gather_count<true, true>(A, s, lo, hi, T, hist, bkt);
-                else root_gather_count<false, true>(A, s, lo, hi, T, hist, bkt);
+            if (IDX || SKIP) {  // index mode (arenas >= 4 GiB) / root prefix skip
+                if (A.k2_stage == 1 && A.ctl->k2) root_gather_count<true, IDX, SKIP>(A, s, lo, hi, T, hist, bkt);
+                else root_gather_count<false, IDX, SKIP>(A, s, lo, hi, T, hist, bkt);
             } else if (A.k2_stage == 1 && A.ctl->k2) {
                 root_gather_count<true>(A, s, lo, hi, T, hist, bkt);
             } else {
@@ -2388,6 +2433,7 @@ __global__ void __launch_bounds__(kWideThreads) k_wide_scatter(SortArgs A, WideP
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;
+    if (A.k2_stage == 1 && A.ctl->skip_fail) return;  // level 0 is redone without the prefix skip
     uint64_t* sk = reinterpret_cast<uint64_t*>(sm);
     uint32_t* so = reinterpret_cast<uint32_t*>(sk + kWideTile);
     uint16_t* sb = reinterpret_cast<uint16_t*>(so + kWideTile);
@@ -2515,6 +2561,7 @@ __global__ void __launch_bounds__(THREADS) k_wide_scatter_tma(SortArgs A, WidePl
     extern __shared__ __align__(16) uint8_t sm[];
     const uint32_t G = blockIdx.x;
     if (G >= A.ctl->wide_ctas) return;
+    if (A.k2_stage == 1 && A.ctl->skip_fail) return;  // level 0 is redone without the prefix skip
     TmaStage* stage = reinterpret_cast<TmaStage*>(sm);
     uint16_t* perm = reinterpret_cast<uint16_t*>(sm + NS * sizeof(TmaStage));
     const uint32_t kc = 2u << A.wide_dcap;

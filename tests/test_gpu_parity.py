@@ -616,3 +616,54 @@ def test_arena_beyond_4gib():
     from paper_1305_1157_b200 import samplesort as SS
     arena.drop_device()
     SS.release_workspace()
+
+
+# ---------------------------------------------------------------------------
+# root prefix skip (cfg flags bit14 turns it off): the root sample's common
+# prefix is checked against every string; one mismatch redoes the sort
+
+NO_SKIP = 16384
+
+
+def _prefixed(prefix: bytes, n: int, seed: int, extra=()):
+    from paper_1305_1157_b200 import arena_from_strings
+    rng = np.random.default_rng(seed)
+    body = rng.integers(97, 123, size=(n, 20), dtype=np.uint8)
+    lens = rng.integers(0, 21, n)
+    strs = [prefix + body[i, :lens[i]].tobytes() for i in range(n)]
+    strs.extend(extra)
+    order = rng.permutation(len(strs))
+    return arena_from_strings([strs[i] for i in order])
+
+
+@pytest.mark.parametrize("prefix", [b"ab", b"http://", b"/var/log/app/", b"\xff\xfe\xfd"])
+def test_root_prefix_skip_matches_oracle(prefix):
+    arena, h0 = _prefixed(prefix, 200_000, 5)
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, 8)
+    want_lcp = O.adjacent_lcps(arena, want)
+    c_skip, c_plain = Counters(), Counters()
+    h = h0.copy()
+    lcp = np.empty(h.size - 1, np.int64)
+    parallel_sample_sort(arena, h, cfg=SampleSortConfig(), counters=c_skip, lcp_out=lcp)
+    _check_sorted(arena, h0, h, want, lcp, want_lcp, f"skip/{prefix!r}")
+    h = h0.copy()
+    parallel_sample_sort(arena, h, cfg=SampleSortConfig(flags=NO_SKIP), counters=c_plain, lcp_out=lcp)
+    _check_sorted(arena, h0, h, want, lcp, want_lcp, f"noskip/{prefix!r}")
+    # the skip never costs a level; behind a 7-byte prefix it saves one
+    assert c_skip.get("parallel_steps") <= c_plain.get("parallel_steps")
+    if prefix == b"http://":
+        assert c_skip.get("parallel_steps") < c_plain.get("parallel_steps")
+
+
+@pytest.mark.parametrize("odd", [[b"ftp://other"], [b"http:/"], [b""], [b"http://"],
+                                 [b"http:/\x01zzz", b"h", b"i" * 40]])
+def test_root_prefix_skip_falls_back_on_a_mismatch(odd):
+    # the sample (a few thousand of 300 001+ strings) sees only "http://..."
+    arena, h0 = _prefixed(b"http://", 300_000, 9, extra=odd)
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, 8)
+    for cfg in (SampleSortConfig(), SampleSortConfig(flags=INDEXED, seed=2)):
+        h = h0.copy()
+        _, lcp = sort_with_lcp(arena, h, cfg=cfg)
+        _check_sorted(arena, h0, h, want, lcp, O.adjacent_lcps(arena, want), f"fallback/{odd!r}")
