@@ -16,7 +16,7 @@ for C in $CFGS; do
   echo "cfg $C rc=$?"
   python profiles/ncu_summary.py $REP/full_cfg$C.ncu-rep --json gpurun_out/${TAG}_ncu_cfg$C.json \
       > gpurun_out/${TAG}_ncu_cfg$C.txt 2>&1
-  for K in "k_local_w" "k_local.*)64," "k_local.*)128," "k_local.*)256," "k_local.*)512," \
+  for K in "k_local_w" "k_local.*int.64," "k_local.*int.128," "k_local.*int.256," "k_local.*int.512," \
            "k_wide_scatter" "k_wide_count" "k_narrow"; do
     echo "== $K" >> gpurun_out/${TAG}_stalls_cfg$C.txt
     timeout 300 python profiles/stall_by_line.py $REP/full_cfg$C.ncu-rep "$K" 0 \
