@@ -667,3 +667,20 @@ def test_root_prefix_skip_falls_back_on_a_mismatch(odd):
         h = h0.copy()
         _, lcp = sort_with_lcp(arena, h, cfg=cfg)
         _check_sorted(arena, h0, h, want, lcp, O.adjacent_lcps(arena, want), f"fallback/{odd!r}")
+
+
+def test_root_prefix_skip_behind_a_caller_depth():
+    # sample_sort(depth=6): every string starts with "prefix", and the bytes
+    # behind it share "http://" -- the skip applies on top of the caller's depth
+    from paper_1305_1157_b200 import arena_from_strings
+    rng = np.random.default_rng(31)
+    strs = [b"prefixhttp://" + bytes(rng.integers(97, 101, rng.integers(0, 14)).tolist())
+            for _ in range(60_000)]
+    arena, h = arena_from_strings(strs)
+    want = h.copy()
+    O.parallel_sample_sort(arena, want, 8)
+    for flags in (0, NO_SKIP, INDEXED):
+        got = h.copy()
+        lcp = np.empty(h.size - 1, np.int64)
+        sample_sort(arena, got, depth=6, cfg=SampleSortConfig(flags=flags), lcp_out=lcp)
+        _check_sorted(arena, h, got, want, lcp, O.adjacent_lcps(arena, want), f"depth6/{flags}")
