@@ -239,11 +239,24 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
     n_local = h.numel()
 
     t = time.perf_counter()
+    if G == 1:
+        # one rank: no splitters, no count matrix, no boundary -- the shard is
+        # the slice; the same u32 payload and in-place local sort as below
+        recv = torch.empty(n_local, dtype=torch.int64, device=dev)
+        recv.view(torch.int32)[:n_local].copy_(h)  # u32 offsets (bit pattern kept)
+        t = _mark("exchange", t)
+        recv, lcp = be.sort_u32(recv, n_local)
+        _mark("local_sort", t)
+        return ShardResult(recv, lcp, 0, [n_local])
     # 1. samples (with replacement, seeded per rank) -> all_gather
     s = oversample * G
-    if n_local:  # drawn on the device: no host round trip
-        gen = torch.Generator(device=dev).manual_seed(seed * 1_000_003 + rank)
-        samp = h[torch.randint(0, n_local, (s,), generator=gen, device=dev)]
+    if n_local:  # drawn on the device (a multiplicative hash of the slot: no
+        # generator object, no host round trip)
+        slot = torch.arange(s, dtype=torch.int64, device=dev)
+        salt = ((seed * 1_000_003 + rank) * 0x2545F4914F6CDD1D) & 0x3FFFFFFFFFFFFFFF
+        pick = (slot + 1) * 0x9E3779B97F4A7C1 + salt  # wraps in int64
+        pick = (pick ^ (pick >> 29)) * 0x3F58476D1CE4E5B9  # one splitmix round
+        samp = h[((pick ^ (pick >> 32)) & 0x7FFFFFFFFFFFFFFF).remainder(n_local)]
     else:
         samp = torch.full((s,), -1, dtype=torch.int64, device=dev)
     allsamp = torch.empty(G * s, dtype=torch.int64, device=dev)
@@ -259,10 +272,7 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
     t = _mark("splitters", t)
 
     # 3. destination of every local string, handles grouped by destination
-    if G == 1:
-        send, counts = h, [n_local]
-    else:
-        send, counts = be.partition(h, splitters)
+    send, counts = be.partition(h, splitters)
     t = _mark("partition", t)
 
     # 4. the G x G count matrix on every rank (row = source, column =
@@ -277,11 +287,8 @@ def distributed_sample_sort(arena, local_handles, group=None, oversample: int = 
     recv = torch.empty(n_recv, dtype=torch.int64, device=dev)
     recv32 = recv.view(torch.int32)[:n_recv]  # the first 4 n_recv bytes
     send32 = send.to(torch.int32)  # u32 offsets (bit pattern kept)
-    if G == 1:
-        recv32.copy_(send32)
-    else:
-        dist.all_to_all_single(recv32, send32, output_split_sizes=recv_sizes,
-                               input_split_sizes=[int(c) for c in counts], group=group)
+    dist.all_to_all_single(recv32, send32, output_split_sizes=recv_sizes,
+                           input_split_sizes=[int(c) for c in counts], group=group)
     t = _mark("exchange", t)
 
     # 5. local sort of the received u32 offsets (in place) + LCP
