@@ -1722,6 +1722,7 @@ k_narrow(SortArgs A, const Seg* __restrict__ segs) {
         block_minmax<T>(mn, mx, red);
         if (mn != mx) break;  // no: an ordinary step (one dominant equality bucket)
         s.depth += 8;
+        s.side &= 1u;  // carried second key words belong to the old depth: not valid any more
         for (uint32_t i = threadIdx.x; i < s.size; i += T) {
             key[i] = load_key(A.arena, apos(A, off[i]) + s.depth);
             ++fetches;

@@ -1,0 +1,97 @@
+"""Seeded differential fuzz of the GPU sort against the CPU oracle: random
+alphabets, length laws, shared prefixes, duplicates and tier configurations
+(each case: sorted string sequence, LCP array, permutation -- exact)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_1305_1157_b200 import SampleSortConfig, arena_from_strings, sort_with_lcp
+
+pytestmark = pytest.mark.gpu
+
+
+def _strings(rng):
+    n = int(rng.choice([2, 3, 33, 257, 1000, 4097, 20_000, 70_000]))
+    sigma = int(rng.choice([1, 2, 4, 26, 94, 255]))
+    lo = int(rng.choice([0, 0, 1, 7]))
+    hi = lo + int(rng.choice([0, 1, 8, 9, 24, 70]))
+    base = int(rng.integers(1, 256 - sigma + 1)) if sigma < 255 else 1
+    prefix = bytes(rng.integers(1, 256, int(rng.choice([0, 0, 2, 7, 8, 9, 40]))).tolist())
+    pool = None
+    if rng.random() < 0.4:  # many duplicates: draw from a small pool
+        pool = int(rng.choice([1, 3, 50, 2000]))
+    def one():
+        m = int(rng.integers(lo, hi + 1))
+        return prefix + bytes((rng.integers(0, sigma, m) + base).tolist())
+    if pool is not None:
+        bank = [one() for _ in range(pool)]
+        strs = [bank[int(i)] for i in rng.integers(0, pool, n)]
+    else:
+        strs = [one() for _ in range(n)]
+    if rng.random() < 0.3:  # a few strings off the common prefix
+        for i in rng.integers(0, n, 3):
+            strs[int(i)] = bytes(rng.integers(1, 256, int(rng.integers(0, 6))).tolist())
+    return strs
+
+
+def _config(rng):
+    flags = 0
+    for bit, p in ((8, .2), (16, .1), (32, .2), (64, .1), (128, .2), (256, .2), (2048, .2),
+                   (8192, .25), (16384, .2)):
+        if rng.random() < p:
+            flags |= bit
+    small = int(rng.choice([1, 8, 32]))
+    local = int(rng.choice([32, 256, 1024, 4096]))
+    narrow = int(rng.choice([local, 4096, 16384])) if local <= 4096 else local
+    return SampleSortConfig(v=int(rng.choice([15, 63, 255, 1023, 8191])),
+                            alpha=int(rng.choice([1, 2, 4, 8])),
+                            classifier=str(rng.choice(["unroll", "equal"])),
+                            small_max=small, local_max=max(local, small),
+                            narrow_max=max(narrow, local, small), flags=flags,
+                            seed=int(rng.integers(1, 1 << 30)))
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("S5_FUZZ_CASES", "200"))))
+def test_fuzz_against_oracle(seed):
+    rng = np.random.default_rng(1000 + seed)
+    strs = _strings(rng)
+    cfg = _config(rng)
+    arena, h0 = arena_from_strings(strs)
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, 4)
+    got = h0.copy()
+    _, lcp = sort_with_lcp(arena, got, cfg=cfg)
+    tag = f"seed {seed} n={len(strs)} cfg={cfg}"
+    assert np.array_equal(np.sort(got), np.sort(h0)), tag
+    assert O.contents_equal(arena, got, want), tag
+    assert np.array_equal(lcp, O.adjacent_lcps(arena, want)), tag
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("S5_FUZZ_BIG_CASES", "12"))))
+def test_fuzz_large_against_oracle(seed):
+    """Several wide levels, carried second key words, prefix skip, deep
+    equality chains: 200 K - 600 K strings over tiny alphabets."""
+    rng = np.random.default_rng(5000 + seed)
+    n = int(rng.choice([200_000, 600_000]))
+    sigma = int(rng.choice([1, 2, 3, 4, 20]))
+    lmax = int(rng.choice([6, 12, 30, 60]))
+    prefix = bytes(rng.integers(1, 256, int(rng.choice([0, 3, 7, 16]))).tolist())
+    body = (rng.integers(0, sigma, size=(n, lmax)) + 65).astype(np.uint8)
+    lens = rng.integers(0, lmax + 1, n)
+    if rng.random() < 0.5:  # long runs of equal leading characters
+        body[:, : lmax // 2] = 65
+    strs = [prefix + body[i, :lens[i]].tobytes() for i in range(n)]
+    cfg = _config(rng)
+    cfg.local_max = max(cfg.local_max, 256)  # keep the level count bounded
+    cfg.narrow_max = max(cfg.narrow_max, cfg.local_max)
+    arena, h0 = arena_from_strings(strs)
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, O.max_threads())
+    got = h0.copy()
+    _, lcp = sort_with_lcp(arena, got, cfg=cfg)
+    tag = f"seed {seed} n={n} sigma={sigma} lmax={lmax} cfg={cfg}"
+    assert np.array_equal(np.sort(got), np.sort(h0)), tag
+    assert O.contents_equal(arena, got, want), tag
+    assert np.array_equal(lcp, O.adjacent_lcps(arena, want)), tag
