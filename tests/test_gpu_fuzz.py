@@ -74,7 +74,7 @@ def test_fuzz_large_against_oracle(seed):
     """Several wide levels, carried second key words, prefix skip, deep
     equality chains: 200 K - 600 K strings over tiny alphabets."""
     rng = np.random.default_rng(5000 + seed)
-    n = int(rng.choice([200_000, 600_000]))
+    n = int(rng.choice([200_000, 600_000])) * int(os.environ.get("S5_FUZZ_BIG_SCALE", "1"))
     sigma = int(rng.choice([1, 2, 3, 4, 20]))
     lmax = int(rng.choice([6, 12, 30, 60]))
     prefix = bytes(rng.integers(1, 256, int(rng.choice([0, 3, 7, 16]))).tolist())
@@ -95,3 +95,40 @@ def test_fuzz_large_against_oracle(seed):
     assert np.array_equal(np.sort(got), np.sort(h0)), tag
     assert O.contents_equal(arena, got, want), tag
     assert np.array_equal(lcp, O.adjacent_lcps(arena, want)), tag
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("S5_FUZZ_MULTI_CASES", "40"))))
+def test_fuzz_entry_points_against_oracle(seed):
+    """The other doors into the same sort: device-resident handles, a caller
+    depth behind a shared prefix, and workers = G shards on a repeated device
+    list (partition kernel, exchange and boundary LCPs on one GPU)."""
+    import torch
+    from paper_1305_1157_b200 import parallel_sample_sort, sample_sort
+    rng = np.random.default_rng(9000 + seed)
+    strs = _strings(rng)
+    cfg = _config(rng)
+    arena, h0 = arena_from_strings(strs)
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, 4)
+    want_lcp = O.adjacent_lcps(arena, want)
+    mode = seed % 3
+    tag = f"seed {seed} mode {mode} n={len(strs)} cfg={cfg}"
+    if mode == 0:    # CUDA tensors in and out
+        d = torch.from_numpy(h0.copy()).cuda()
+        dl = torch.empty(d.numel() - 1, dtype=torch.int64, device="cuda")
+        parallel_sample_sort(arena, d, cfg=cfg, lcp_out=dl)
+        got, lcp = d.cpu().numpy(), dl.cpu().numpy()
+    elif mode == 1:  # sample_sort from the depth every string shares
+        depth = int(O.adjacent_lcps(arena, want).min()) if h0.size > 1 else 0
+        depth = int(rng.integers(0, depth + 1))
+        got = h0.copy()
+        lcp = np.empty(h0.size - 1, np.int64)
+        sample_sort(arena, got, depth=depth, cfg=cfg, lcp_out=lcp)
+    else:            # workers = G over one device
+        G = int(rng.choice([2, 3, 5]))
+        got = h0.copy()
+        lcp = np.empty(h0.size - 1, np.int64)
+        parallel_sample_sort(arena, got, workers=G, cfg=cfg, lcp_out=lcp, devices=[0] * G)
+    assert np.array_equal(np.sort(got), np.sort(h0)), tag
+    assert O.contents_equal(arena, got, want), tag
+    assert np.array_equal(lcp, want_lcp), tag
