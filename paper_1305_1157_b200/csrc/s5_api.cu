@@ -1132,7 +1132,10 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             live_elems += h.elems[q];
         }
         if (!live) break;
-        if (level >= 100000) return fail(S5_E_INTERNAL, "no progress");
+        // every level splits a segment or moves one 8 bytes deeper (a wide
+        // segment of strings sharing P more bytes takes P / 8 levels), so the
+        // level count is bounded by the splits plus the deepest advance
+        if (level >= n + arena_len / 8 + 1024) return fail(S5_E_INTERNAL, "no progress");
         if (audit && level > 0) {
             // debug replay of the reference's audit hook (samplesort.py:235-236, :431-432):
             // the children emitted by the previous level, with both sides' offsets

@@ -180,8 +180,8 @@ __device__ __forceinline__ int size_class(const SortArgs& A, uint32_t size) {
 }
 
 __device__ __forceinline__ void emit_child(const SortArgs& A, uint32_t begin, uint32_t size,
-                                           uint32_t depth, uint32_t side) {
-    int cls = size_class(A, size);
+                                           uint32_t depth, uint32_t side, int cls = -1) {
+    if (cls < 0) cls = size_class(A, size);
     uint32_t idx = atomicAdd(&A.ctl->n_list[cls], 1u);
     if (idx < A.cap[cls]) {
         A.next[cls][idx] = Seg{begin, size, depth, side};
@@ -2381,8 +2381,17 @@ __global__ void __launch_bounds__(256) k_wide_bscan(SortArgs A, WidePlan P) {
     __syncthreads();
     if (threadIdx.x == 0) starts[g.k + 1] = solo;
     if (solo) {
-        if (threadIdx.x == 0)
-            emit_child(A, s.begin, s.size, s.depth + 8, sd(s) | (k2_kind(A, s) == K2_MAKE ? 2u : 0u));
+        // Seg.side bits 8..15 count the levels a segment has stayed whole.  A
+        // shared prefix of P bytes costs a wide segment P / 8 levels; from the
+        // fourth on, a segment the one-CTA step can hold goes to k_narrow, whose
+        // in-place prefix skip walks the rest of the prefix inside one kernel
+        if (threadIdx.x == 0) {
+            const uint32_t streak = min(255u, ((s.side >> 8) & 0xFFu) + 1u);
+            const bool walk = streak >= 4 && s.size <= kNarrowMaxSize && s.size > A.local_max;
+            emit_child(A, s.begin, s.size, s.depth + 8,
+                       sd(s) | (k2_kind(A, s) == K2_MAKE ? 2u : 0u) | (streak << 8),
+                       walk ? static_cast<int>(NARROW) : -1);
+        }
         return;
     }
     __shared__ EmitScratch es;

@@ -684,3 +684,31 @@ def test_root_prefix_skip_behind_a_caller_depth():
         lcp = np.empty(h.size - 1, np.int64)
         sample_sort(arena, got, depth=6, cfg=SampleSortConfig(flags=flags), lcp_out=lcp)
         _check_sorted(arena, h, got, want, lcp, O.adjacent_lcps(arena, want), f"depth6/{flags}")
+
+
+def test_long_shared_prefix_in_a_wide_segment():
+    # 6000 strings (above the one-CTA limit) sharing 40 KB: a wide segment
+    # moves 8 bytes per level, so after four whole-segment levels it goes to
+    # the one-CTA step, whose in-place skip walks the prefix in one kernel
+    from paper_1305_1157_b200 import arena_from_strings
+    rng = np.random.default_rng(77)
+    base = bytes(rng.integers(1, 256, 40_000).tolist())
+    strs = [base + bytes(rng.integers(97, 100, rng.integers(0, 5)).tolist()) for _ in range(6000)]
+    arena, h = arena_from_strings(strs)
+    want = h.copy()
+    O.parallel_sample_sort(arena, want, 8)
+    ctr = Counters()
+    got = h.copy()
+    lcp = np.empty(h.size - 1, np.int64)
+    parallel_sample_sort(arena, got, counters=ctr, lcp_out=lcp)
+    _check_sorted(arena, h, got, want, lcp, O.adjacent_lcps(arena, want), "prefix40k")
+    assert ctr.get("parallel_steps") < 64
+    # the same through the wide tier only (narrow step off by size): every level counts
+    big = [base[:4000] + bytes(rng.integers(97, 100, rng.integers(0, 5)).tolist()) for _ in range(6000)]
+    arena, h = arena_from_strings(big)
+    want = h.copy()
+    O.parallel_sample_sort(arena, want, 8)
+    got = h.copy()
+    parallel_sample_sort(arena, got, cfg=SampleSortConfig(local_max=8192), counters=(c2 := Counters()),
+                         lcp_out=lcp)
+    _check_sorted(arena, h, got, want, lcp, O.adjacent_lcps(arena, want), "prefix4k")
