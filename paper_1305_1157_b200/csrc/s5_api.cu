@@ -61,6 +61,7 @@ struct Cfg {
 #define S5_ROOT_STAGES 3
 #endif
 constexpr uint32_t kRootStages = S5_ROOT_STAGES;  // bulk-copy stages of the root scatter
+constexpr uint32_t kTreeAhead = 1024;  // tree CTAs launched ahead of the level's host read
 constexpr uint32_t kLocalThreads = 512;   // segments of <= 4096 strings
 using LocalCfg = LocalSmem<kLocalThreads>;
 constexpr uint32_t kLocalXSThreads = 64;  // <= 512
@@ -1088,6 +1089,7 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     S5_CUDA(cudaGetLastError());
 
     fetches_total = hints_total = 0;
+    bool wide_before = true;  // the previous level ran S^5 steps (wide or narrow segments)
     for (level = 0;; ++level) {
         prof.level = level;
         A.root = level == 0 && fuse_root && !in32 ? d_handles : nullptr;
@@ -1101,6 +1103,20 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
         P.nsegs = 0;
         prof.begin(S5_K_WIDE_PLAN);
         k_wide_plan<<<1, 1024, 0, st>>>(A, P);
+        prof.end();
+        // ... and so do the splitter trees: enqueued behind the plan, they are
+        // built while the host wakes up, reads the block and launches the rest
+        // of the level (the segment count comes from the control block; grid
+        // = an upper bound, surplus CTAs return)
+        A.k2_stage = fuse_root && level == 0 ? 1u : 0u;
+        // (only S^5 steps emit wide children: none can exist behind a level without one)
+        const uint32_t tree_ub = level == 0 ? 1u : !wide_before ? 0u
+                                                 : std::min<uint32_t>(L.cap[WIDE], kTreeAhead);
+        prof.begin(S5_K_WIDE_TREE);
+        if (level == 0)  // one segment: its CTA's sample sort is the level's critical path
+            k_wide_tree<kTreeThreadsFew><<<1, kTreeThreadsFew, wide_tree_smem(c), st>>>(A, P, 0, 0);
+        else if (tree_ub)
+            k_wide_tree<kTreeThreads><<<tree_ub, kTreeThreads, wide_tree_smem(c), st>>>(A, P, 0, 0);
         prof.end();
         S5_CUDA(cudaGetLastError());
         if (int e = wait_published(hp, tag, st)) return e;
@@ -1182,15 +1198,16 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
             return sd->s[i];
         };
 
+        wide_before = m[WIDE] + m[NARROW] > 0;
         if (m[WIDE]) {
             P.segs = segs[WIDE];
             P.nsegs = m[WIDE];
-            prof.begin(S5_K_WIDE_TREE);
-            if (m[WIDE] <= 8)  // few segments: one CTA's sample sort is the level's critical path
-                k_wide_tree<kTreeThreadsFew><<<m[WIDE], kTreeThreadsFew, wide_tree_smem(c), st>>>(A, P);
-            else
-                k_wide_tree<kTreeThreads><<<m[WIDE], kTreeThreads, wide_tree_smem(c), st>>>(A, P);
-            prof.end();
+            if (m[WIDE] > tree_ub) {  // the trees beyond the launch made ahead of the host read
+                prof.begin(S5_K_WIDE_TREE);
+                k_wide_tree<kTreeThreads><<<m[WIDE] - tree_ub, kTreeThreads, wide_tree_smem(c), st>>>(
+                    A, P, tree_ub, m[WIDE]);
+                prof.end();
+            }
             // upper bound on CTAs; surplus CTAs exit on ctl->wide_ctas
             uint32_t ub = static_cast<uint32_t>(std::min<uint64_t>(
                 uint64_t(m[WIDE]) * kWideCtasMax, n / A.wide_chunk + m[WIDE]));

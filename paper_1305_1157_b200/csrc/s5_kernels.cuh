@@ -1955,16 +1955,25 @@ constexpr uint32_t kTreeThreads = S5_TREE_THREADS;  // one CTA per wide segment
 // the critical path of the level
 constexpr uint32_t kTreeThreadsFew = 1024;
 
+// The level driver enqueues this kernel right behind the plan, before the
+// host has read the level's control block (the trees are built while the
+// host wakes up and launches the rest of the level): `nsegs` = 0 then, and the
+// segment count comes from the control block (not yet reset for the level);
+// a level with more wide segments than that launch's grid gets a second
+// launch (seg_base, nsegs from the host) for the rest.
 template <uint32_t TT>
-__global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P) {
+__global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P, uint32_t seg_base,
+                                                 uint32_t nsegs) {
     extern __shared__ __align__(16) uint8_t sm[];
     if (A.ctl->wide_ctas == 0) return;
+    const uint32_t si = seg_base + blockIdx.x;
+    if (si >= (nsegs ? nsegs : A.ctl->n_list[WIDE])) return;
     const uint32_t dw = A.dmax < A.wide_dcap ? A.dmax : A.wide_dcap;
     uint64_t* sample = reinterpret_cast<uint64_t*>(sm);
     int32_t* na = reinterpret_cast<int32_t*>(sm + A.wide_sample * 8);
     int32_t* nb = na + (1u << dw);
     uint32_t* nf = reinterpret_cast<uint32_t*>(nb + (1u << dw));
-    const Seg s = P.segs[blockIdx.x];
+    const Seg s = P.segs[si];
     const WideGeom g = wide_geom(s, A);
     uint32_t m = A.alpha * g.v;
     if (m > kWideSampleCap) m = kWideSampleCap;
@@ -2018,7 +2027,7 @@ __global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P) {
         if (threadIdx.x == 0) {
             A.ctl->skip = L;
             A.ctl->skip_prefix = lo_k >> (64 - 8 * L);
-            const_cast<Seg*>(P.segs)[blockIdx.x].depth = s.depth + L;
+            const_cast<Seg*>(P.segs)[si].depth = s.depth + L;
         }
     }
     if (A.k2_stage == 1 && threadIdx.x == 0) {
@@ -2052,7 +2061,7 @@ __global__ void __launch_bounds__(TT) k_wide_tree(SortArgs A, WidePlan P) {
         __syncthreads();
         if (threadIdx.x == 0) A.ctl->w32 = (A.flags & 2048) == 0 && m >= 256 && s_same * 64 <= m;
     }
-    uint64_t* tree = P.tree_pool + P.tree_off[blockIdx.x];
+    uint64_t* tree = P.tree_pool + P.tree_off[si];
     build_tree_levels<TT>(sample, m, g.d, tree, na, nb, nf);
     // classification table for k_wide_count, once per segment
     uint64_t* spl = tree + g.v + 1;
