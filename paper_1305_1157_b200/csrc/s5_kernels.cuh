@@ -1420,9 +1420,14 @@ k_local(SortArgs A, const Seg* __restrict__ segs) {
 // Warp tier: one warp finishes a segment of <= 256 strings (8 per lane) with
 // the local tier's algorithm at warp scope -- the sort words are merged in
 // registers (sort8_regs + warp_merge256), so there are no shared-memory sort
-// rounds and no block barriers; 8 segments per CTA.
+// rounds and no block barriers; 4 segments per CTA (a CTA lives as long as
+// its slowest warp: with 8 the achieved occupancy of URL-like levels was 25 %;
+// 4 and 2 measure the same, k_local_w -11 % on config 3, -7 % on 2 and 5).
 constexpr uint32_t kWarpLocalMax = 256;
-constexpr uint32_t kWarpLocalWarps = 8;
+#ifndef S5_WARP_LOCAL_WARPS
+#define S5_WARP_LOCAL_WARPS 4
+#endif
+constexpr uint32_t kWarpLocalWarps = S5_WARP_LOCAL_WARPS;
 
 struct WarpLocalSmem {
     uint64_t key1[kWarpLocalMax];
