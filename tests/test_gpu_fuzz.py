@@ -132,3 +132,60 @@ def test_fuzz_entry_points_against_oracle(seed):
     assert np.array_equal(np.sort(got), np.sort(h0)), tag
     assert O.contents_equal(arena, got, want), tag
     assert np.array_equal(lcp, want_lcp), tag
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("S5_FUZZ_AUX_CASES", "30"))))
+def test_fuzz_auxiliary_surfaces(seed):
+    """Line ingest, string lengths, materialisation, key packing, LCP and
+    verification kernels on random inputs against numpy / Python."""
+    from paper_1305_1157_b200 import (StringArena, adjacent_lcps, first_unsorted, ingest_lines,
+                                      materialize, pack_keys, string_lengths,
+                                      verify_sorted_permutation)
+    rng = np.random.default_rng(20_000 + seed)
+    n = int(rng.choice([1, 2, 31, 1000, 40_000]))
+    lmax = int(rng.choice([0, 1, 7, 8, 9, 63, 300]))
+    sigma = int(rng.choice([1, 3, 90]))
+    lines = [bytes((rng.integers(0, sigma, int(rng.integers(0, lmax + 1))) + 33).tolist())
+             for _ in range(n)]
+    tail = [b"", b"\n", b"x", b"\n\n"][int(rng.integers(0, 4))]
+    raw = b"\n".join(lines) + tail
+    # ingest == harness.load_lines (newline -> terminator, one appended if missing)
+    data = np.frombuffer(raw, np.uint8).copy()
+    if data.size:
+        data[data == 10] = 0
+        if data[-1] != 0:
+            data = np.append(data, np.uint8(0))
+    ends = np.nonzero(data == 0)[0]
+    want_h = np.zeros(ends.size, np.int64)
+    want_h[1:] = ends[:-1] + 1
+    arena, h = ingest_lines(raw)
+    h = h.cpu().numpy()
+    assert np.array_equal(arena.data, data) and np.array_equal(h, want_h)
+    if h.size == 0:
+        return
+    strs = [data[a:e].tobytes() for a, e in zip(want_h, ends)]
+    assert np.array_equal(np.asarray(string_lengths(arena, h)), np.array([len(s) for s in strs]))
+    depth = int(rng.integers(0, 12))
+    ok = (want_h + depth) < data.size
+    keys = np.asarray(pack_keys(arena, h[ok], depth))
+    ref = StringArena(data)
+    assert np.array_equal(keys.astype(np.uint64), O.pack_keys(ref, h[ok], depth).astype(np.uint64))
+    # sort, then LCP / verification / materialisation of the sorted order
+    got = h.copy()
+    _, lcp = sort_with_lcp(arena, got)
+    order = sorted(range(len(strs)), key=lambda i: strs[i])
+    want_sorted = [strs[i] for i in order]
+    assert [strs[int(np.searchsorted(want_h, x))] for x in got] == want_sorted
+    if h.size > 1:
+        assert np.array_equal(np.asarray(adjacent_lcps(arena, got)), lcp)
+        assert np.array_equal(lcp, O.adjacent_lcps(ref, got))
+    assert first_unsorted(arena, got) == -1
+    assert verify_sorted_permutation(arena, h, got).ok
+    if h.size > 2 and want_sorted[0] != want_sorted[-1]:
+        bad = got[::-1].copy()
+        assert first_unsorted(arena, bad) >= 0
+        assert not verify_sorted_permutation(arena, h, bad).ok
+    out, oh = materialize(arena, got)
+    oh = oh.cpu().numpy()
+    blob = out.data.tobytes()
+    assert [blob[a:blob.index(0, a)] for a in oh] == want_sorted
