@@ -1020,6 +1020,13 @@ static int sort_impl(const uint8_t* d_arena, uint64_t arena_len, int64_t* d_hand
     }
     A.pos = indexed ? reinterpret_cast<int64_t*>(ws + L.pos) : nullptr;
     A.k2_cap = n > c.narrow_max;  // the key2 arrays exist (make_layout)
+    {
+        int dev = 0, sms = 0;
+        S5_CUDA(cudaGetDevice(&dev));
+        S5_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        A.sm_count = static_cast<uint32_t>(sms);
+        if (const char* e = getenv("S5_SM_ROUND")) A.sm_count = static_cast<uint32_t>(atoi(e));  // tuning
+    }
     A.out = d_handles;
     A.lcp = d_lcp;
     A.hint_list = reinterpret_cast<uint2*>(ws + L.hints);

@@ -96,6 +96,7 @@ struct SortArgs {
     // arena -- every other level of a shared-prefix chain without a random
     // fetch.  k2_cap: the arrays exist (n > narrow_max).
     uint32_t k2_cap;
+    uint32_t sm_count;  // SMs of the device (wide_geom rounds a huge segment's CTAs to whole waves)
     // Arenas of >= 4 GiB (the reference's handles are int64 offsets,
     // strings.py:3-7): the u32 offset arrays hold each string's index in the
     // caller's array and `pos` (a copy of the handles, filled by level 0)
@@ -1880,6 +1881,10 @@ __device__ __forceinline__ WideGeom wide_geom(const Seg& s, const SortArgs& A) {
     uint32_t cmax = kWideFrontier / g.k;
     cmax = cmax < 1 ? 1 : (cmax > kWideCtasMax ? kWideCtasMax : cmax);
     g.C = c < 1 ? 1 : (c > cmax ? cmax : c);
+    // a segment that fills the machine on its own (the root): whole waves of
+    // CTAs -- 512 equal chunks on 148 SMs left the count's second wave (3 CTAs
+    // per SM resident) and the scatter's fourth (1 per SM) mostly empty
+    if (A.sm_count && g.C >= A.sm_count) g.C -= g.C % A.sm_count;
     return g;
 }
 
