@@ -40,7 +40,7 @@ enum {
     S5_E_WORKSPACE = -3, /* workspace too small                                        */
     S5_E_RANGE = -4,     /* handle outside the arena / n >= 2^31                        */
     S5_E_INTERNAL = -5,  /* internal capacity exceeded (bug)                           */
-    S5_E_NCCL = -6       /* NCCL error (multi-GPU entry points)                        */
+    S5_E_NCCL = -6       /* reserved: no entry point of this library calls NCCL         */
 };
 
 /* SampleSortConfig (samplesort.py:37-45) plus the GPU tiering knobs.
@@ -188,6 +188,34 @@ int s5_download(const int64_t *d_handles, uint64_t n, const int64_t *d_lcp, uint
 int s5_partition(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_handles,
                  uint64_t n, const int64_t *d_splitters, uint32_t nsplit, int64_t *d_out,
                  uint64_t *h_counts, void *stream);
+
+/* parallel_sample_sort(arena, handles, workers) with workers = GPUs of this
+ * process (samplesort.py:437-444; the p-way split of the fully parallel
+ * step, :369-434).  Shard g (shard_n[g]
+ * int64 handles on devices[g], left untouched) and a replica of the padded
+ * arena d_arenas[g] live on devices[g]; a device may be listed more than
+ * once.  The library draws 64 * n_gpus samples per shard, sorts them on
+ * devices[0], picks n_gpus - 1 splitter strings in (string, handle) order,
+ * groups every shard by destination (s5_partition), moves group (g -> d)
+ * into d_out_handles[d] with peer copies (u32 offsets for arenas below
+ * 4 GiB) and sorts slice d in place there (s5_sort).  On return slice d
+ * holds out_counts[d] sorted handles and the slices in device-list order are
+ * the global order; d_out_lcp (NULL, or one buffer per slice) receives slice
+ * d's out_counts[d] - 1 LCPs followed by the LCP to the first string of the
+ * next non-empty slice, so the concatenation is _adjacent_lcps of the whole
+ * output (strings.py:99-102).  out_capacity[d] = elements d_out_handles[d]
+ * (and d_out_lcp[d]) can hold -- the sum of shard_n always suffices;
+ * S5_E_WORKSPACE when a slice outgrows it.  Exchange by cudaMemcpyPeer over
+ * NVLink instead of the NCCL communicators the survey's sketch names (one
+ * process owns every device, so no communicator is needed).  Blocking;
+ * uses the devices' default streams; one call at a time per process.
+ * stats: the largest slice's sort statistics, launches and key_fetches
+ * summed over the slices, ms_total = host wall time of the call. */
+int s5_sort_multi(int n_gpus, const int *devices, const uint8_t *const *d_arenas,
+                  uint64_t arena_len, int64_t *const *d_handle_shards, const uint64_t *shard_n,
+                  int64_t *const *d_out_handles, int64_t *const *d_out_lcp,
+                  const uint64_t *out_capacity, uint64_t *out_counts, const s5_config *cfg,
+                  s5_stats *stats);
 
 /* load_lines (harness.py:72-95) on the device: d_raw[len] (one string per
  * line) -> d_arena (newlines become terminators; a terminator is appended

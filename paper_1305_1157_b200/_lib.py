@@ -118,6 +118,8 @@ SIGNATURES = {
     "s5_adjacent_lcp": (C.c_int, [_vp, _u64, _vp, _u64, _vp, _vp]),
     "s5_first_unsorted": (C.c_int, [_vp, _u64, _vp, _u64, _vp, _vp]),
     "s5_partition": (C.c_int, [_vp, _u64, _vp, _u64, _vp, C.c_uint32, _vp, _vp, _vp]),
+    "s5_sort_multi": (C.c_int, [C.c_int, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp,
+                                C.POINTER(S5Config), C.POINTER(S5Stats)]),
     "s5_ingest_lines": (C.c_int, [_vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "s5_release_caches": (C.c_int, []),
     "s5_upload_handles": (C.c_int, [_vp, _u64, _u64, _vp, _vp]),

@@ -1785,9 +1785,12 @@ int s5_host_copy_pieces(uint8_t* dst, const int64_t* dst_start, const int64_t* s
     return 0;
 }
 
+static void (*g_multi_release)() = nullptr;  // set by s5_multi.cuh
+
 int s5_release_caches(void) {
     int cur = 0;
     cudaGetDevice(&cur);
+    if (g_multi_release) g_multi_release();
     std::lock_guard<std::mutex> g(registry_mutex());
     for (auto& kv : registry<HostPath>()) {
         HostPath& H = kv.second;
@@ -1845,3 +1848,5 @@ int s5_release_caches(void) {
 }
 
 }  // extern "C"
+
+#include "s5_multi.cuh"

@@ -150,3 +150,51 @@ def multi_gpu_sort(arena, handles, devices, cfg=None, lcp_out=None, oversample: 
     finally:
         pool.shutdown(wait=True)
     return handles
+
+
+def sort_multi_device(arena, shards, devices, cfg=None, want_lcp: bool = True, counters=None):
+    """``s5_sort_multi`` (include/s5.h): the same split done by the library
+    itself from C -- one call, device shards in, sorted device slices out.
+
+    ``shards[g]`` is a CUDA int64 tensor of handles on ``devices[g]`` (left
+    untouched).  Returns ``(slices, lcps)``: ``slices[d]`` the sorted handles
+    of slice d on ``devices[d]``; the concatenation in device order is the
+    global order and that of ``lcps`` its LCP array (``None`` without
+    ``want_lcp``)."""
+    import ctypes as C
+
+    import torch
+    from . import _lib
+    from .samplesort import SampleSortConfig
+    G = len(devices)
+    if G != len(shards):
+        raise ValueError("one shard per device")
+    devs = [torch.device("cuda", int(d)) for d in devices]
+    total = sum(int(s.numel()) for s in shards)
+    arenas = [arena.device(d) for d in devs]
+    shards = [s.contiguous() for s in shards]
+    outs = [torch.empty(max(total, 1), dtype=torch.int64, device=d) for d in devs]
+    lcps = [torch.empty(max(total, 1), dtype=torch.int64, device=d) for d in devs] if want_lcp else None
+    for d in devs:
+        torch.cuda.synchronize(d)
+    ptrs = lambda ts: (C.c_void_p * G)(*[t.data_ptr() for t in ts])
+    dev_ids = (C.c_int * G)(*[d.index for d in devs])
+    ns = (C.c_uint64 * G)(*[int(s.numel()) for s in shards])
+    cap = (C.c_uint64 * G)(*[max(total, 1)] * G)
+    counts = (C.c_uint64 * G)()
+    ccfg = (cfg or SampleSortConfig()).to_c()
+    st = _lib.S5Stats()
+    rc = _lib.lib().s5_sort_multi(G, dev_ids, ptrs(arenas), arena.size, ptrs(shards), ns, ptrs(outs),
+                                  ptrs(lcps) if want_lcp else None, cap, counts, C.byref(ccfg),
+                                  C.byref(st))
+    _lib.check(rc, "s5_sort_multi")
+    if counters is not None:
+        counters.add("gpus", G)
+        counters.add("parallel_steps", int(st.levels))
+        counters.add("fetches", int(st.key_fetches))
+    sizes = [int(c) for c in counts]
+    last = max((d for d in range(G) if sizes[d]), default=-1)
+    slices = [outs[d][:sizes[d]] for d in range(G)]
+    if not want_lcp:
+        return slices, None
+    return slices, [lcps[d][:max(sizes[d] - (1 if d == last else 0), 0)] for d in range(G)]

@@ -63,6 +63,65 @@ def test_workers_over_devices_matches_oracle(devices, config, n):
     assert np.array_equal(lcp, want_lcp)
 
 
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0], [0] * 8])
+@pytest.mark.parametrize("config,n", [(1, None), (2, 1 << 17), (3, 1 << 16), (4, 1 << 15),
+                                      (5, 1 << 16)])
+def test_s5_sort_multi_matches_oracle(devices, config, n):
+    """The C-ABI multi-GPU entry (s5_sort_multi): slices in device order are
+    the oracle's order, their LCP buffers its LCP array."""
+    import torch
+    from paper_1305_1157_b200.multi import sort_multi_device
+    arena, h0 = datasets.generate(config, n)
+    want, want_lcp = _want(arena, h0)
+    G = len(devices)
+    bounds = [(h0.size * g // G, h0.size * (g + 1) // G) for g in range(G)]
+    shards = [torch.from_numpy(h0[a:b].copy()).cuda() for a, b in bounds]
+    keep = [s.clone() for s in shards]
+    slices, lcps = sort_multi_device(arena, shards, devices)
+    for s, k in zip(shards, keep):
+        assert torch.equal(s, k)  # inputs untouched
+    h = torch.cat(slices).cpu().numpy()
+    lcp = torch.cat(lcps).cpu().numpy()
+    assert np.array_equal(np.sort(h), np.sort(h0))
+    assert O.contents_equal(arena, h, want)
+    assert np.array_equal(lcp, want_lcp)
+
+
+def test_s5_sort_multi_ragged_empty_and_duplicates():
+    """Empty shards, a one-string shard, heavy duplicates (identical strings
+    must split consistently by handle) and a too-small output buffer."""
+    import ctypes as C
+
+    import torch
+    from paper_1305_1157_b200 import _lib, arena_from_strings
+    from paper_1305_1157_b200.multi import sort_multi_device
+    strs = [b"same"] * 30000 + [b"dup-%d" % (i % 7) for i in range(20000)] + [b"", b"z"]
+    arena, h0 = arena_from_strings(strs)
+    rng = np.random.default_rng(5)
+    h0 = h0[rng.permutation(h0.size)]
+    want, want_lcp = _want(arena, h0)
+    cuts = [0, 0, 1, 40000, 40000, h0.size]
+    shards = [torch.from_numpy(h0[a:b].copy()).cuda() for a, b in zip(cuts[:-1], cuts[1:])]
+    slices, lcps = sort_multi_device(arena, shards, [0] * 5)
+    h = torch.cat(slices).cpu().numpy()
+    assert np.array_equal(np.sort(h), np.sort(h0))
+    assert O.contents_equal(arena, h, want)
+    assert np.array_equal(torch.cat(lcps).cpu().numpy(), want_lcp)
+    # nothing to sort
+    slices, lcps = sort_multi_device(arena, [shards[0], shards[0]], [0, 0])
+    assert all(s.numel() == 0 for s in slices)
+    # capacity too small -> S5_E_WORKSPACE, message names the slice
+    G = 2
+    d_ar = arena.device(torch.device("cuda", 0))
+    sh = [shards[3], shards[5 - 1]]
+    outs = [torch.empty(8, dtype=torch.int64, device="cuda") for _ in range(G)]
+    P = lambda ts: (C.c_void_p * G)(*[t.data_ptr() for t in ts])
+    rc = _lib.lib().s5_sort_multi(G, (C.c_int * G)(0, 0), P([d_ar, d_ar]), arena.size, P(sh),
+                                  (C.c_uint64 * G)(*[s.numel() for s in sh]), P(outs), None,
+                                  (C.c_uint64 * G)(8, 8), (C.c_uint64 * G)(), None, None)
+    assert rc == -3 and b"slice" in _lib.lib().s5_last_error()
+
+
 def test_workers_device_tensor_and_duplicates():
     import torch
     from paper_1305_1157_b200 import arena_from_strings
