@@ -11,7 +11,8 @@
 
 namespace {
 
-constexpr uint32_t kMultiOversample = 64;  // samples per shard and destination
+constexpr uint32_t kMultiOversample = 64;   // samples per shard and destination ...
+constexpr uint32_t kMultiMinSamples = 2048;  // ... and at least this many per shard (slice balance)
 
 __device__ __forceinline__ uint64_t multi_mix(uint64_t x) {
     x += 0x9E3779B97F4A7C15ull;
@@ -134,8 +135,39 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
     }
     if (stats) *stats = s5_stats{};
     if (total == 0) return 0;
+    if (G == 1) {  // one device: nothing to split or exchange
+        const uint64_t n = shard_n[0];
+        if (n > out_capacity[0])
+            return fail(S5_E_WORKSPACE, "slice 0 holds %llu strings, capacity %llu",
+                        (unsigned long long)n, (unsigned long long)out_capacity[0]);
+        S5_CUDA(cudaSetDevice(devices[0]));
+        MultiSlot& X = M.slot[0];
+        if (X.dev != devices[0]) {
+            if (X.dev >= 0) cudaSetDevice(X.dev);
+            if (X.d) cudaFree(X.d);
+            if (X.ws) cudaFree(X.ws);
+            S5_CUDA(cudaSetDevice(devices[0]));
+            X = MultiSlot{};
+            X.dev = devices[0];
+        }
+        S5_CUDA(cudaMemcpyAsync(d_out_handles[0], d_handle_shards[0], n * 8, cudaMemcpyDeviceToDevice,
+                                nullptr));
+        if (n > 1) {
+            const uint64_t wsb = s5_workspace_bytes(n, arena_len, cfg);
+            if (int r = multi_reserve(&X.ws, &X.ws_bytes, wsb)) return r;
+            if (int r = s5_sort(d_arenas[0], arena_len, d_out_handles[0], n, 0,
+                                d_out_lcp ? d_out_lcp[0] : nullptr, cfg, X.ws, X.ws_bytes, nullptr, stats))
+                return r;
+        }
+        S5_CUDA(cudaDeviceSynchronize());
+        out_counts[0] = n;
+        if (stats)
+            stats->ms_total =
+                std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        return 0;
+    }
     const bool narrow = arena_len < (1ull << 32);  // u32 payload; index-mode arenas send int64
-    const uint32_t S = kMultiOversample * uint32_t(G);  // samples per shard
+    const uint32_t S = std::max(kMultiOversample * uint32_t(G), kMultiMinSamples);  // samples per shard
     const uint32_t nsplit = uint32_t(G) - 1;
     s5_config c = cfg ? *cfg : s5_config{};
     const uint64_t seed = c.seed ? c.seed : 1;
