@@ -194,7 +194,7 @@ int s5_partition(const uint8_t *d_arena, uint64_t arena_len, const int64_t *d_ha
  * step, :369-434).  Shard g (shard_n[g]
  * int64 handles on devices[g], left untouched) and a replica of the padded
  * arena d_arenas[g] live on devices[g]; a device may be listed more than
- * once.  The library draws 64 * n_gpus samples per shard, sorts them on
+ * once; n_gpus <= 64.  The library draws max(64 * n_gpus, 2048) samples per shard, sorts them on
  * devices[0], picks n_gpus - 1 splitter strings in (string, handle) order,
  * groups every shard by destination (s5_partition), moves group (g -> d)
  * into d_out_handles[d] with peer copies (u32 offsets for arenas below

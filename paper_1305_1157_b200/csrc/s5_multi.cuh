@@ -11,6 +11,7 @@
 
 namespace {
 
+constexpr uint32_t kMultiMaxGpus = 64;      // one host thread per shard
 constexpr uint32_t kMultiOversample = 64;   // samples per shard and destination ...
 constexpr uint32_t kMultiMinSamples = 2048;  // ... and at least this many per shard (slice balance)
 
@@ -52,7 +53,7 @@ struct MultiSlot {  // device scratch of shard g, kept between calls
 };
 struct MultiState {
     std::mutex mu;  // one s5_sort_multi at a time
-    MultiSlot slot[kPartMaxRanks];
+    MultiSlot slot[kMultiMaxGpus];
 };
 MultiState& multi_state() {
     static MultiState s;
@@ -111,8 +112,8 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
                              const uint64_t* shard_n, int64_t* const* d_out_handles,
                              int64_t* const* d_out_lcp, const uint64_t* out_capacity,
                              uint64_t* out_counts, const s5_config* cfg, s5_stats* stats) {
-    if (n_gpus < 1 || uint32_t(n_gpus) > kPartMaxRanks)
-        return fail(S5_E_INVALID, "n_gpus must be in 1..%u", kPartMaxRanks);
+    if (n_gpus < 1 || uint32_t(n_gpus) > kMultiMaxGpus)
+        return fail(S5_E_INVALID, "n_gpus must be in 1..%u", kMultiMaxGpus);
     if (!devices || !d_arenas || !d_handle_shards || !shard_n || !d_out_handles || !out_capacity ||
         !out_counts)
         return fail(S5_E_INVALID, "null argument");
@@ -174,8 +175,8 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
 
     // Scratch per shard: [samples S] [splitters G-1] [pair 2] [grouped n_g] [payload n_g]
     auto off_spl = [&](void* d) { return static_cast<int64_t*>(d) + S; };
-    auto off_pair = [&](void* d) { return static_cast<int64_t*>(d) + S + kPartMaxRanks; };
-    auto off_grp = [&](void* d) { return static_cast<int64_t*>(d) + S + kPartMaxRanks + 2; };
+    auto off_pair = [&](void* d) { return static_cast<int64_t*>(d) + S + kMultiMaxGpus; };
+    auto off_grp = [&](void* d) { return static_cast<int64_t*>(d) + S + kMultiMaxGpus + 2; };
     for (int g = 0; g < G; ++g) {
         MultiSlot& X = M.slot[g];
         S5_CUDA(cudaSetDevice(devices[g]));
@@ -189,7 +190,7 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
             X = MultiSlot{};
             X.dev = devices[g];
         }
-        const uint64_t need = (uint64_t(S) + kPartMaxRanks + 2 + 2 * shard_n[g]) * 8 + 64;
+        const uint64_t need = (uint64_t(S) + kMultiMaxGpus + 2 + 2 * shard_n[g]) * 8 + 64;
         if (int rc = multi_reserve(&X.d, &X.bytes, need)) return rc;
     }
 

@@ -49,6 +49,20 @@ def test_trivial_sizes_are_noops_without_gpu():
     assert L.s5_sort(None, 0, None, 0, 0, None, C.byref(cfg), None, 0, None, None) == 0
 
 
+def test_sort_multi_argument_validation_without_gpu():
+    """s5_sort_multi rejects bad device counts and null tables before it
+    touches a device (include/s5.h)."""
+    L = _lib.lib()
+    one = (C.c_uint64 * 1)(0)
+    dev = (C.c_int * 1)(0)
+    ptr = (C.c_void_p * 1)(None)
+    assert L.s5_sort_multi(0, dev, ptr, 0, ptr, one, ptr, None, one, one, None, None) == -1
+    assert b"n_gpus" in L.s5_last_error()
+    assert L.s5_sort_multi(65, dev, ptr, 0, ptr, one, ptr, None, one, one, None, None) == -1
+    assert L.s5_sort_multi(1, dev, ptr, 0, ptr, None, ptr, None, one, one, None, None) == -1
+    assert b"null" in L.s5_last_error()
+
+
 def test_markov_helper_matches_numpy_searchsorted():
     import numpy as np
     from paper_1305_1157_b200 import _native
