@@ -6,11 +6,12 @@ them, :369-434).  Here it is the number of GPUs: the same sample-sort
 partitioning as ``distributed.distributed_sample_sort``,
 driven by one host thread per device instead of one process per GPU, and
 with the exchange done as direct device-to-device copies (NVLink peer
-copies through ``Tensor.copy_``) instead of NCCL:
+copies) instead of NCCL.  Steps 2-5 are one C-ABI call, ``s5_sort_multi``
+(csrc/s5_multi.cuh); this module moves the caller's buffers in and out:
 
 1. the handles are split into G contiguous shards, one per device (host
    arrays cross PCIe as u32 offsets, ``s5_upload_handles``);
-2. every device draws ``oversample * G`` sample handles; the samples are
+2. every device draws ``max(64 * G, 2048)`` sample handles; the samples are
    gathered on the first device, sorted there by (string, handle) and the
    G-1 splitter strings sent to every device;
 3. every device groups its shard by destination (``s5_partition``);
@@ -33,7 +34,7 @@ from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
-from .distributed import GpuBackend, _pick_splitters
+from .distributed import GpuBackend
 
 
 def _on(dev, fn, *a):
@@ -42,8 +43,7 @@ def _on(dev, fn, *a):
         return fn(*a)
 
 
-def multi_gpu_sort(arena, handles, devices, cfg=None, lcp_out=None, oversample: int = 64,
-                   seed: int = 1, counters=None):
+def multi_gpu_sort(arena, handles, devices, cfg=None, lcp_out=None, counters=None):
     """Sort ``handles`` (numpy int64 or a CUDA int64 tensor) in place over the
     GPUs ``devices``; the LCP array goes to ``lcp_out`` (same kind of
     buffer, n-1 entries) when given.  Returns ``handles``."""
@@ -69,66 +69,13 @@ def multi_gpu_sort(arena, handles, devices, cfg=None, lcp_out=None, oversample: 
             return bes[g].upload(np.ascontiguousarray(handles[lo:hi]))
         shards = par(load)
 
-        # 2. samples -> first device -> splitters -> every device
-        s = oversample * G
-
-        def sample(g):
-            h = shards[g]
-            if not h.numel():
-                return torch.full((s,), -1, dtype=torch.int64, device=devs[g])
-            gen = torch.Generator(device=devs[g]).manual_seed(seed * 1_000_003 + g)
-            return h[torch.randint(0, h.numel(), (s,), generator=gen, device=devs[g])]
-        samp = par(sample)
-        with torch.cuda.device(devs[0]):
-            allsamp = torch.cat([x.to(devs[0]) for x in samp])
-            top = allsamp.max().clamp(min=0)
-            allsamp = torch.where(allsamp >= 0, allsamp, top)
-            splitters = _pick_splitters(bes[0], allsamp, G)
-        spl = [splitters.to(d) for d in devs]
-
-        # 3. group by destination
-        def part(g):
-            return bes[g].partition(shards[g], spl[g])
-        parts = par(part)
-        send32 = [_on(devs[g], lambda t: t.to(torch.int32), parts[g][0]) for g in range(G)]
-        counts = [p[1] for p in parts]  # counts[src][dst]
-        sizes = [sum(counts[g][d] for g in range(G)) for d in range(G)]
-
-        # 4. exchange (peer copies into each destination's buffer)
-        def exchange(d):
-            buf = torch.empty(sizes[d], dtype=torch.int64, device=devs[d])
-            b32 = buf.view(torch.int32)
-            at = 0
-            for g in range(G):
-                c = counts[g][d]
-                if c:
-                    lo = sum(counts[g][:d])
-                    b32[at:at + c].copy_(send32[g][lo:lo + c])
-                at += c
-            torch.cuda.synchronize(devs[d])
-            return buf
-        recv = par(exchange)
-        for g in range(G):
-            torch.cuda.synchronize(devs[g])
-
-        # 5. local sorts (the library releases the GIL: the devices overlap)
-        def local(d):
-            return bes[d].sort_u32(recv[d], sizes[d])
-        res = par(local)
-        out_h = [r[0] for r in res]
-        out_l = [r[1] for r in res]
-        for d in range(G):  # boundary LCP on the left device
-            nxt = next((r for r in range(d + 1, G) if sizes[r]), None)
-            if sizes[d] and nxt is not None:
-                pair = torch.cat([out_h[d][-1:], out_h[nxt][:1].to(devs[d])])
-                out_l[d] = torch.cat([out_l[d], _on(devs[d], bes[d].lcp_pair, pair)])
-        if counters is not None:
-            counters.add("gpus", G)
-            for be in bes:
-                st = getattr(be, "last_stats", None)
-                if st is not None:
-                    counters.add("parallel_steps", int(st.levels))
-                    counters.add("fetches", int(st.key_fetches))
+        # 2.-5. samples, splitters, partition, exchange, local sorts and the
+        # boundary LCPs: one library call (s5_sort_multi, include/s5.h)
+        out_h, out_l = sort_multi_device(arena, shards, [d.index for d in devs], cfg,
+                                         want_lcp=lcp_out is not None, counters=counters)
+        sizes = [int(t.numel()) for t in out_h]
+        if out_l is None:
+            out_l = [t[:0] for t in out_h]
 
         # 6. the slices back into the caller's buffers, in global order
         offs = [sum(sizes[:d]) for d in range(G)]
