@@ -54,6 +54,7 @@ struct MultiSlot {  // device scratch of shard g, kept between calls
 struct MultiState {
     std::mutex mu;  // one s5_sort_multi at a time
     MultiSlot slot[kMultiMaxGpus];
+    MultiSlot samp;  // the sample sort's scratch on devices[0] (d only)
 };
 MultiState& multi_state() {
     static MultiState s;
@@ -78,6 +79,11 @@ void multi_release() {
         if (X.ws) cudaFree(X.ws);
         X = MultiSlot{};
     }
+    if (M.samp.d) {
+        cudaSetDevice(M.samp.dev);
+        cudaFree(M.samp.d);
+    }
+    M.samp = MultiSlot{};
 }
 const bool g_multi_release_set = (g_multi_release = multi_release, true);
 
@@ -128,6 +134,12 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
     MultiState& M = multi_state();
     std::lock_guard<std::mutex> lock(M.mu);
 
+    const bool trace = getenv("S5_MULTI_TRACE") != nullptr;  // phase wall times on stderr
+    auto mark = [&](const char* what) {
+        if (trace)
+            fprintf(stderr, "s5_sort_multi %-10s %8.3f ms\n", what,
+                    std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    };
     uint64_t total = 0;
     for (int g = 0; g < G; ++g) {
         if (shard_n[g] >= (1ull << 31)) return fail(S5_E_RANGE, "shard %d: n must be < 2^31", g);
@@ -194,6 +206,28 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
         if (int rc = multi_reserve(&X.d, &X.bytes, need)) return rc;
     }
 
+    // direct NVLink copies between distinct devices (otherwise cudaMemcpyPeer
+    // stages through the host); already-enabled pairs are fine
+    for (int a = 0; a < G; ++a)
+        for (int b = 0; b < G; ++b) {
+            if (devices[a] == devices[b]) continue;
+            bool seen = false;  // each ordered pair once
+            for (int k = 0; k < b && !seen; ++k) seen = devices[k] == devices[b];
+            for (int k = 0; k < a && !seen; ++k) seen = devices[k] == devices[a];
+            if (seen) continue;
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, devices[a], devices[b]) != cudaSuccess || !can) {
+                cudaGetLastError();
+                continue;
+            }
+            S5_CUDA(cudaSetDevice(devices[a]));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                return fail(S5_E_CUDA, "cudaDeviceEnablePeerAccess(%d -> %d): %s", devices[a],
+                            devices[b], cudaGetErrorString(e));
+            cudaGetLastError();
+        }
+
     // 1. samples of every non-empty shard -> host -> first device
     std::vector<int64_t> samp;
     samp.reserve(uint64_t(S) * G);
@@ -208,18 +242,27 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
         samp.resize(at + S);
         S5_CUDA(cudaMemcpy(samp.data() + at, d_s, S * 8ull, cudaMemcpyDeviceToHost));
     }
+    mark("samples");
     // 2. splitters: G-1 evenly spaced strings of the (string, handle)-sorted sample
     std::vector<int64_t> spl(nsplit);
     if (nsplit) {
         const uint32_t m = static_cast<uint32_t>(samp.size());
         S5_CUDA(cudaSetDevice(devices[0]));
-        void* d_tmp = nullptr;  // [sample m] [lcp m] [same m] [workspace]
+        // [sample m] [lcp m] [same m] [workspace], kept between calls
         const uint64_t wsb = s5_workspace_bytes(m, arena_len, &c);
-        S5_CUDA(cudaMalloc(&d_tmp, align_up(m * 8ull) * 2 + align_up(m) + wsb + 256));
-        struct Free {
-            void* p;
-            ~Free() { cudaFree(p); }
-        } free_tmp{d_tmp};
+        MultiSlot& T = M.samp;
+        if (T.dev != devices[0]) {
+            if (T.d) {
+                cudaSetDevice(T.dev);
+                cudaFree(T.d);
+                S5_CUDA(cudaSetDevice(devices[0]));
+            }
+            T = MultiSlot{};
+            T.dev = devices[0];
+        }
+        if (int r = multi_reserve(&T.d, &T.bytes, align_up(m * 8ull) * 2 + align_up(m) + wsb + 256))
+            return r;
+        void* d_tmp = T.d;
         int64_t* d_s = static_cast<int64_t*>(d_tmp);
         int64_t* d_l = reinterpret_cast<int64_t*>(static_cast<char*>(d_tmp) + align_up(m * 8ull));
         uint8_t* d_same = reinterpret_cast<uint8_t*>(static_cast<char*>(d_tmp) + 2 * align_up(m * 8ull));
@@ -244,6 +287,7 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
             spl[j] = samp[std::min<uint64_t>(uint64_t(j + 1) * m / G, m - 1)];
     }
 
+    mark("splitters");
     // 3. group every shard by destination; 4. payload ready for the peers
     std::vector<uint64_t> counts(uint64_t(G) * G, 0);  // counts[src * G + dst]
     int rc = multi_par(G, devices, [&](int g) -> int {
@@ -275,6 +319,7 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
         if (sizes[d] >= (1ull << 31)) return fail(S5_E_RANGE, "slice %d: n must be < 2^31", d);
     }
 
+    mark("partition");
     // 5. exchange (peer copies into the destination's output buffer) and local sorts
     std::vector<s5_stats> st(stats ? G : 0);
     rc = multi_par(G, devices, [&](int d) -> int {
@@ -318,6 +363,7 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
     });
     if (rc) return rc;
 
+    mark("sorts");
     // 6. the LCP across each slice boundary, on the left device
     if (d_out_lcp) {
         for (int d = 0; d < G; ++d) {
@@ -338,6 +384,7 @@ extern "C" int s5_sort_multi(int n_gpus, const int* devices, const uint8_t* cons
             S5_CUDA(cudaDeviceSynchronize());
         }
     }
+    mark("boundaries");
     for (int d = 0; d < G; ++d) out_counts[d] = sizes[d];
     if (stats) {
         int big = 0;
