@@ -107,6 +107,10 @@ def test_s5_sort_multi_ragged_empty_and_duplicates():
     assert np.array_equal(np.sort(h), np.sort(h0))
     assert O.contents_equal(arena, h, want)
     assert np.array_equal(torch.cat(lcps).cpu().numpy(), want_lcp)
+    # the library's cached multi-GPU scratch can be released between calls
+    assert _lib.lib().s5_release_caches() == 0
+    slices2, _ = sort_multi_device(arena, shards, [0] * 5, want_lcp=False)
+    assert O.contents_equal(arena, torch.cat(slices2).cpu().numpy(), want)
     # nothing to sort
     slices, lcps = sort_multi_device(arena, [shards[0], shards[0]], [0, 0])
     assert all(s.numel() == 0 for s in slices)
