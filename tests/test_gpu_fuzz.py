@@ -189,3 +189,30 @@ def test_fuzz_auxiliary_surfaces(seed):
     oh = oh.cpu().numpy()
     blob = out.data.tobytes()
     assert [blob[a:blob.index(0, a)] for a in oh] == want_sorted
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("S5_FUZZ_NATIVE_MULTI_CASES", "40"))))
+def test_fuzz_s5_sort_multi_against_oracle(seed):
+    """s5_sort_multi (the C-ABI multi-GPU entry) with ragged shard cuts --
+    empty and one-string shards included -- over a repeated device list."""
+    import torch
+    from paper_1305_1157_b200.multi import sort_multi_device
+    rng = np.random.default_rng(14000 + seed)
+    strs = _strings(rng)
+    cfg = _config(rng)
+    arena, h0 = arena_from_strings(strs)
+    want = h0.copy()
+    O.parallel_sample_sort(arena, want, 4)
+    want_lcp = O.adjacent_lcps(arena, want)
+    G = int(rng.choice([1, 2, 3, 4, 7, 9]))
+    cuts = np.sort(rng.integers(0, h0.size + 1, G - 1)) if rng.random() < 0.7 else \
+        np.array([h0.size * g // G for g in range(1, G)])
+    cuts = [0] + [int(c) for c in cuts] + [int(h0.size)]
+    shards = [torch.from_numpy(h0[a:b].copy()).cuda() for a, b in zip(cuts[:-1], cuts[1:])]
+    slices, lcps = sort_multi_device(arena, shards, [0] * G, cfg)
+    got = torch.cat(slices).cpu().numpy()
+    lcp = torch.cat(lcps).cpu().numpy()
+    tag = f"seed {seed} G={G} cuts={cuts} n={len(strs)} cfg={cfg}"
+    assert np.array_equal(np.sort(got), np.sort(h0)), tag
+    assert O.contents_equal(arena, got, want), tag
+    assert np.array_equal(lcp, want_lcp), tag
