@@ -87,28 +87,71 @@ void multi_release() {
 }
 const bool g_multi_release_set = (g_multi_release = multi_release, true);
 
-// Runs fn(g) on one host thread per shard; the first failure's code and
-// message are re-raised on the calling thread.
+// One persistent host thread per shard slot (a thread keeps its device's
+// per-thread library state -- the mapped control block of s5_sort -- between
+// calls instead of allocating it per call).  run(G, devices, fn) executes
+// fn(g) on thread g with devices[g] current; the first failure's code and
+// message are re-raised on the calling thread.  Threads are detached and the
+// pool is never destroyed (no join at process exit).
+struct MultiPool {
+    std::mutex mu;
+    std::condition_variable go, done;
+    std::function<int(int)> job;
+    const int* devices = nullptr;
+    uint64_t gen = 0;
+    int G = 0, left = 0, nthreads = 0;
+    std::vector<int> rc;
+    std::vector<std::string> msg;
+
+    void worker(int g, uint64_t seen) {
+        for (;;) {
+            std::unique_lock<std::mutex> lk(mu);
+            go.wait(lk, [&] { return gen != seen; });
+            seen = gen;
+            if (g >= G) continue;  // not part of this job
+            const std::function<int(int)> f = job;
+            const int dev = devices[g];
+            lk.unlock();
+            int r = 0;
+            std::string m;
+            if (cudaSetDevice(dev) != cudaSuccess) {
+                r = S5_E_CUDA;
+                m = "cudaSetDevice failed";
+            } else {
+                r = f(g);
+                if (r) m = s5_last_error();
+            }
+            lk.lock();
+            rc[g] = r;
+            msg[g] = m;
+            if (--left == 0) done.notify_all();
+        }
+    }
+    int run(int G_, const int* devs, std::function<int(int)> f) {
+        std::unique_lock<std::mutex> lk(mu);
+        for (; nthreads < G_; ++nthreads) std::thread(&MultiPool::worker, this, nthreads, gen).detach();
+        G = G_;
+        devices = devs;
+        job = std::move(f);
+        rc.assign(G_, 0);
+        msg.assign(G_, std::string());
+        left = G_;
+        ++gen;
+        go.notify_all();
+        done.wait(lk, [&] { return left == 0; });
+        job = nullptr;
+        for (int g = 0; g < G_; ++g)
+            if (rc[g]) return fail(rc[g], "shard %d (device %d): %s", g, devs[g], msg[g].c_str());
+        return 0;
+    }
+};
+MultiPool& multi_pool() {
+    static MultiPool* p = new MultiPool;
+    return *p;
+}
 template <class F>
 int multi_par(int G, const int* devices, F fn) {
-    std::vector<int> rc(G, 0);
-    std::vector<std::string> msg(G);
-    std::vector<std::thread> th;
-    th.reserve(G);
-    for (int g = 0; g < G; ++g)
-        th.emplace_back([&, g] {
-            if (cudaSetDevice(devices[g]) != cudaSuccess) {
-                rc[g] = S5_E_CUDA;
-                msg[g] = "cudaSetDevice failed";
-                return;
-            }
-            rc[g] = fn(g);
-            if (rc[g]) msg[g] = s5_last_error();
-        });
-    for (auto& t : th) t.join();
-    for (int g = 0; g < G; ++g)
-        if (rc[g]) return fail(rc[g], "shard %d (device %d): %s", g, devices[g], msg[g].c_str());
-    return 0;
+    return multi_pool().run(G, devices, std::function<int(int)>(fn));
 }
 
 }  // namespace
